@@ -1,0 +1,38 @@
+#!/usr/bin/env bash
+# Build the reference planner (maniplan) into oracle/_ref/ as compiled
+# extension modules, from its own sources under /root/reference (read-only;
+# scratch in a temp dir).  TEST / BASELINE INFRASTRUCTURE ONLY: the product
+# never imports it.  The kernel backend (_compiled.pyx) gets the reference's
+# own flags (pkg/setup.py:45-53); the pure-Python modules are cythonized as-is
+# so the package is importable on the GPU box, where /root/reference is absent.
+set -euo pipefail
+REF=${REF:-/root/reference/pkg/src/maniplan}
+HERE="$(cd "$(dirname "${BASH_SOURCE[0]}")" && pwd)"
+OUT="$HERE/_ref"
+PY=${PYTHON:-python3}
+[ -d "$REF" ] || { echo "reference sources not found at $REF" >&2; exit 1; }
+TMP=$(mktemp -d /tmp/cprrtc_refbuild.XXXXXX)
+trap 'rm -rf "$TMP"' EXIT
+mkdir -p "$TMP/src"
+cp -r "$REF" "$TMP/src/maniplan"
+find "$TMP/src" -name '__pycache__' -prune -exec rm -rf {} +
+cat > "$TMP/setup_ref.py" <<'PYEOF'
+import glob, os
+from setuptools import setup, Extension
+from Cython.Build import cythonize
+flags = ["-O3", "-ffp-contract=off", "-fno-builtin-sin", "-fno-builtin-cos"]
+exts = [Extension("maniplan._kernels._compiled", ["src/maniplan/_kernels/_compiled.pyx"],
+                  extra_compile_args=flags)]
+for path in sorted(glob.glob("src/maniplan/**/*.py", recursive=True)):
+    mod = path[len("src/"):-3].replace(os.sep, ".")
+    exts.append(Extension(mod, [path], extra_compile_args=flags))
+setup(name="maniplan_ref", ext_modules=cythonize(exts, compiler_directives={
+    "language_level": "3", "boundscheck": False, "wraparound": False, "cdivision": True,
+    "binding": True}, quiet=True, nthreads=8), script_args=["build_ext", "--build-lib", "build_out", "--parallel", "8"])
+PYEOF
+( cd "$TMP" && "$PY" setup_ref.py > build.log 2>&1 ) || { tail -30 "$TMP/build.log"; exit 1; }
+rm -rf "$OUT"
+mkdir -p "$OUT"
+( cd "$TMP/build_out" && find maniplan -name '*.so' -print0 | while IFS= read -r -d '' f; do
+      mkdir -p "$OUT/$(dirname "$f")"; cp "$f" "$OUT/$f"; done )
+echo "reference built into $OUT"

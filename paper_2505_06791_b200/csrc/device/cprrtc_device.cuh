@@ -1,0 +1,1329 @@
+// cprrtc_device.cuh -- B200 (sm_100a) device code of the cpRRTC planner.
+//
+// Compiled at run time by NVRTC (csrc/runtime.cpp) after a generated prelude
+// that supplies the robot (unrolled FK `cp_fk`, limits, radii, self pairs; see
+// csrc/codegen.cpp) and the module configuration:
+//   CP_G       team width in lanes (16 or 32): one team = one extension
+//   CP_KIND    0 plane / 1 line position constraint     (compile-time)
+//   CP_ORIENT  1 if the EE orientation is locked         (compile-time)
+//   CP_NTHREADS threads per CTA of the persistent planner
+//
+// Execution model: a team of CP_G lanes of one warp
+// owns one tree extension at a time -- lane t holds waypoint t of the motion
+// (the paper's "one thread per waypoint").  Alg. 1's barriers
+// become __syncwarp on the team mask, stage 2's prefix scan a ballot, and the
+// paper's shared-memory collision flag a team vote taken every
+// CP_CHUNK primitive checks.  Obstacles are staged once per CTA in shared
+// memory; trees are SoA float arrays in HBM with atomic append.
+//
+// Every function cites the reference function it replaces
+// (maniplan/..., /root/reference/pkg/src/).
+
+#ifndef CP_G
+#error "CP_G must be defined by the runtime prelude"
+#endif
+
+#define CP_M ((CP_KIND == 0 ? 1 : 2) + (CP_ORIENT ? 3 : 0))
+#define CP_NP ((CP_N % 2) ? CP_N : (CP_N + 1))   // odd row pitch: no bank conflicts
+#define CP_CHUNK 8
+#define CP_INTMAX 0x7fffffff
+#define CP_PATH_CAP 4096
+
+
+__device__ __forceinline__ float cp_inf() { return __int_as_float(0x7f800000); }
+__device__ __forceinline__ u64 cp_clock_ns() {
+    u64 t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return t;
+}
+__device__ __forceinline__ float4 cp_ldcg4(const float* p) {
+    float4 v;
+    asm volatile("ld.global.cg.v4.f32 {%0,%1,%2,%3}, [%4];"
+                 : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "l"(p));
+    return v;
+}
+__device__ __forceinline__ int cp_ldvol(const int* p) { return *(const volatile int*)p; }
+template <class T> __device__ __forceinline__ bool cp_finite(T x) { return isfinite(x); }
+
+// ---------------------------------------------------------------------------
+// team = CP_G lanes of a warp
+// ---------------------------------------------------------------------------
+struct Team {
+    unsigned lane, base, mask;
+    __device__ Team() {
+        unsigned l = threadIdx.x & 31u;
+        lane = l % CP_G;
+        base = l - lane;
+        mask = (CP_G == 32) ? 0xffffffffu : (0xffffu << base);
+    }
+    __device__ __forceinline__ unsigned ballot(bool p) const {
+        return __ballot_sync(mask, p) >> base;
+    }
+    __device__ __forceinline__ bool any(bool p) const { return ballot(p) != 0u; }
+    __device__ __forceinline__ void sync() const { __syncwarp(mask); }
+    __device__ __forceinline__ int bcast(int v, int src) const { return __shfl_sync(mask, v, src, CP_G); }
+    __device__ __forceinline__ float bcastf(float v, int src) const { return __shfl_sync(mask, v, src, CP_G); }
+    __device__ __forceinline__ float sum(float v) const {
+#pragma unroll
+        for (int o = CP_G / 2; o > 0; o >>= 1) v += __shfl_xor_sync(mask, v, o, CP_G);
+        return v;
+    }
+    __device__ __forceinline__ float maxf(float v) const {
+#pragma unroll
+        for (int o = CP_G / 2; o > 0; o >>= 1) v = fmaxf(v, __shfl_xor_sync(mask, v, o, CP_G));
+        return v;
+    }
+    // lexicographic (key, idx) minimum over the team
+    __device__ __forceinline__ void argmin(float& key, int& idx) const {
+#pragma unroll
+        for (int o = CP_G / 2; o > 0; o >>= 1) {
+            float k2 = __shfl_xor_sync(mask, key, o, CP_G);
+            int i2 = __shfl_xor_sync(mask, idx, o, CP_G);
+            if (k2 < key || (k2 == key && i2 < idx)) { key = k2; idx = i2; }
+        }
+    }
+    __device__ __forceinline__ void argmin_i(int& key, int& idx) const {
+#pragma unroll
+        for (int o = CP_G / 2; o > 0; o >>= 1) {
+            int k2 = __shfl_xor_sync(mask, key, o, CP_G);
+            int i2 = __shfl_xor_sync(mask, idx, o, CP_G);
+            if (k2 < key || (k2 == key && i2 < idx)) { key = k2; idx = i2; }
+        }
+    }
+};
+
+// ---------------------------------------------------------------------------
+// constraint (packed layout of maniplan/constraints.py:123-176)
+// ---------------------------------------------------------------------------
+
+// rotation -> quaternion, w >= 0 (maniplan/_kernels/pure.py:130-159)
+template <class T>
+__device__ __forceinline__ void cp_quat(const T* r, T* q) {
+    T w, x, y, z, s;
+    T tr = (r[0] + r[4]) + r[8];
+    if (tr > T(0)) {
+        s = sqrt(tr + T(1)) * T(2);
+        w = T(0.25) * s; x = (r[7] - r[5]) / s; y = (r[2] - r[6]) / s; z = (r[3] - r[1]) / s;
+    } else if (r[0] > r[4] && r[0] > r[8]) {
+        s = sqrt(((T(1) + r[0]) - r[4]) - r[8]) * T(2);
+        w = (r[7] - r[5]) / s; x = T(0.25) * s; y = (r[1] + r[3]) / s; z = (r[2] + r[6]) / s;
+    } else if (r[4] > r[8]) {
+        s = sqrt(((T(1) + r[4]) - r[0]) - r[8]) * T(2);
+        w = (r[2] - r[6]) / s; x = (r[1] + r[3]) / s; y = T(0.25) * s; z = (r[5] + r[7]) / s;
+    } else {
+        s = sqrt(((T(1) + r[8]) - r[0]) - r[4]) * T(2);
+        w = (r[3] - r[1]) / s; x = (r[2] + r[6]) / s; y = (r[5] + r[7]) / s; z = T(0.25) * s;
+    }
+    if (w < T(0)) { w = -w; x = -x; y = -y; z = -z; }
+    q[0] = w; q[1] = x; q[2] = y; q[3] = z;
+}
+
+// q_fixed^-1 * q_ee as a rotation vector k*v (pure.py:328-344)
+template <class T>
+__device__ __forceinline__ T cp_relrot(const Con<T>& c, const T* qe, T* v) {
+    T aw = c.qf[0], ax = -c.qf[1], ay = -c.qf[2], az = -c.qf[3];
+    T rw = ((aw * qe[0] - ax * qe[1]) - ay * qe[2]) - az * qe[3];
+    T rx = ((aw * qe[1] + ax * qe[0]) + ay * qe[3]) - az * qe[2];
+    T ry = ((aw * qe[2] - ax * qe[3]) + ay * qe[0]) + az * qe[1];
+    T rz = ((aw * qe[3] + ax * qe[2]) - ay * qe[1]) + az * qe[0];
+    if (rw < T(0)) { rw = -rw; rx = -rx; ry = -ry; rz = -rz; }
+    T vn = sqrt((rx * rx + ry * ry) + rz * rz);
+    v[0] = rx; v[1] = ry; v[2] = rz;
+    return vn < T(1e-12) ? T(2) : T(2) * atan2(vn, rw) / vn;
+}
+
+// task error at a pose (pure.py:312-345); writes CP_M rows
+template <class T>
+__device__ __forceinline__ void cp_task_err(const Con<T>& c, const T* p, const T* qe, T* e) {
+    int m = 0;
+#if CP_KIND == 0
+    e[m++] = ((c.anchor[0] * p[0] + c.anchor[1] * p[1]) + c.anchor[2] * p[2]) - c.offset;
+#else
+    T dx = p[0] - c.anchor[0], dy = p[1] - c.anchor[1], dz = p[2] - c.anchor[2];
+    e[m++] = (c.b1[0] * dx + c.b1[1] * dy) + c.b1[2] * dz;
+    e[m++] = (c.b2[0] * dx + c.b2[1] * dy) + c.b2[2] * dz;
+#endif
+#if CP_ORIENT
+    T v[3];
+    T k = cp_relrot(c, qe, v);
+    e[m++] = c.weight * (k * v[0]);
+    e[m++] = c.weight * (k * v[1]);
+    e[m++] = c.weight * (k * v[2]);
+#endif
+    (void)qe;
+}
+
+// inverse left Jacobian of SO(3) (pure.py:348-366)
+template <class T>
+__device__ __forceinline__ void cp_so3_rate(T p0, T p1, T p2, T* a) {
+    T c2, t2 = (p0 * p0 + p1 * p1) + p2 * p2;
+    if (t2 < T(1e-8)) {
+        c2 = T(1.0 / 12.0) + t2 / T(720);
+    } else {
+        T th = sqrt(t2), s, co;
+        sincos(th, &s, &co);
+        c2 = T(1) / t2 - (T(1) + co) / ((T(2) * th) * s);
+    }
+    T h0 = T(0.5) * p0, h1 = T(0.5) * p1, h2 = T(0.5) * p2;
+    T c01 = c2 * (p0 * p1), c02 = c2 * (p0 * p2), c12 = c2 * (p1 * p2);
+    a[0] = T(1) - c2 * (p1 * p1 + p2 * p2); a[1] = h2 + c01; a[2] = c02 - h1;
+    a[3] = c01 - h2; a[4] = T(1) - c2 * (p0 * p0 + p2 * p2); a[5] = h0 + c12;
+    a[6] = h1 + c02; a[7] = c12 - h0; a[8] = T(1) - c2 * (p0 * p0 + p1 * p1);
+}
+
+// (e, J) at q from one FK pass (pure.py:369-427).  Returns the EE pose too.
+template <class T>
+__device__ __forceinline__ void cp_err_jac(const Con<T>& c, const T* q, T* e, T (*J)[CP_N]) {
+    T R[CP_N * 9], P[CP_N * 3], AX[CP_N * 3], OR[CP_N * 3], SPH[(CP_S > 0 ? CP_S : 1) * 3];
+    cp_fk<T>(q, R, P, AX, OR, SPH);
+    const T* pe = P + 3 * CP_EE;
+    T qe[4];
+    cp_quat<T>(R + 9 * CP_EE, qe);
+    cp_task_err<T>(c, pe, qe, e);
+#if CP_ORIENT
+    T v[3], A[9], Mo[9];
+    T k = cp_relrot(c, qe, v);
+    cp_so3_rate<T>(k * v[0], k * v[1], k * v[2], A);
+#pragma unroll
+    for (int i = 0; i < 3; i++)
+#pragma unroll
+        for (int j = 0; j < 3; j++)
+            Mo[3 * i + j] = c.weight * ((A[3 * i] * c.rft[j] + A[3 * i + 1] * c.rft[3 + j]) + A[3 * i + 2] * c.rft[6 + j]);
+#endif
+#pragma unroll
+    for (int j = 0; j < CP_N; j++) {
+        const T* a = AX + 3 * j;
+        T l0, l1, l2;
+        if (cp_jtype(j) == 0) {
+            T rx = pe[0] - OR[3 * j], ry = pe[1] - OR[3 * j + 1], rz = pe[2] - OR[3 * j + 2];
+            l0 = a[1] * rz - a[2] * ry; l1 = a[2] * rx - a[0] * rz; l2 = a[0] * ry - a[1] * rx;
+        } else {
+            l0 = a[0]; l1 = a[1]; l2 = a[2];
+        }
+        int r = 0;
+#if CP_KIND == 0
+        J[r++][j] = (c.anchor[0] * l0 + c.anchor[1] * l1) + c.anchor[2] * l2;
+#else
+        J[r++][j] = (c.b1[0] * l0 + c.b1[1] * l1) + c.b1[2] * l2;
+        J[r++][j] = (c.b2[0] * l0 + c.b2[1] * l1) + c.b2[2] * l2;
+#endif
+#if CP_ORIENT
+        if (cp_jtype(j) == 0) {
+#pragma unroll
+            for (int i = 0; i < 3; i++) J[r + i][j] = (Mo[3 * i] * a[0] + Mo[3 * i + 1] * a[1]) + Mo[3 * i + 2] * a[2];
+        } else {
+#pragma unroll
+            for (int i = 0; i < 3; i++) J[r + i][j] = T(0);
+        }
+#endif
+        (void)r;
+    }
+}
+
+// J^T (J J^T + lam^2 I)^-1 e by Cholesky; false when not SPD (pure.py:437-480)
+template <class T, int M>
+__device__ __forceinline__ bool cp_damped(const T (*J)[CP_N], const T* e, T lam, T* step) {
+    T L[M][M], y[M], z[M];
+#pragma unroll
+    for (int i = 0; i < M; i++)
+#pragma unroll
+        for (int j = 0; j <= i; j++) {
+            T acc = T(0);
+#pragma unroll
+            for (int k = 0; k < CP_N; k++) acc += J[i][k] * J[j][k];
+            if (i == j) acc += lam * lam;
+#pragma unroll
+            for (int k = 0; k < j; k++) acc -= L[i][k] * L[j][k];
+            if (i == j) {
+                if (!(acc > T(0))) return false;
+                L[i][i] = sqrt(acc);
+            } else {
+                L[i][j] = acc / L[j][j];
+            }
+        }
+#pragma unroll
+    for (int i = 0; i < M; i++) {
+        T acc = e[i];
+#pragma unroll
+        for (int k = 0; k < i; k++) acc -= L[i][k] * y[k];
+        y[i] = acc / L[i][i];
+    }
+#pragma unroll
+    for (int i = M - 1; i >= 0; i--) {
+        T acc = y[i];
+#pragma unroll
+        for (int k = i + 1; k < M; k++) acc -= L[k][i] * z[k];
+        z[i] = acc / L[i][i];
+    }
+#pragma unroll
+    for (int k = 0; k < CP_N; k++) {
+        T acc = T(0);
+#pragma unroll
+        for (int i = 0; i < M; i++) acc += J[i][k] * z[i];
+        step[k] = acc;
+    }
+    return true;
+}
+
+// One out-of-line FP32 copy of (e, J): shared by stage 1, the sequential
+// projector and the parity kernels (keeps the NVRTC module small).
+__device__ __noinline__ void cp_err_jac_f(const Con<float>& c, const float* q, float* e, float (*J)[CP_N]) {
+    float qq[CP_N];
+#pragma unroll
+    for (int k = 0; k < CP_N; k++) qq[k] = q[k];
+    cp_err_jac<float>(c, qq, e, J);
+}
+
+// ---------------------------------------------------------------------------
+// projection parameters (maniplan/projection.py:75-90), FP32 with margins
+// ---------------------------------------------------------------------------
+
+// stage 1 of Alg. 1 for one waypoint (pure.py:511-546).  Validity is judged
+// at the pre-update waypoint with the device margins.
+__device__ __forceinline__ bool cp_stage1(const Con<float>& c, const ProjArgs& pa, const float* xt,
+                                          const float* xp, float tau_sm, float* xn) {
+    bool fin = true;
+#pragma unroll
+    for (int k = 0; k < CP_N; k++) fin &= cp_finite(xt[k]);
+    if (!fin) {
+#pragma unroll
+        for (int k = 0; k < CP_N; k++) xn[k] = xt[k];
+        return false;
+    }
+    float e[CP_M], J[CP_M][CP_N], g[CP_N];
+    cp_err_jac_f(c, xt, e, J);
+    float en2 = 0.f;
+#pragma unroll
+    for (int i = 0; i < CP_M; i++) en2 += e[i] * e[i];
+    if (!cp_damped<float, CP_M>(J, e, pa.lam, g)) {
+#pragma unroll
+        for (int k = 0; k < CP_N; k++) g[k] = 0.f;
+    }
+    float d[CP_N], s2 = 0.f;
+#pragma unroll
+    for (int k = 0; k < CP_N; k++) { d[k] = xt[k] - xp[k]; s2 += d[k] * d[k]; }
+    float gap = sqrtf(s2);
+    float exc = fmaxf(gap - tau_sm, 0.f);
+#pragma unroll
+    for (int k = 0; k < CP_N; k++) xn[k] = xt[k] - pa.alpha * (g[k] + d[k] * exc);
+    return gap < tau_sm * 0.99999f && sqrtf(en2) < pa.tau_task_dev;
+}
+
+__device__ __noinline__ float cp_err_norm(const Con<float>& c, const float* q) {
+    float R[CP_N * 9], P[CP_N * 3], AX[CP_N * 3], OR[CP_N * 3], SPH[(CP_S > 0 ? CP_S : 1) * 3];
+    cp_fk<float>(q, R, P, AX, OR, SPH);
+    float qe[4], e[CP_M];
+    cp_quat<float>(R + 9 * CP_EE, qe);
+    cp_task_err<float>(c, P + 3 * CP_EE, qe, e);
+    float s = 0.f;
+#pragma unroll
+    for (int i = 0; i < CP_M; i++) s += e[i] * e[i];
+    return sqrtf(s);
+}
+
+// Project the team's segment in place: Alg. 1 (pure.py:549-577) for modes
+// 0/1, the sequential baseline (pure.py:580-615) for mode 2, then the
+// clamp-and-revalidate finish (maniplan/projection.py:162-180).
+// seg rows [0, W) live in shared memory; lane t owns row t.
+// trace (optional, parity only): after every iteration the buffer is copied
+// to trace[it-1] and the prefix to trace_prog[it-1].
+__device__ bool cp_project(const Team& tm, float (*seg)[CP_NP], int W, const Con<float>& c,
+                           const ProjArgs& pa, int* iters_out, int* prog_out,
+                           float* trace = nullptr, int* trace_prog = nullptr) {
+    const int t = (int)tm.lane;
+    const bool row = t < W;
+    float tau_sm = pa.tau_sm_fixed;
+    if (!(tau_sm > 0.f)) {   // _resolve_taus (projection.py:137-144)
+        float g = 0.f;
+        if (row && t >= 1) {
+            float s2 = 0.f;
+#pragma unroll
+            for (int k = 0; k < CP_N; k++) { float d = seg[t][k] - seg[t - 1][k]; s2 += d * d; }
+            g = sqrtf(s2);
+        }
+        g = tm.maxf(g);
+        tau_sm = g > 0.f ? 1.5f * g : 1e-6f;
+    }
+    const unsigned full = (W >= 32) ? 0xffffffffu : ((1u << W) - 1u);
+    int prog = 0, iters = pa.max_iters;
+    bool ok = false;
+    if (pa.mode == 2) {
+        // sequential: converge waypoint t before t+1 (one lane active at a time)
+        int total = 0;
+        ok = true;
+        for (int w = 1; w < W && ok; w++) {
+            int res = 0, its = 0;
+            if (t == w) {
+                float q[CP_N];
+#pragma unroll
+                for (int k = 0; k < CP_N; k++) q[k] = seg[w][k];
+                res = 1;
+                for (;;) {
+                    bool fin = true;
+#pragma unroll
+                    for (int k = 0; k < CP_N; k++) fin &= cp_finite(q[k]);
+                    if (!fin) { res = 0; break; }
+                    float e[CP_M], J[CP_M][CP_N], st[CP_N], en2 = 0.f;
+                    cp_err_jac_f(c, q, e, J);
+#pragma unroll
+                    for (int i = 0; i < CP_M; i++) en2 += e[i] * e[i];
+                    if (sqrtf(en2) < pa.tau_task_dev) break;
+                    if (its == pa.max_iters) { res = 0; break; }
+                    if (!cp_damped<float, CP_M>(J, e, pa.lam, st)) { res = 0; break; }
+#pragma unroll
+                    for (int k = 0; k < CP_N; k++) q[k] = q[k] - pa.alpha * st[k];
+                    its++;
+                }
+                if (res) {
+                    float s2 = 0.f;
+#pragma unroll
+                    for (int k = 0; k < CP_N; k++) { float d = q[k] - seg[w - 1][k]; s2 += d * d; }
+                    if (!(sqrtf(s2) < tau_sm * 0.99999f)) res = 0;
+                }
+                if (res) {
+#pragma unroll
+                    for (int k = 0; k < CP_N; k++) seg[w][k] = q[k];
+                }
+            }
+            res = tm.bcast(res, w);
+            its = tm.bcast(its, w);
+            tm.sync();
+            if (!res) { ok = false; prog = w - 1; }
+            else total += its;
+        }
+        if (ok) { prog = W - 1; iters = total; }
+    } else {
+        const bool unconstrained = !(pa.tau_task_dev < cp_inf());
+        for (int it = 1; it <= pa.max_iters; it++) {
+            const bool act = row && t > prog;
+            float xn[CP_N], xt[CP_N], xp[CP_N];
+            bool valid = false, full_step = true;
+            if (act) {
+#pragma unroll
+                for (int k = 0; k < CP_N; k++) { xt[k] = seg[t][k]; xp[k] = seg[t - 1][k]; }
+            }
+            if (unconstrained) {
+                // tau_task = inf: validity needs no FK (pure.py:545); the
+                // update is computed only if the segment is not accepted as is.
+                bool cheap = true;
+                if (act) {
+                    float s2 = 0.f;
+                    bool fin = true;
+#pragma unroll
+                    for (int k = 0; k < CP_N; k++) { float d = xt[k] - xp[k]; s2 += d * d; fin &= cp_finite(xt[k]); }
+                    cheap = fin && sqrtf(s2) < tau_sm * 0.99999f;
+                }
+                if (!tm.any(!cheap)) { valid = act; full_step = false; }
+            }
+            if (full_step && act) valid = cp_stage1(c, pa, xt, xp, tau_sm, xn);
+            unsigned vm = tm.ballot(act && valid) & full;
+            int np = prog;
+            if (pa.mode == 1) {   // literal-gap: largest valid index (pure.py:560-563)
+                unsigned hi = vm & ~((2u << prog) - 1u);
+                if (hi) np = 31 - __clz(hi);
+            } else {              // contiguous prefix (pure.py:564-568)
+                unsigned rest = ~(vm >> (prog + 1));
+                int run = __ffs(rest) - 1;
+                if (run < 0) run = 32;
+                np = min(prog + run, W - 1);
+            }
+            if (np == W - 1) {
+                if (trace) {
+                    if (row) {
+#pragma unroll
+                        for (int k = 0; k < CP_N; k++) trace[((size_t)(it - 1) * W + t) * CP_N + k] = seg[t][k];
+                    }
+                    if (t == 0) trace_prog[it - 1] = np;
+                }
+                ok = true;
+                iters = it;
+                prog = np;
+                break;
+            }
+            tm.sync();
+            if (row && t > np) {
+#pragma unroll
+                for (int k = 0; k < CP_N; k++) seg[t][k] = xn[k];
+            }
+            tm.sync();
+            prog = np;
+            if (trace) {
+                if (row) {
+#pragma unroll
+                    for (int k = 0; k < CP_N; k++) trace[((size_t)(it - 1) * W + t) * CP_N + k] = seg[t][k];
+                }
+                if (t == 0) trace_prog[it - 1] = np;
+            }
+        }
+    }
+    if (ok) {
+        // clamp to limits; if anything moved, re-check both tolerances
+        float q[CP_N], qc[CP_N];
+        bool moved = false;
+        if (row) {
+#pragma unroll
+            for (int k = 0; k < CP_N; k++) {
+                q[k] = seg[t][k];
+                qc[k] = fminf(fmaxf(q[k], (float)cp_lo(k)), (float)cp_hi(k));
+                moved |= !(qc[k] == q[k]);
+            }
+        }
+        if (tm.any(moved)) {
+            tm.sync();
+            bool good = true;
+            if (row) {
+#pragma unroll
+                for (int k = 0; k < CP_N; k++) seg[t][k] = qc[k];
+            }
+            tm.sync();
+            if (row) {
+                good = cp_err_norm(c, qc) < pa.tau_task_dev;
+                if (t >= 1) {
+                    float s2 = 0.f;
+#pragma unroll
+                    for (int k = 0; k < CP_N; k++) { float d = qc[k] - seg[t - 1][k]; s2 += d * d; }
+                    good = good && sqrtf(s2) < tau_sm * 0.99999f;
+                }
+            }
+            if (tm.any(!good)) {
+                ok = false;
+                iters = pa.max_iters;
+                if (row) {
+#pragma unroll
+                    for (int k = 0; k < CP_N; k++) seg[t][k] = q[k];
+                }
+            }
+            tm.sync();
+        }
+    } else {
+        iters = pa.max_iters;
+    }
+    *iters_out = iters;
+    *prog_out = prog;
+    return ok;
+}
+
+// ---------------------------------------------------------------------------
+// collision checking against the smem scene (pure.py:646-699)
+// ---------------------------------------------------------------------------
+
+struct ValOut {
+    bool valid;
+    int first_bad;         // waypoint of the first detection in (round, waypoint) order
+    i64 performed;         // lockstep-equivalent count (reference semantics), exact mode
+    i64 gpu_checks;        // checks this team actually evaluated
+};
+
+__device__ __forceinline__ bool cp_hit_box(float cx, float cy, float cz, float r2, float4 c, float4 h) {
+    float dx = fmaxf(fabsf(cx - c.x) - h.x, 0.f);
+    float dy = fmaxf(fabsf(cy - c.y) - h.y, 0.f);
+    float dz = fmaxf(fabsf(cz - c.z) - h.z, 0.f);
+    return fmaf(dx, dx, fmaf(dy, dy, dz * dz)) < r2;
+}
+__device__ __forceinline__ bool cp_hit_sph(float cx, float cy, float cz, float r, float4 s) {
+    float dx = cx - s.x, dy = cy - s.y, dz = cz - s.z, rr = r + s.w;
+    return fmaf(dx, dx, fmaf(dy, dy, dz * dz)) < rr * rr;
+}
+
+// Validate rows [t_first, W) of seg.  Lanes run in lockstep over the
+// reference's check order (robot sphere major, boxes then spheres, then the
+// self pairs), so a team vote after every CP_CHUNK rounds both implements the
+// early-exit flag and yields the reference's first detection exactly.
+// margin inflates every robot sphere (planner safety margin; 0 for parity).
+__device__ ValOut cp_validate(const Team& tm, const float (*seg)[CP_NP], int W, int t_first,
+                              bool flag_on, float margin, const SceneSm& sc) {
+    const int t = (int)tm.lane;
+    const bool mine = t >= t_first && t < W;
+    const int E = sc.nb + sc.ne;
+    float sx[CP_S > 0 ? CP_S : 1], sy[CP_S > 0 ? CP_S : 1], sz[CP_S > 0 ? CP_S : 1];
+    {
+        float q[CP_N];
+#pragma unroll
+        for (int k = 0; k < CP_N; k++) q[k] = mine ? seg[t][k] : 0.f;
+        float R[CP_N * 9], P[CP_N * 3], AX[CP_N * 3], OR[CP_N * 3], SPH[(CP_S > 0 ? CP_S : 1) * 3];
+        cp_fk<float>(q, R, P, AX, OR, SPH);
+#pragma unroll
+        for (int s = 0; s < CP_S; s++) { sx[s] = SPH[3 * s]; sy[s] = SPH[3 * s + 1]; sz[s] = SPH[3 * s + 2]; }
+    }
+    int first_r = CP_INTMAX;
+    i64 rounds_done = 0;
+    bool stop = false;
+#pragma unroll
+    for (int s = 0; s < CP_S; s++) {
+        if (!stop) {
+            const float r = (float)cp_rad(s) + margin, r2 = r * r;
+            const float cx = sx[s], cy = sy[s], cz = sz[s];
+            const int rbase = s * E;
+            for (int p0 = 0; p0 < E; p0 += CP_CHUNK) {
+                const int p1 = min(p0 + CP_CHUNK, E);
+                for (int p = p0; p < p1; p++) {
+                    bool hit = p < sc.nb ? cp_hit_box(cx, cy, cz, r2, sc.box_c[p], sc.box_h[p])
+                                         : cp_hit_sph(cx, cy, cz, r, sc.sph[p - sc.nb]);
+                    if (mine && hit && first_r == CP_INTMAX) first_r = rbase + p;
+                }
+                rounds_done = rbase + p1;
+                if (flag_on && tm.any(first_r != CP_INTMAX)) { stop = true; break; }
+            }
+        }
+    }
+    if (!stop && CP_P > 0) {
+        const int rbase = CP_S * E;
+#pragma unroll
+        for (int k = 0; k < CP_P; k++) {
+            const int a = cp_pair_a(k), b = cp_pair_b(k);
+            const float rr = (float)(cp_rad(a) + cp_rad(b)) + 2.f * margin;
+            float dx = sx[a] - sx[b], dy = sy[a] - sy[b], dz = sz[a] - sz[b];
+            bool hit = fmaf(dx, dx, fmaf(dy, dy, dz * dz)) < rr * rr;
+            if (mine && hit && first_r == CP_INTMAX) first_r = rbase + k;
+        }
+        rounds_done = rbase + CP_P;
+    }
+    ValOut o;
+    int key = first_r, idx = t;
+    tm.argmin_i(key, idx);
+    const i64 per = (i64)CP_S * E + CP_P;
+    o.valid = key == CP_INTMAX;
+    o.first_bad = o.valid ? -1 : idx;
+    o.performed = (flag_on && !o.valid) ? (i64)key * W + idx + 1 : per * W;
+    o.gpu_checks = rounds_done * (W - t_first);
+    return o;
+}
+
+// ---------------------------------------------------------------------------
+// nearest neighbour: coalesced float4 SoA scan + team argmin (planner.py:198-201)
+// nodes: coordinate d of node i at nodes[d * cap + i]; never-written slots are
+// NaN and drop out of the comparison.  Ties go to the lowest index.
+// ---------------------------------------------------------------------------
+__device__ int cp_nearest(const Team& tm, const float* nodes, int cap, int count, const float* q) {
+    float qq[CP_N];
+#pragma unroll
+    for (int k = 0; k < CP_N; k++) qq[k] = q[k];
+    float best = cp_inf();
+    int bi = CP_INTMAX;
+    const int n4 = (count + 3) >> 2;
+    for (int i4 = (int)tm.lane; i4 < n4; i4 += CP_G) {
+        float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+        for (int k = 0; k < CP_N; k++) {
+            float4 v = cp_ldcg4(nodes + (size_t)k * cap + 4 * i4);
+            float a = v.x - qq[k], b = v.y - qq[k], cc = v.z - qq[k], d = v.w - qq[k];
+            acc.x = fmaf(a, a, acc.x); acc.y = fmaf(b, b, acc.y);
+            acc.z = fmaf(cc, cc, acc.z); acc.w = fmaf(d, d, acc.w);
+        }
+        const int i0 = 4 * i4;
+        if (acc.x < best && i0 < count) { best = acc.x; bi = i0; }
+        if (acc.y < best && i0 + 1 < count) { best = acc.y; bi = i0 + 1; }
+        if (acc.z < best && i0 + 2 < count) { best = acc.z; bi = i0 + 2; }
+        if (acc.w < best && i0 + 3 < count) { best = acc.w; bi = i0 + 3; }
+    }
+    tm.argmin(best, bi);
+    return bi == CP_INTMAX ? 0 : bi;
+}
+
+// ---------------------------------------------------------------------------
+// Halton sampling, FP64, bit-exact with maniplan/sampling.py:32-81
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ int cp_prime(int k) {
+    const int pr[32] = {2, 3, 5, 7, 11, 13, 17, 19, 23, 29, 31, 37, 41, 43, 47, 53,
+                        59, 61, 67, 71, 73, 79, 83, 89, 97, 101, 103, 107, 109, 113, 127, 131};
+    return pr[k];
+}
+__device__ __forceinline__ double cp_radical_inverse(i64 index, int base) {
+    double f = 0.0;
+    const double b = (double)base;
+    double scale = __ddiv_rn(1.0, b);
+    i64 i = index;
+    while (i > 0) {
+        f = __dadd_rn(f, __dmul_rn((double)(i % base), scale));
+        scale = __ddiv_rn(scale, b);
+        i /= base;
+    }
+    return f;
+}
+__device__ __forceinline__ double cp_halton(i64 index, int k) {
+    double u = cp_radical_inverse(index, cp_prime(k));
+    return __dadd_rn(cp_lo(k), __dmul_rn(__dsub_rn(cp_hi(k), cp_lo(k)), u));
+}
+
+// ---------------------------------------------------------------------------
+// small team vector helpers (lanes k < CP_N own coordinate k)
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ bool cp_vec_equal(const Team& tm, const float* a, const float* b) {
+    bool ne = (int)tm.lane < CP_N && !(a[tm.lane] == b[tm.lane]);
+    return !tm.any(ne);
+}
+__device__ __forceinline__ float cp_vec_dist(const Team& tm, const float* a, const float* b) {
+    float d = 0.f;
+    if ((int)tm.lane < CP_N) { d = a[tm.lane] - b[tm.lane]; d = d * d; }
+    return sqrtf(tm.sum(d));
+}
+// steer (planner.py:204-211)
+__device__ __forceinline__ void cp_steer(const Team& tm, const float* qn, const float* qr, float step, float* out) {
+    float dist = cp_vec_dist(tm, qn, qr);
+    if ((int)tm.lane < CP_N) {
+        int k = tm.lane;
+        out[k] = dist <= step ? qr[k] : qn[k] + (step / dist) * (qr[k] - qn[k]);
+    }
+    tm.sync();
+}
+// interpolate_segment (projection.py:114-128): endpoints stored exactly
+__device__ __forceinline__ void cp_interp(const Team& tm, float (*seg)[CP_NP], int W, const float* a, const float* b) {
+    const int t = tm.lane;
+    tm.sync();
+    if (t < W) {
+        float f = (float)t / (float)(W - 1);
+#pragma unroll
+        for (int k = 0; k < CP_N; k++) {
+            float v = a[k] + f * (b[k] - a[k]);
+            seg[t][k] = t == 0 ? a[k] : (t == W - 1 ? b[k] : v);
+        }
+    }
+    tm.sync();
+}
+__device__ __forceinline__ void cp_copy(const Team& tm, float* dst, const float* src) {
+    tm.sync();
+    if ((int)tm.lane < CP_N) dst[tm.lane] = src[tm.lane];
+    tm.sync();
+}
+
+// ===========================================================================
+// Planner (maniplan/planner.py:361-485) -- persistent kernel
+// ===========================================================================
+
+
+
+__device__ __forceinline__ float* cp_tree(const PlanArgs& A, int q, int k) {
+    return A.trees + ((size_t)(2 * q + k) * CP_N) * A.cap;
+}
+__device__ __forceinline__ int* cp_par(const PlanArgs& A, int q, int k) {
+    return A.parents + (size_t)(2 * q + k) * A.cap;
+}
+
+struct TeamWS {
+    float seg[CP_G][CP_NP];
+    float qr[CP_NP], qn[CP_NP], qs[CP_NP], qe[CP_NP], qc[CP_NP], qt[CP_NP], qm[CP_NP];
+};
+
+struct Stats {
+    unsigned long long v[ST_NSTAT];
+    __device__ Stats() {
+#pragma unroll
+        for (int i = 0; i < ST_NSTAT; i++) v[i] = 0ull;
+    }
+};
+
+__device__ __forceinline__ bool cp_should_stop(const Team& tm, QueryState& Q, const PlanArgs& A) {
+    int s = 0;
+    if (tm.lane == 0) {
+        s = cp_ldvol(&Q.solved) | cp_ldvol(&Q.stop);
+        if (!s && A.budget_ns > 0 && cp_clock_ns() - Q.t0_ns > (u64)A.budget_ns) {
+            atomicExch(&Q.timed_out, 1);
+            atomicExch(&Q.stop, 1);
+            s = 1;
+        }
+    }
+    return tm.bcast(s, 0) != 0;
+}
+
+// validate with stats accumulation; waypoint 0 (an existing tree node) skipped
+__device__ __forceinline__ bool cp_check_motion(const Team& tm, TeamWS& ws, const PlanArgs& A,
+                                                const SceneSm& sc, Stats& st) {
+    ValOut v = cp_validate(tm, ws.seg, A.W, 1, A.flag_on, A.margin, sc);
+    st.v[ST_CCPERF] += v.gpu_checks;
+    st.v[ST_CCPOSS] += (u64)((i64)CP_S * (sc.nb + sc.ne) + CP_P) * (A.W - 1);
+    st.v[ST_GPUCHK] += v.gpu_checks;
+    if (!v.valid) st.v[ST_CREJ]++;
+    return v.valid;
+}
+
+// derive_edge (planner.py:223-245): the motion a->b re-derivable from its endpoints
+__device__ bool cp_derive_edge(const Team& tm, TeamWS& ws, const PlanArgs& A, const SceneSm& sc,
+                               const float* a, const float* b, Stats& st) {
+    cp_interp(tm, ws.seg, A.W, a, b);
+    int it, pr;
+    if (!cp_project(tm, ws.seg, A.W, A.con, A.pa, &it, &pr)) {
+        st.v[ST_PFAIL]++;
+        return false;
+    }
+    return cp_check_motion(tm, ws, A, sc, st);
+}
+
+// append q to tree k of query qi with parent par; returns index or -1 (full)
+__device__ __forceinline__ int cp_append(const Team& tm, const PlanArgs& A, QueryState& Q, int qi, int k,
+                                         const float* q, int par) {
+    int idx = 0;
+    if (tm.lane == 0) idx = atomicAdd(&Q.count[k], 1);
+    idx = tm.bcast(idx, 0);
+    if (idx >= A.cap) {
+        if (tm.lane == 0) { atomicExch(&Q.overflow, 1); atomicExch(&Q.stop, 1); }
+        return -1;
+    }
+    if (tm.lane == 0) cp_par(A, qi, k)[idx] = par;
+    if ((int)tm.lane < CP_N) cp_tree(A, qi, k)[(size_t)tm.lane * A.cap + idx] = q[tm.lane];
+    tm.sync();
+    return idx;
+}
+
+__device__ __forceinline__ int cp_count(const PlanArgs& A, QueryState& Q, int k) {
+    return min(cp_ldvol(&Q.count[k]), A.cap);
+}
+
+__device__ __forceinline__ void cp_load_node(const Team& tm, const PlanArgs& A, int qi, int k, int idx, float* out) {
+    tm.sync();
+    if ((int)tm.lane < CP_N) out[tm.lane] = __ldcg(cp_tree(A, qi, k) + (size_t)tm.lane * A.cap + idx);
+    tm.sync();
+}
+
+// connect (planner.py:361-409): greedy walk of tree k toward ws.qt.
+// Returns the meet node index if Reached, else -1.
+__device__ int cp_connect(const Team& tm, TeamWS& ws, const PlanArgs& A, const SceneSm& sc,
+                          QueryState& Q, int qi, int k, Stats& st) {
+    int icur = cp_nearest(tm, cp_tree(A, qi, k), A.cap, cp_count(A, Q, k), ws.qt);
+    cp_load_node(tm, A, qi, k, icur, ws.qc);
+    float dist = cp_vec_dist(tm, ws.qc, ws.qt);
+    if (dist <= A.tol) return icur;
+    for (int segs = 0; segs < A.max_connect; segs++) {
+        if (cp_should_stop(tm, Q, A)) return -1;
+        cp_steer(tm, ws.qc, ws.qt, A.step, ws.qs);
+        cp_interp(tm, ws.seg, A.W, ws.qc, ws.qs);
+        int it, pr;
+        if (!cp_project(tm, ws.seg, A.W, A.con, A.pa, &it, &pr)) { st.v[ST_PFAIL]++; return -1; }
+        cp_copy(tm, ws.qe, ws.seg[A.W - 1]);
+        if (cp_vec_equal(tm, ws.qe, ws.qs)) {
+            if (!cp_check_motion(tm, ws, A, sc, st)) return -1;
+        } else if (!cp_derive_edge(tm, ws, A, sc, ws.qc, ws.qe, st)) {
+            return -1;
+        }
+        float nd = cp_vec_dist(tm, ws.qe, ws.qt);
+        if (!(nd < dist)) return -1;
+        int idx = cp_append(tm, A, Q, qi, k, ws.qe, icur);
+        if (idx < 0) return -1;
+        icur = idx;
+        cp_copy(tm, ws.qc, ws.qe);
+        dist = nd;
+        if (dist <= A.tol) return icur;
+    }
+    return -1;
+}
+
+// One team works on query qi until it is solved / stopped / out of samples.
+__device__ void cp_plan_query(const Team& tm, TeamWS& ws, const PlanArgs& A, const SceneSm& sc, int qi) {
+    QueryState& Q = A.qs[qi];
+    Stats st;
+    const int W = A.W;
+    for (;;) {
+        if (cp_should_stop(tm, Q, A)) break;
+        int it = 0;
+        if (tm.lane == 0) it = atomicAdd(&Q.next_sample, 1) + 1;
+        it = tm.bcast(it, 0);
+        if (it > A.max_iterations) {
+            if (tm.lane == 0) { atomicExch(&Q.exhausted, 1); atomicExch(&Q.stop, 1); }
+            break;
+        }
+        st.v[ST_ITER]++;
+        st.v[ST_ATT]++;
+        const int a = (it - 1) & 1, b = a ^ 1;   // start tree extends on odd iterations
+        // sample (sampling.py:65-81) -- FP64 Halton, bit-exact with the reference
+        if ((int)tm.lane < CP_N) ws.qr[tm.lane] = (float)cp_halton((i64)it + Q.seed_offset, tm.lane);
+        tm.sync();
+        // _attempt_extend (planner.py:265-306)
+        const int inear = cp_nearest(tm, cp_tree(A, qi, a), A.cap, cp_count(A, Q, a), ws.qr);
+        cp_load_node(tm, A, qi, a, inear, ws.qn);
+        cp_steer(tm, ws.qn, ws.qr, A.step, ws.qs);
+        if (cp_vec_equal(tm, ws.qs, ws.qn)) continue;              // degenerate
+        cp_interp(tm, ws.seg, W, ws.qn, ws.qs);
+        int pit, ppr;
+        if (!cp_project(tm, ws.seg, W, A.con, A.pa, &pit, &ppr)) { st.v[ST_PFAIL]++; continue; }
+        cp_copy(tm, ws.qe, ws.seg[W - 1]);
+        if (cp_vec_equal(tm, ws.qe, ws.qn)) continue;              // degenerate
+        if (cp_vec_equal(tm, ws.qe, ws.qs)) {
+            if (!cp_check_motion(tm, ws, A, sc, st)) continue;
+        } else if (!cp_derive_edge(tm, ws, A, sc, ws.qn, ws.qe, st)) {
+            continue;
+        }
+        const int node = cp_append(tm, A, Q, qi, a, ws.qe, inear);
+        if (node < 0) break;
+        st.v[ST_ADDED]++;
+        // connect the other tree toward q_new (planner.py:463)
+        cp_copy(tm, ws.qt, ws.qe);
+        const int meet = cp_connect(tm, ws, A, sc, Q, qi, b, st);
+        if (meet < 0) continue;
+        // junction (planner.py:466-481)
+        cp_load_node(tm, A, qi, b, meet, ws.qm);
+        const float* js = a == 0 ? ws.qt : ws.qm;
+        const float* jg = a == 0 ? ws.qm : ws.qt;
+        bool ok = cp_vec_equal(tm, js, jg);
+        if (!ok) {
+            cp_copy(tm, ws.qr, js);   // derive_edge overwrites seg / qs only
+            cp_copy(tm, ws.qn, jg);
+            ok = cp_derive_edge(tm, ws, A, sc, ws.qr, ws.qn, st);
+        }
+        if (ok) {
+            if (tm.lane == 0 && atomicCAS(&Q.solved, 0, 1) == 0) {
+                Q.meet[a] = node;
+                Q.meet[b] = meet;
+                Q.t_end_ns = cp_clock_ns();
+                __threadfence();
+                atomicExch(&Q.stop, 1);
+            }
+            break;
+        }
+    }
+    if (tm.lane == 0) {
+#pragma unroll
+        for (int i = 0; i < ST_NSTAT; i++)
+            if (st.v[i]) atomicAdd(&Q.stats[i], st.v[i]);
+    }
+}
+
+__device__ __forceinline__ SceneSm cp_stage_scene(const SceneSm& g, float4* sm) {
+    float4* bc = sm;
+    float4* bh = sm + g.nb;
+    float4* sp = sm + 2 * g.nb;
+    for (int i = threadIdx.x; i < g.nb; i += blockDim.x) { bc[i] = g.box_c[i]; bh[i] = g.box_h[i]; }
+    for (int i = threadIdx.x; i < g.ne; i += blockDim.x) sp[i] = g.sph[i];
+    __syncthreads();
+    SceneSm s;
+    s.box_c = bc; s.box_h = bh; s.sph = sp; s.nb = g.nb; s.ne = g.ne;
+    return s;
+}
+
+#if !CP_PARITY
+// Dynamic smem: [scene float4s][team workspaces]
+extern "C" __global__ void __launch_bounds__(CP_NTHREADS, 1)
+cp_plan_kernel(const __grid_constant__ PlanArgs A) {
+    extern __shared__ float4 cp_smem[];
+    SceneSm sc = cp_stage_scene(A.scene_g, cp_smem);
+    TeamWS* wsa = reinterpret_cast<TeamWS*>(cp_smem + 2 * A.scene_g.nb + A.scene_g.ne);
+    Team tm;
+    const int team_in_cta = (threadIdx.x >> 5) * (32 / CP_G) + (threadIdx.x & 31) / CP_G;
+    TeamWS& ws = wsa[team_in_cta];
+    int visits = 0;
+    for (;;) {
+        int qi = -1;
+        if (tm.lane == 0) {
+            int h = atomicAdd(A.queue_head, 1);
+            if (h < A.nq) {
+                qi = h;
+            } else {
+                // queue drained: join an unfinished query (work stealing)
+                int s0 = atomicAdd(A.team_counter, 1) % A.nq;
+                for (int j = 0; j < A.nq; j++) {
+                    int c = (s0 + j) % A.nq;
+                    QueryState& Q = A.qs[c];
+                    if (!cp_ldvol(&Q.stop) && !cp_ldvol(&Q.solved) && Q.setup_code == 0) { qi = c; break; }
+                }
+            }
+        }
+        qi = tm.bcast(qi, 0);
+        if (qi < 0 || ++visits > 4 * A.nq + 4) break;
+        if (A.qs[qi].setup_code != 0) continue;
+        cp_plan_query(tm, ws, A, sc, qi);
+    }
+}
+
+#endif  // !CP_PARITY
+
+// Per-query setup, FP64 (planner.py:416-427 _check_endpoint, :442-445 trees).
+// One CTA (64 threads) per query: warp 0 checks the start, warp 1 the goal.
+
+__device__ int cp_check_config_d(const SetupArgs& S, const double* q, int lane) {
+    // 1 limits, 2 manifold, 3 collision, 0 ok  (evaluated by all 32 lanes)
+    bool lim = false;
+#pragma unroll
+    for (int k = 0; k < CP_N; k++) lim |= (q[k] < cp_lo(k) || q[k] > cp_hi(k));
+    if (lim) return 1;
+    double R[CP_N * 9], P[CP_N * 3], AX[CP_N * 3], OR[CP_N * 3], SPH[(CP_S > 0 ? CP_S : 1) * 3];
+    double qq[CP_N];
+#pragma unroll
+    for (int k = 0; k < CP_N; k++) qq[k] = q[k];
+    cp_fk<double>(qq, R, P, AX, OR, SPH);
+    double qe[4], e[CP_M], s = 0.0;
+    cp_quat<double>(R + 9 * CP_EE, qe);
+    cp_task_err<double>(S.con, P + 3 * CP_EE, qe, e);
+#pragma unroll
+    for (int i = 0; i < CP_M; i++) s += e[i] * e[i];
+    if (!(sqrt(s) < S.tau_task)) return 2;
+    bool hit = false;
+    const int E = S.nb + S.ne;
+    const int total = CP_S * E + CP_P;
+    for (int c = lane; c < total; c += 32) {
+        double cl;
+        if (c < CP_S * E) {
+            int si = c / E, pi = c - si * E;
+            double x = 0, y = 0, z = 0;
+#pragma unroll
+            for (int s2 = 0; s2 < CP_S; s2++)
+                if (s2 == si) { x = SPH[3 * s2]; y = SPH[3 * s2 + 1]; z = SPH[3 * s2 + 2]; }
+            double r = cp_rad(si);
+            if (pi < S.nb) {
+                const double* lo = S.box_min + 3 * pi;
+                const double* hi = S.box_max + 3 * pi;
+                double d2 = 0.0, tt;
+                if (x < lo[0]) { tt = lo[0] - x; d2 += tt * tt; } else if (x > hi[0]) { tt = x - hi[0]; d2 += tt * tt; }
+                if (y < lo[1]) { tt = lo[1] - y; d2 += tt * tt; } else if (y > hi[1]) { tt = y - hi[1]; d2 += tt * tt; }
+                if (z < lo[2]) { tt = lo[2] - z; d2 += tt * tt; } else if (z > hi[2]) { tt = z - hi[2]; d2 += tt * tt; }
+                cl = sqrt(d2) - r;
+            } else {
+                const double* oc = S.sph_c + 3 * (pi - S.nb);
+                double dx = x - oc[0], dy = y - oc[1], dz = z - oc[2];
+                cl = sqrt((dx * dx + dy * dy) + dz * dz) - (r + S.sph_r[pi - S.nb]);
+            }
+        } else {
+            int k = c - CP_S * E;
+            int a = cp_pair_a(k), b = cp_pair_b(k);
+            double ax = 0, ay = 0, az = 0, bx = 0, by = 0, bz = 0;
+#pragma unroll
+            for (int s2 = 0; s2 < CP_S; s2++) {
+                if (s2 == a) { ax = SPH[3 * s2]; ay = SPH[3 * s2 + 1]; az = SPH[3 * s2 + 2]; }
+                if (s2 == b) { bx = SPH[3 * s2]; by = SPH[3 * s2 + 1]; bz = SPH[3 * s2 + 2]; }
+            }
+            double dx = ax - bx, dy = ay - by, dz = az - bz;
+            cl = sqrt((dx * dx + dy * dy) + dz * dz) - (cp_rad(a) + cp_rad(b));
+        }
+        hit |= cl < 0.0;
+    }
+    return __any_sync(0xffffffffu, hit) ? 3 : 0;
+}
+
+#if !CP_PARITY
+extern "C" __global__ void __launch_bounds__(64) cp_setup_kernel(const __grid_constant__ SetupArgs S) {
+    const int qi = blockIdx.x;
+    const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    QueryState& Q = S.qs[qi];
+    __shared__ int codes[2];
+    const double* q = (w == 0 ? S.starts : S.goals) + (size_t)qi * CP_N;
+    int code = cp_check_config_d(S, q, lane);
+    if (lane == 0) codes[w] = code;
+    // trees: roots (planner.py:442-443); slots past the root are NaN already
+    if (lane < CP_N) S.trees[((size_t)(2 * qi + w) * CP_N + lane) * S.cap + 0] = (float)q[lane];
+    if (lane == 0) S.parents[(size_t)(2 * qi + w) * S.cap] = 0;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        int c = codes[0] ? codes[0] : (codes[1] ? 3 + codes[1] : 0);
+        Q.setup_code = c;
+        Q.seed_offset = S.seeds[qi];
+        Q.count[0] = 1; Q.count[1] = 1;
+        Q.next_sample = 0;
+        Q.solved = 0; Q.stop = c != 0; Q.timed_out = 0; Q.overflow = 0; Q.exhausted = 0;
+        Q.meet[0] = -1; Q.meet[1] = -1;
+        for (int i = 0; i < ST_NSTAT; i++) Q.stats[i] = 0ull;
+        Q.t0_ns = cp_clock_ns();
+        Q.t_end_ns = 0;
+    }
+}
+
+// Reset the node slots used by the previous run to NaN (publication marker).
+extern "C" __global__ void cp_reset_kernel(QueryState* qs, float* trees, int cap, int nq) {
+    for (int qk = blockIdx.y; qk < 2 * nq; qk += gridDim.y) {
+        const int qi = qk >> 1, k = qk & 1;
+        const int h = min(qs[qi].hwm[k], cap);
+        float* base = trees + (size_t)qk * CP_N * cap;
+        const float nan = __int_as_float(0x7fffffff);
+        for (int d = 0; d < CP_N; d++)
+            for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < h; i += gridDim.x * blockDim.x)
+                base[(size_t)d * cap + i] = nan;
+    }
+}
+
+// Path extraction (planner.py:488-505) into the result area (mapped host
+// memory).  One warp per query; lane 0 walks the parent chains.
+
+extern "C" __global__ void cp_extract_kernel(QueryState* qs, const float* trees, const int* parents, int cap,
+                                             int nq, QueryOut* out, float* paths, int* sources, int path_cap) {
+    const int qi = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+    if (qi >= nq || (threadIdx.x & 31) != 0) return;
+    QueryState& Q = qs[qi];
+    QueryOut& O = out[qi];
+    O.setup_code = Q.setup_code;
+    O.n_nodes[0] = min(Q.count[0], cap);
+    O.n_nodes[1] = min(Q.count[1], cap);
+    Q.hwm[0] = O.n_nodes[0];
+    Q.hwm[1] = O.n_nodes[1];
+    for (int i = 0; i < ST_NSTAT; i++) O.stats[i] = Q.stats[i];
+    const u64 tend = Q.solved ? Q.t_end_ns : cp_clock_ns();
+    O.device_ms = (double)(tend - Q.t0_ns) * 1e-6;
+    O.path_len = 0;
+    if (Q.setup_code != 0) { O.status = -1; return; }
+    if (!Q.solved) {
+        O.status = Q.timed_out ? 1 : (Q.overflow ? 3 : 2);
+        return;
+    }
+    O.status = 0;
+    const float* ts = trees + (size_t)(2 * qi) * CP_N * cap;
+    const float* tg = trees + (size_t)(2 * qi + 1) * CP_N * cap;
+    const int* ps = parents + (size_t)(2 * qi) * cap;
+    const int* pg = parents + (size_t)(2 * qi + 1) * cap;
+    float* path = paths + (size_t)qi * path_cap * CP_N;
+    int* src = sources + (size_t)qi * path_cap;
+    int ca = 1, cb = 1;
+    for (int i = Q.meet[0]; ps[i] != i && ca <= path_cap; i = ps[i]) ca++;
+    for (int i = Q.meet[1]; pg[i] != i && cb <= path_cap; i = pg[i]) cb++;
+    bool same = true;
+    for (int d = 0; d < CP_N; d++) same &= ts[(size_t)d * cap + Q.meet[0]] == tg[(size_t)d * cap + Q.meet[1]];
+    const int skip = same ? 1 : 0;
+    const int len = ca + cb - skip;
+    if (len > path_cap) { O.status = 4; return; }
+    int k = ca - 1;
+    for (int i = Q.meet[0];; i = ps[i]) {
+        for (int d = 0; d < CP_N; d++) path[(size_t)k * CP_N + d] = ts[(size_t)d * cap + i];
+        k--;
+        if (ps[i] == i) break;
+    }
+    k = ca;
+    int first = 1;
+    for (int i = Q.meet[1];; i = pg[i]) {
+        if (!(first && skip)) {
+            for (int d = 0; d < CP_N; d++) path[(size_t)k * CP_N + d] = tg[(size_t)d * cap + i];
+            k++;
+        }
+        first = 0;
+        if (pg[i] == i) break;
+    }
+    int s = 0;
+    for (int i = 0; i < ca - 1; i++) src[s++] = 0;
+    if (cb - skip > 0) {
+        src[s++] = skip ? 2 : 1;
+        for (int i = 0; i < cb - skip - 1; i++) src[s++] = 2;
+    }
+    O.path_len = len;
+}
+
+#endif  // !CP_PARITY
+#if CP_PARITY
+
+// ===========================================================================
+// Parity / batch entry kernels (one team per item)
+// ===========================================================================
+template <class T>
+__device__ __forceinline__ void cp_fk_item(const double* qin, double* frames, double* axes, double* orgs,
+                                           double* ee, double* sph, int i) {
+    T q[CP_N];
+#pragma unroll
+    for (int k = 0; k < CP_N; k++) q[k] = (T)qin[(size_t)i * CP_N + k];
+    T R[CP_N * 9], P[CP_N * 3], AX[CP_N * 3], OR[CP_N * 3], SPH[(CP_S > 0 ? CP_S : 1) * 3];
+    cp_fk<T>(q, R, P, AX, OR, SPH);
+    if (frames)
+        for (int j = 0; j < CP_N; j++) {
+            for (int k = 0; k < 9; k++) frames[((size_t)i * CP_N + j) * 12 + k] = R[9 * j + k];
+            for (int k = 0; k < 3; k++) frames[((size_t)i * CP_N + j) * 12 + 9 + k] = P[3 * j + k];
+        }
+    if (axes)
+        for (int j = 0; j < 3 * CP_N; j++) { axes[(size_t)i * 3 * CP_N + j] = AX[j]; orgs[(size_t)i * 3 * CP_N + j] = OR[j]; }
+    if (ee) {
+        T qe[4];
+        cp_quat<T>(R + 9 * CP_EE, qe);
+        for (int k = 0; k < 3; k++) ee[(size_t)i * 7 + k] = P[3 * CP_EE + k];
+        for (int k = 0; k < 4; k++) ee[(size_t)i * 7 + 3 + k] = qe[k];
+    }
+    if (sph)
+        for (int s = 0; s < CP_S; s++) {
+            for (int k = 0; k < 3; k++) sph[((size_t)i * CP_S + s) * 4 + k] = SPH[3 * s + k];
+            sph[((size_t)i * CP_S + s) * 4 + 3] = cp_rad(s);
+        }
+}
+
+extern "C" __global__ void cp_fk_kernel(int B, int fp64, const double* q, double* frames, double* axes,
+                                        double* orgs, double* ee, double* sph) {
+    int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= B) return;
+    if (fp64) cp_fk_item<double>(q, frames, axes, orgs, ee, sph, i);
+    else cp_fk_item<float>(q, frames, axes, orgs, ee, sph, i);
+}
+
+template <class T>
+__device__ __forceinline__ void cp_tej_item(const Con<T>& c, const double* qin, double* e_out, double* J_out, int i) {
+    T q[CP_N], e[CP_M], J[CP_M][CP_N];
+#pragma unroll
+    for (int k = 0; k < CP_N; k++) q[k] = (T)qin[(size_t)i * CP_N + k];
+    cp_err_jac<T>(c, q, e, J);
+    for (int r = 0; r < CP_M; r++) {
+        e_out[(size_t)i * CP_M + r] = e[r];
+        for (int k = 0; k < CP_N; k++) J_out[((size_t)i * CP_M + r) * CP_N + k] = J[r][k];
+    }
+}
+
+extern "C" __global__ void cp_tej_kernel(int B, int fp64, Con<float> cf, Con<double> cd, const double* q,
+                                         double* e, double* J) {
+    int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= B) return;
+    if (fp64) cp_tej_item<double>(cd, q, e, J, i);
+    else cp_tej_item<float>(cf, q, e, J, i);
+}
+
+// task error at given poses (reference task_error_at), FP64
+extern "C" __global__ void cp_err_at_kernel(int B, Con<double> cd, const double* pose, double* e) {
+    int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= B) return;
+    double p[3], qe[4], ee[CP_M];
+    for (int k = 0; k < 3; k++) p[k] = pose[(size_t)i * 7 + k];
+    for (int k = 0; k < 4; k++) qe[k] = pose[(size_t)i * 7 + 3 + k];
+    cp_task_err<double>(cd, p, qe, ee);
+    for (int r = 0; r < CP_M; r++) e[(size_t)i * CP_M + r] = ee[r];
+}
+
+// Newton projection of single configurations, FP64 (projection.py:231-254)
+extern "C" __global__ void cp_project_config_kernel(int B, Con<double> cd, double tau, double lam, int max_iters,
+                                                    double* q_io, int* ok_out) {
+    int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= B) return;
+    double q[CP_N];
+    for (int k = 0; k < CP_N; k++) q[k] = q_io[(size_t)i * CP_N + k];
+    int ok = 0;
+    for (int it = 0; it < max_iters; it++) {
+        bool fin = true;
+        for (int k = 0; k < CP_N; k++) fin &= cp_finite(q[k]);
+        if (!fin) break;
+        double e[CP_M], J[CP_M][CP_N], st[CP_N], s = 0.0;
+        cp_err_jac<double>(cd, q, e, J);
+        for (int r = 0; r < CP_M; r++) s += e[r] * e[r];
+        if (sqrt(s) < tau) {
+            double qc[CP_N];
+            bool moved = false;
+            for (int k = 0; k < CP_N; k++) {
+                qc[k] = fmin(fmax(q[k], cp_lo(k)), cp_hi(k));
+                moved |= !(qc[k] == q[k]);
+            }
+            if (!moved) { ok = 1; break; }
+            double R[CP_N * 9], P[CP_N * 3], AX[CP_N * 3], OR[CP_N * 3], SPH[(CP_S > 0 ? CP_S : 1) * 3], qe[4], e2[CP_M];
+            cp_fk<double>(qc, R, P, AX, OR, SPH);
+            cp_quat<double>(R + 9 * CP_EE, qe);
+            cp_task_err<double>(cd, P + 3 * CP_EE, qe, e2);
+            double s2 = 0.0;
+            for (int r = 0; r < CP_M; r++) s2 += e2[r] * e2[r];
+            for (int k = 0; k < CP_N; k++) q[k] = qc[k];
+            ok = sqrt(s2) < tau;
+            break;
+        }
+        if (!cp_damped<double, CP_M>(J, e, lam, st)) break;
+        for (int k = 0; k < CP_N; k++) q[k] = q[k] - st[k];
+    }
+    for (int k = 0; k < CP_N; k++) q_io[(size_t)i * CP_N + k] = q[k];
+    ok_out[i] = ok;
+}
+
+// Exact endpoint-style checks for a batch of configurations, FP64:
+// 0 ok, 1 limits, 2 manifold, 3 collision.  One warp per configuration.
+extern "C" __global__ void cp_check_config_kernel(int B, const __grid_constant__ SetupArgs S, const double* q, int* code) {
+    int i = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+    if (i >= B) return;
+    int c = cp_check_config_d(S, q + (size_t)i * CP_N, threadIdx.x & 31);
+    if ((threadIdx.x & 31) == 0) code[i] = c;
+}
+
+// Batch motion validation with reference semantics (exact counters).
+// One team per motion; wps (B, W, CP_N) FP64 in, scene staged in smem.
+extern "C" __global__ void __launch_bounds__(CP_NTHREADS, 1)
+cp_validate_kernel(int B, int W, int flag_on, float margin, SceneSm scg, const double* wps, int* valid,
+                   int* first_bad, i64* performed, i64* gpu_checks) {
+    extern __shared__ float4 cp_smem[];
+    SceneSm sc = cp_stage_scene(scg, cp_smem);
+    TeamWS* wsa = reinterpret_cast<TeamWS*>(cp_smem + 2 * scg.nb + scg.ne);
+    Team tm;
+    const int tpc = CP_NTHREADS / CP_G;
+    const int team_in_cta = (threadIdx.x >> 5) * (32 / CP_G) + (threadIdx.x & 31) / CP_G;
+    TeamWS& ws = wsa[team_in_cta];
+    for (int i = blockIdx.x * tpc + team_in_cta; i < B; i += gridDim.x * tpc) {
+        tm.sync();
+        if ((int)tm.lane < W)
+            for (int k = 0; k < CP_N; k++) ws.seg[tm.lane][k] = (float)wps[((size_t)i * W + tm.lane) * CP_N + k];
+        tm.sync();
+        ValOut o = cp_validate(tm, ws.seg, W, 0, flag_on != 0, margin, sc);
+        if (tm.lane == 0) {
+            valid[i] = o.valid;
+            first_bad[i] = o.first_bad;
+            performed[i] = o.performed;
+            if (gpu_checks) gpu_checks[i] = o.gpu_checks;
+        }
+    }
+}
+
+// Batch segment projection (parallel / literal-gap / sequential), FP32.
+extern "C" __global__ void __launch_bounds__(CP_NTHREADS, 1)
+cp_project_kernel(int B, int W, Con<float> con, ProjArgs pa, const float* tau_sm, const double* wps, double* xi,
+                  int* ok, int* iters, int* prog, float* trace, int* trace_prog) {
+    extern __shared__ float4 cp_smem[];
+    TeamWS* wsa = reinterpret_cast<TeamWS*>(cp_smem);
+    Team tm;
+    const int tpc = CP_NTHREADS / CP_G;
+    const int team_in_cta = (threadIdx.x >> 5) * (32 / CP_G) + (threadIdx.x & 31) / CP_G;
+    TeamWS& ws = wsa[team_in_cta];
+    for (int i = blockIdx.x * tpc + team_in_cta; i < B; i += gridDim.x * tpc) {
+        tm.sync();
+        if ((int)tm.lane < W)
+            for (int k = 0; k < CP_N; k++) ws.seg[tm.lane][k] = (float)wps[((size_t)i * W + tm.lane) * CP_N + k];
+        tm.sync();
+        ProjArgs p = pa;
+        if (tau_sm) p.tau_sm_fixed = tau_sm[i];
+        int it, pr;
+        bool good = cp_project(tm, ws.seg, W, con, p, &it, &pr,
+                               trace ? trace + (size_t)i * pa.max_iters * W * CP_N : nullptr,
+                               trace ? trace_prog + (size_t)i * pa.max_iters : nullptr);
+        tm.sync();
+        if ((int)tm.lane < W)
+            for (int k = 0; k < CP_N; k++) xi[((size_t)i * W + tm.lane) * CP_N + k] = ws.seg[tm.lane][k];
+        if (tm.lane == 0) { ok[i] = good; iters[i] = it; prog[i] = pr; }
+    }
+}
+
+// Batch nearest neighbour over an SoA node array (planner.py:198-201).
+extern "C" __global__ void __launch_bounds__(CP_NTHREADS, 1)
+cp_nearest_kernel(int count, int cap, const float* nodes, int Q, const float* queries, int* idx) {
+    Team tm;
+    const int tpc = CP_NTHREADS / CP_G;
+    const int team_in_cta = (threadIdx.x >> 5) * (32 / CP_G) + (threadIdx.x & 31) / CP_G;
+    for (int i = blockIdx.x * tpc + team_in_cta; i < Q; i += gridDim.x * tpc) {
+        int r = cp_nearest(tm, nodes, cap, count, queries + (size_t)i * CP_N);
+        if (tm.lane == 0) idx[i] = r;
+    }
+}
+
+// Halton samples, FP64 bit-exact (sampling.py:65-81): out[i] = sample at
+// index first + i.
+extern "C" __global__ void cp_halton_kernel(int count, i64 first, i64 seed_offset, const double* lo,
+                                            const double* hi, double* out) {
+    int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= count) return;
+    for (int k = 0; k < CP_N; k++) {
+        double u = cp_radical_inverse(first + i + seed_offset, cp_prime(k));
+        out[(size_t)i * CP_N + k] = __dadd_rn(lo[k], __dmul_rn(__dsub_rn(hi[k], lo[k]), u));
+    }
+}
+
+#endif  // CP_PARITY
+
+#if !CP_PARITY
+// Dense edges of a solved path, re-derived on the device exactly as the
+// planner certified them (planner.py:508-523 revalidate_path).  One team per
+// edge; nodes (E+1, CP_N) FP32, sources (E): 0 start, 1 junction, 2 goal.
+extern "C" __global__ void __launch_bounds__(CP_NTHREADS, 1)
+cp_dense_kernel(int E, const __grid_constant__ PlanArgs A, const float* nodes, const int* sources, float* dense,
+                int* ok) {
+    extern __shared__ float4 cp_smem[];
+    SceneSm sc = cp_stage_scene(A.scene_g, cp_smem);
+    TeamWS* wsa = reinterpret_cast<TeamWS*>(cp_smem + 2 * A.scene_g.nb + A.scene_g.ne);
+    Team tm;
+    const int tpc = CP_NTHREADS / CP_G;
+    const int team_in_cta = (threadIdx.x >> 5) * (32 / CP_G) + (threadIdx.x & 31) / CP_G;
+    TeamWS& ws = wsa[team_in_cta];
+    for (int e = blockIdx.x * tpc + team_in_cta; e < E; e += gridDim.x * tpc) {
+        const bool rev = sources[e] == 2;
+        const float* x = nodes + (size_t)e * CP_N;
+        const float* y = nodes + (size_t)(e + 1) * CP_N;
+        tm.sync();
+        if ((int)tm.lane < CP_N) {
+            ws.qr[tm.lane] = rev ? y[tm.lane] : x[tm.lane];
+            ws.qn[tm.lane] = rev ? x[tm.lane] : y[tm.lane];
+        }
+        tm.sync();
+        Stats st;
+        bool good = cp_derive_edge(tm, ws, A, sc, ws.qr, ws.qn, st);
+        tm.sync();
+        if ((int)tm.lane < A.W) {
+            int row = rev ? A.W - 1 - (int)tm.lane : (int)tm.lane;
+            for (int k = 0; k < CP_N; k++) dense[((size_t)e * A.W + row) * CP_N + k] = ws.seg[tm.lane][k];
+        }
+        if (tm.lane == 0) ok[e] = good;
+    }
+}
+#endif  // !CP_PARITY

@@ -1,0 +1,99 @@
+// cprrtc_shared.h -- structs shared bit-for-bit by the host runtime
+// (runtime.cpp) and the NVRTC device code (prepended to cprrtc_device.cuh).
+// Plain C++ only: compiled by both g++/nvcc (host) and NVRTC (device).
+#ifndef CPRRTC_SHARED_H
+#define CPRRTC_SHARED_H
+
+typedef unsigned long long u64;
+typedef long long i64;
+
+// packed constraint (maniplan/constraints.py:123-176)
+template <class T> struct Con {
+    T anchor[3];
+    T offset;
+    T b1[3], b2[3];
+    T qf[4];
+    T rft[9];
+    T weight;
+};
+
+// projection parameters (maniplan/projection.py:75-90), FP32 + device margins
+struct ProjArgs {
+    float alpha, lam;
+    float tau_task;       // reference tolerance (inf = unconstrained)
+    float tau_task_dev;   // tau_task * (1 - 1e-3) - 2e-6: FP32 safety margin
+    float tau_sm_fixed;   // > 0: fixed tau_sm, else auto (1.5 x max initial gap)
+    int max_iters;
+    int mode;             // 0 parallel, 1 literal-gap, 2 sequential ("naive")
+};
+
+// scene: boxes as centre / half extent, spheres as centre + radius (FP32)
+struct SceneSm {
+    const float4* box_c;
+    const float4* box_h;
+    const float4* sph;
+    int nb, ne;
+};
+
+enum { ST_ITER = 0, ST_ATT, ST_ADDED, ST_PFAIL, ST_CREJ, ST_CCPERF, ST_CCPOSS, ST_GPUCHK, ST_NSTAT };
+
+// per-query planner state in HBM
+struct QueryState {
+    i64 seed_offset;
+    int count[2];          // tree node counters (atomic append)
+    int hwm[2];            // nodes used by the previous run (NaN refill)
+    int next_sample;       // Halton index counter (= reference iteration)
+    int solved, stop, timed_out, overflow, exhausted;
+    int meet[2];           // meet node in the start / goal tree
+    int setup_code;        // endpoint check (planner.py:416-427)
+    int pad;
+    u64 t0_ns, t_end_ns;
+    u64 stats[ST_NSTAT];
+};
+
+struct PlanArgs {
+    QueryState* qs;
+    float* trees;          // (nq, 2, CP_N, cap) SoA
+    int* parents;          // (nq, 2, cap)
+    int cap;
+    int nq;
+    int* queue_head;
+    int* team_counter;
+    SceneSm scene_g;       // global-memory scene (staged to smem by each CTA)
+    Con<float> con;
+    ProjArgs pa;
+    int W;
+    float step, tol, margin;
+    int flag_on;
+    int max_iterations, max_connect;
+    i64 budget_ns;         // <= 0: no time budget (deterministic)
+};
+
+struct SetupArgs {
+    QueryState* qs;
+    const double* starts;   // (nq, CP_N)
+    const double* goals;
+    const i64* seeds;
+    float* trees;
+    int* parents;
+    int cap;
+    Con<double> con;
+    double tau_task;
+    const double* box_min;  // (nb,3) FP64 scene for the exact endpoint test
+    const double* box_max;
+    const double* sph_c;
+    const double* sph_r;
+    int nb, ne;
+};
+
+struct QueryOut {
+    int status;            // 0 Solved, 1 TimedOut, 2 IterLimit, 3 tree full, 4 path overflow, -1 setup
+    int setup_code;
+    int path_len;
+    int n_nodes[2];
+    int pad;
+    double device_ms;
+    u64 stats[ST_NSTAT];
+};
+
+#endif

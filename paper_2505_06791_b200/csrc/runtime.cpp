@@ -1,0 +1,1173 @@
+// runtime.cpp -- host runtime and C ABI of libcprrtc.so (include/cprrtc.h).
+//
+// Owns, per context: the CUDA stream, the robot description and its generated
+// FK source, NVRTC-compiled modules (one per constraint kind x orientation
+// lock x team width, cached on disk as sm_100a cubins), the FP32 scene in
+// HBM, the planner's query states and SoA trees, and mapped pinned result
+// buffers.  CUDA runtime API (cudart_static) for memory and streams; the
+// driver API (module load, launch) is reached through
+// cudaGetDriverEntryPoint and NVRTC through dlopen, so the library loads on a
+// machine without a GPU driver (the CPU test suite checks its exports).
+#include <cuda.h>
+#include <cuda_runtime.h>
+#include <dlfcn.h>
+#include <nvrtc.h>
+#include <sys/stat.h>
+#include <unistd.h>
+
+#include <cmath>
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
+#include <fstream>
+#include <map>
+#include <memory>
+#include <mutex>
+#include <sstream>
+#include <string>
+#include <tuple>
+#include <vector>
+
+#include "../../include/cprrtc.h"
+#include "device/cprrtc_shared.h"
+
+namespace cprrtc {
+std::string codegen_robot(const cprrtc_robot& r, std::string* err);
+cudaError_t launch_clearance(int B, int kind, const double* a, const double* b, double* out, cudaStream_t st);
+cudaError_t launch_damped_step(int B, int m, int n, const double* J, const double* e, double lam, double* step,
+                               int32_t* ok, cudaStream_t st);
+}  // namespace cprrtc
+
+namespace {
+
+const char* kDeviceSrc =
+#include "device_src.inc"
+    ;
+const char* kSharedSrc =
+#include "shared_src.inc"
+    ;
+
+constexpr int kThreads = 256;   // CTA size of every team kernel
+
+thread_local std::string g_err;
+
+int fail(int code, const std::string& msg) {
+    g_err = msg;
+    return code;
+}
+
+#define CUDA_TRY(expr)                                                                        \
+    do {                                                                                      \
+        cudaError_t _e = (expr);                                                              \
+        if (_e != cudaSuccess)                                                                \
+            return fail(CPRRTC_ECUDA, std::string(#expr ": ") + cudaGetErrorString(_e));      \
+    } while (0)
+
+// ---------------------------------------------------------------------------
+// driver API entry points (via the runtime; no link-time libcuda dependency)
+// ---------------------------------------------------------------------------
+struct Driver {
+    CUresult (*moduleLoadData)(CUmodule*, const void*) = nullptr;
+    CUresult (*moduleUnload)(CUmodule) = nullptr;
+    CUresult (*moduleGetFunction)(CUfunction*, CUmodule, const char*) = nullptr;
+    CUresult (*launchKernel)(CUfunction, unsigned, unsigned, unsigned, unsigned, unsigned, unsigned, unsigned,
+                             CUstream, void**, void**) = nullptr;
+    CUresult (*funcSetAttribute)(CUfunction, CUfunction_attribute, int) = nullptr;
+    CUresult (*occupancy)(int*, CUfunction, int, size_t) = nullptr;
+    CUresult (*getErrorString)(CUresult, const char**) = nullptr;
+    bool ok = false;
+};
+
+template <class F>
+bool entry(const char* name, F& fn) {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint(name, &p, cudaEnableDefault, &q) != cudaSuccess || !p) return false;
+    fn = reinterpret_cast<F>(p);
+    return true;
+}
+
+Driver& drv() {
+    static Driver d;
+    static std::once_flag once;
+    std::call_once(once, [] {
+        d.ok = entry("cuModuleLoadData", d.moduleLoadData) && entry("cuModuleUnload", d.moduleUnload) &&
+               entry("cuModuleGetFunction", d.moduleGetFunction) && entry("cuLaunchKernel", d.launchKernel) &&
+               entry("cuFuncSetAttribute", d.funcSetAttribute) &&
+               entry("cuOccupancyMaxActiveBlocksPerMultiprocessor", d.occupancy) &&
+               entry("cuGetErrorString", d.getErrorString);
+    });
+    return d;
+}
+
+std::string cu_err(CUresult r) {
+    const char* s = nullptr;
+    if (drv().getErrorString) drv().getErrorString(r, &s);
+    return s ? s : ("CUresult " + std::to_string((int)r));
+}
+
+// ---------------------------------------------------------------------------
+// NVRTC (dlopen)
+// ---------------------------------------------------------------------------
+struct Nvrtc {
+    nvrtcResult (*create)(nvrtcProgram*, const char*, const char*, int, const char* const*, const char* const*);
+    nvrtcResult (*compile)(nvrtcProgram, int, const char* const*);
+    nvrtcResult (*logSize)(nvrtcProgram, size_t*);
+    nvrtcResult (*log)(nvrtcProgram, char*);
+    nvrtcResult (*cubinSize)(nvrtcProgram, size_t*);
+    nvrtcResult (*cubin)(nvrtcProgram, char*);
+    nvrtcResult (*destroy)(nvrtcProgram*);
+    nvrtcResult (*version)(int*, int*);
+    const char* (*errstr)(nvrtcResult);
+    bool ok = false;
+    std::string why;
+};
+
+Nvrtc& nvrtc() {
+    static Nvrtc n;
+    static std::once_flag once;
+    std::call_once(once, [] {
+        void* h = dlopen("libnvrtc.so.12", RTLD_NOW | RTLD_GLOBAL);
+        if (!h) h = dlopen("libnvrtc.so", RTLD_NOW | RTLD_GLOBAL);
+        if (!h) {
+            n.why = std::string("cannot load libnvrtc: ") + dlerror();
+            return;
+        }
+#define SYM(field, name) n.field = reinterpret_cast<decltype(n.field)>(dlsym(h, name))
+        SYM(create, "nvrtcCreateProgram");
+        SYM(compile, "nvrtcCompileProgram");
+        SYM(logSize, "nvrtcGetProgramLogSize");
+        SYM(log, "nvrtcGetProgramLog");
+        SYM(cubinSize, "nvrtcGetCUBINSize");
+        SYM(cubin, "nvrtcGetCUBIN");
+        SYM(destroy, "nvrtcDestroyProgram");
+        SYM(version, "nvrtcVersion");
+        SYM(errstr, "nvrtcGetErrorString");
+#undef SYM
+        n.ok = n.create && n.compile && n.logSize && n.log && n.cubinSize && n.cubin && n.destroy && n.version &&
+               n.errstr;
+        if (!n.ok) n.why = "libnvrtc is missing symbols";
+    });
+    return n;
+}
+
+uint64_t fnv1a(const std::string& s, uint64_t h = 1469598103934665603ull) {
+    for (unsigned char c : s) {
+        h ^= c;
+        h *= 1099511628211ull;
+    }
+    return h;
+}
+
+std::string lib_dir() {
+    Dl_info info;
+    if (dladdr(reinterpret_cast<void*>(&lib_dir), &info) && info.dli_fname) {
+        std::string p(info.dli_fname);
+        size_t k = p.rfind('/');
+        if (k != std::string::npos) return p.substr(0, k);
+    }
+    return ".";
+}
+
+std::string cache_dir() {
+    const char* e = getenv("CPRRTC_CACHE_DIR");
+    std::string d = e && *e ? e : lib_dir() + "/_nvrtc_cache";
+    mkdir(d.c_str(), 0755);
+    return d;
+}
+
+const char* kArch = "--gpu-architecture=sm_100a";
+
+// Compile (or fetch from the disk cache) a cubin for source `src`.
+int nvrtc_cubin(const std::string& src, const std::string& name, std::vector<char>* cubin, std::string* path_out) {
+    Nvrtc& nv = nvrtc();
+    if (!nv.ok) return fail(CPRRTC_ENVRTC, nv.why);
+    int maj = 0, min = 0;
+    nv.version(&maj, &min);
+    std::vector<const char*> opts = {kArch, "-std=c++17", "-lineinfo", "-default-device", "--dopt=on",
+                                     "--extra-device-vectorization"};
+    std::string key = src + "|" + std::to_string(maj) + "." + std::to_string(min);
+    for (auto o : opts) key += std::string("|") + o;
+    char hex[32];
+    std::snprintf(hex, sizeof hex, "%016llx", (unsigned long long)fnv1a(key));
+    std::string path = cache_dir() + "/" + name + "-" + hex + ".cubin";
+    if (path_out) *path_out = path;
+    {
+        std::ifstream f(path, std::ios::binary);
+        if (f) {
+            cubin->assign(std::istreambuf_iterator<char>(f), std::istreambuf_iterator<char>());
+            if (!cubin->empty()) return 0;
+        }
+    }
+    nvrtcProgram prog;
+    nvrtcResult r = nv.create(&prog, src.c_str(), (name + ".cu").c_str(), 0, nullptr, nullptr);
+    if (r != NVRTC_SUCCESS) return fail(CPRRTC_ENVRTC, std::string("nvrtcCreateProgram: ") + nv.errstr(r));
+    r = nv.compile(prog, (int)opts.size(), opts.data());
+    size_t ls = 0;
+    nv.logSize(prog, &ls);
+    std::string logtxt(ls, '\0');
+    if (ls) nv.log(prog, &logtxt[0]);
+    if (r != NVRTC_SUCCESS) {
+        nv.destroy(&prog);
+        return fail(CPRRTC_ENVRTC, "NVRTC compile failed:\n" + logtxt);
+    }
+    size_t cs = 0;
+    nv.cubinSize(prog, &cs);
+    cubin->resize(cs);
+    nv.cubin(prog, cubin->data());
+    nv.destroy(&prog);
+    std::string tmp = path + ".tmp" + std::to_string(getpid());
+    {
+        std::ofstream f(tmp, std::ios::binary);
+        f.write(cubin->data(), (std::streamsize)cubin->size());
+    }
+    std::rename(tmp.c_str(), path.c_str());
+    return 0;
+}
+
+// ---------------------------------------------------------------------------
+// device buffers
+// ---------------------------------------------------------------------------
+struct DevBuf {
+    void* p = nullptr;
+    size_t bytes = 0;
+    ~DevBuf() {
+        if (p) cudaFree(p);
+    }
+    int ensure(size_t need) {
+        if (need <= bytes && p) return 0;
+        if (p) cudaFree(p);
+        p = nullptr;
+        bytes = 0;
+        size_t b = need < 256 ? 256 : need;
+        cudaError_t e = cudaMalloc(&p, b);
+        if (e != cudaSuccess) return fail(CPRRTC_ECUDA, std::string("cudaMalloc: ") + cudaGetErrorString(e));
+        bytes = b;
+        return 0;
+    }
+    template <class T> T* as() const { return static_cast<T*>(p); }
+};
+
+struct HostBuf {   // pinned, mapped
+    void* h = nullptr;
+    void* d = nullptr;
+    size_t bytes = 0;
+    ~HostBuf() {
+        if (h) cudaFreeHost(h);
+    }
+    int ensure(size_t need) {
+        if (need <= bytes && h) return 0;
+        if (h) cudaFreeHost(h);
+        h = d = nullptr;
+        bytes = 0;
+        size_t b = need < 256 ? 256 : need;
+        cudaError_t e = cudaHostAlloc(&h, b, cudaHostAllocMapped);
+        if (e != cudaSuccess) return fail(CPRRTC_ECUDA, std::string("cudaHostAlloc: ") + cudaGetErrorString(e));
+        e = cudaHostGetDevicePointer(&d, h, 0);
+        if (e != cudaSuccess) return fail(CPRRTC_ECUDA, std::string("cudaHostGetDevicePointer: ") + cudaGetErrorString(e));
+        bytes = b;
+        return 0;
+    }
+    template <class T> T* host() const { return static_cast<T*>(h); }
+    template <class T> T* dev() const { return static_cast<T*>(d); }
+};
+
+struct Module {
+    CUmodule mod = nullptr;
+    int G = 16, kind = 0, orient = 0;
+    size_t ws_bytes = 0;   // sizeof(TeamWS)
+    std::map<std::string, CUfunction> fn;
+    int plan_occ = 0;      // resident plan CTAs per SM
+    std::string cubin_path;
+};
+
+struct Ctx {
+    int device = 0;
+    int sms = 148;
+    cudaStream_t stream = nullptr;
+    int n = 0, S = 0, P = 0, NP = 0;
+    std::string robot_src;
+    std::vector<double> lo, hi;
+    // scene
+    int nb = 0, ne = 0;
+    DevBuf sc_box_c, sc_box_h, sc_sph, sc_bmin, sc_bmax, sc_sc, sc_sr;
+    // constraint
+    int kind = 0, orient = 0;
+    Con<float> conf{};
+    Con<double> cond{};
+    double tau_task = INFINITY;
+    std::map<std::tuple<int, int, int, int>, std::unique_ptr<Module>> modules;
+    // planner buffers
+    int nq_alloc = 0, cap_alloc = 0;
+    DevBuf qs, trees, parents, counters, d_starts, d_goals, d_seeds;
+    HostBuf h_in, h_out, h_paths, h_src;
+    int path_cap = 0;
+    PlanArgs last_args{};
+    Module* last_mod = nullptr;
+    int last_nq = 0;
+    DevBuf dense_buf, dense_ok, dense_nodes;
+    // scratch for parity/batch entry points
+    DevBuf scratch[10];
+    cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};
+    double last_total_ms = 0, last_plan_ms = 0;
+    int64_t launches = 0;
+};
+
+int set_device(Ctx* c) {
+    CUDA_TRY(cudaSetDevice(c->device));
+    return 0;
+}
+
+std::string prelude(const Ctx* c, int G, int kind, int orient, int parity) {
+    std::ostringstream os;
+    os << "#define CP_G " << G << "\n#define CP_KIND " << kind << "\n#define CP_ORIENT " << orient
+       << "\n#define CP_NTHREADS " << kThreads << "\n#define CP_PARITY " << parity << "\n";
+    os << kSharedSrc << "\n" << c->robot_src << "\n";
+    return os.str();
+}
+
+const std::vector<const char*> kPlanKernels = {"cp_plan_kernel", "cp_setup_kernel", "cp_reset_kernel",
+                                                "cp_extract_kernel", "cp_dense_kernel"};
+const std::vector<const char*> kParityKernels = {"cp_fk_kernel",           "cp_tej_kernel",
+                                                  "cp_err_at_kernel",       "cp_project_config_kernel",
+                                                  "cp_check_config_kernel", "cp_validate_kernel",
+                                                  "cp_project_kernel",      "cp_nearest_kernel",
+                                                  "cp_halton_kernel"};
+
+std::string module_name(int G, int kind, int orient, int parity) {
+    char name[64];
+    std::snprintf(name, sizeof name, "cprrtc-%s-g%d-k%d-o%d", parity ? "parity" : "plan", G, kind, orient);
+    return name;
+}
+
+int get_module(Ctx* c, int G, int kind, int orient, int parity, Module** out) {
+    auto key = std::make_tuple(G, kind, orient, parity);
+    auto it = c->modules.find(key);
+    if (it != c->modules.end()) {
+        *out = it->second.get();
+        return 0;
+    }
+    if (!drv().ok) return fail(CPRRTC_ECUDA, "CUDA driver entry points unavailable");
+    std::string src = prelude(c, G, kind, orient, parity) + kDeviceSrc;
+    std::vector<char> cubin;
+    auto m = std::make_unique<Module>();
+    int rc = nvrtc_cubin(src, module_name(G, kind, orient, parity), &cubin, &m->cubin_path);
+    if (rc) return rc;
+    CUresult r = drv().moduleLoadData(&m->mod, cubin.data());
+    if (r != CUDA_SUCCESS) return fail(CPRRTC_ECUDA, "cuModuleLoadData: " + cu_err(r));
+    for (const char* k : parity ? kParityKernels : kPlanKernels) {
+        CUfunction f;
+        r = drv().moduleGetFunction(&f, m->mod, k);
+        if (r != CUDA_SUCCESS) return fail(CPRRTC_ECUDA, std::string("cuModuleGetFunction ") + k + ": " + cu_err(r));
+        m->fn[k] = f;
+    }
+    m->G = G;
+    m->kind = kind;
+    m->orient = orient;
+    m->ws_bytes = (size_t)(G + 7) * c->NP * sizeof(float);
+    for (const char* k : {"cp_plan_kernel", "cp_validate_kernel", "cp_project_kernel", "cp_dense_kernel"})
+        if (m->fn.count(k)) drv().funcSetAttribute(m->fn[k], CU_FUNC_ATTRIBUTE_MAX_DYNAMIC_SHARED_SIZE_BYTES, 200 * 1024);
+    *out = m.get();
+    c->modules[key] = std::move(m);
+    return 0;
+}
+
+int cur_module(Ctx* c, int W, int parity, Module** m) {
+    if (W < 2 || W > 32) return fail(CPRRTC_ELIMIT, "width must be in [2, 32] for this build");
+    return get_module(c, W <= 16 ? 16 : 32, c->kind, c->orient, parity, m);
+}
+
+int launch(Ctx* c, Module* m, const char* k, unsigned gx, unsigned gy, unsigned bx, size_t smem, void** args) {
+    CUresult r = drv().launchKernel(m->fn[k], gx, gy, 1, bx, 1, 1, (unsigned)smem, (CUstream)c->stream, args, nullptr);
+    if (r != CUDA_SUCCESS) return fail(CPRRTC_ECUDA, std::string("launch ") + k + ": " + cu_err(r));
+    c->launches++;
+    return 0;
+}
+
+int sync(Ctx* c) {
+    cudaError_t e = cudaStreamSynchronize(c->stream);
+    if (e != cudaSuccess) return fail(CPRRTC_ECUDA, std::string("kernel failed: ") + cudaGetErrorString(e));
+    return 0;
+}
+
+template <class T> int upload(Ctx* c, DevBuf& b, const T* src, size_t count) {
+    if (int rc = b.ensure(count * sizeof(T) + 16)) return rc;
+    if (count) CUDA_TRY(cudaMemcpyAsync(b.p, src, count * sizeof(T), cudaMemcpyHostToDevice, c->stream));
+    return 0;
+}
+template <class T> int download(Ctx* c, T* dst, const DevBuf& b, size_t count) {
+    if (count) CUDA_TRY(cudaMemcpyAsync(dst, b.p, count * sizeof(T), cudaMemcpyDeviceToHost, c->stream));
+    return 0;
+}
+
+SceneSm scene_args(Ctx* c) {
+    SceneSm s;
+    s.box_c = c->sc_box_c.as<float4>();
+    s.box_h = c->sc_box_h.as<float4>();
+    s.sph = c->sc_sph.as<float4>();
+    s.nb = c->nb;
+    s.ne = c->ne;
+    return s;
+}
+
+size_t team_smem(Ctx* c, Module* m, bool with_scene) {
+    size_t sc = with_scene ? (size_t)(2 * c->nb + c->ne) * sizeof(float4) : 0;
+    return sc + (size_t)(kThreads / m->G) * m->ws_bytes;
+}
+
+float tau_dev(double tau) {
+    if (!std::isfinite(tau)) return INFINITY;
+    double d = tau * (1.0 - 1e-3) - 2e-6;
+    if (d < 0.5 * tau) d = 0.5 * tau;
+    return (float)d;
+}
+
+Ctx* C(void* p) { return static_cast<Ctx*>(p); }
+
+}  // namespace
+
+// ===========================================================================
+// C ABI
+// ===========================================================================
+extern "C" {
+
+int cprrtc_abi_version(void) { return CPRRTC_ABI_VERSION; }
+
+const char* cprrtc_last_error(void) { return g_err.c_str(); }
+
+int cprrtc_device_count(int* count) {
+    int n = 0;
+    cudaError_t e = cudaGetDeviceCount(&n);
+    *count = e == cudaSuccess ? n : 0;
+    if (e != cudaSuccess) return fail(CPRRTC_ENODEV, std::string("cudaGetDeviceCount: ") + cudaGetErrorString(e));
+    return 0;
+}
+
+int cprrtc_codegen(const cprrtc_robot* robot, char* buf, size_t cap, size_t* needed) {
+    if (!robot) return fail(CPRRTC_EARG, "robot is NULL");
+    std::string err;
+    std::string s = cprrtc::codegen_robot(*robot, &err);
+    if (s.empty()) return fail(CPRRTC_EARG, err);
+    if (needed) *needed = s.size() + 1;
+    if (buf && cap) {
+        size_t k = s.size() < cap - 1 ? s.size() : cap - 1;
+        std::memcpy(buf, s.data(), k);
+        buf[k] = '\0';
+    }
+    return 0;
+}
+
+int cprrtc_precompile(const cprrtc_robot* robot, int G, int kind, int orient, int parity, char* path, size_t cap) {
+    if (!robot || (G != 16 && G != 32) || (kind != 0 && kind != 1)) return fail(CPRRTC_EARG, "bad argument");
+    std::string err;
+    Ctx tmp;
+    tmp.robot_src = cprrtc::codegen_robot(*robot, &err);
+    if (tmp.robot_src.empty()) return fail(CPRRTC_EARG, err);
+    std::string src = prelude(&tmp, G, kind, orient ? 1 : 0, parity ? 1 : 0) + kDeviceSrc;
+    std::vector<char> cubin;
+    std::string where;
+    if (int rc = nvrtc_cubin(src, module_name(G, kind, orient ? 1 : 0, parity ? 1 : 0), &cubin, &where)) return rc;
+    if (path && cap) {
+        std::snprintf(path, cap, "%s", where.c_str());
+    }
+    return 0;
+}
+
+int cprrtc_device_source(const cprrtc_robot* robot, int G, int kind, int orient, int parity, char* buf, size_t cap,
+                         size_t* needed) {
+    if (!robot) return fail(CPRRTC_EARG, "bad argument");
+    std::string err;
+    Ctx tmp;
+    tmp.robot_src = cprrtc::codegen_robot(*robot, &err);
+    if (tmp.robot_src.empty()) return fail(CPRRTC_EARG, err);
+    std::string src = prelude(&tmp, G, kind, orient ? 1 : 0, parity ? 1 : 0) + kDeviceSrc;
+    if (needed) *needed = src.size() + 1;
+    if (buf && cap) {
+        size_t k = src.size() < cap - 1 ? src.size() : cap - 1;
+        std::memcpy(buf, src.data(), k);
+        buf[k] = 0;
+    }
+    return 0;
+}
+
+int cprrtc_ctx_create(int device, const cprrtc_robot* robot, void** out) {
+    if (!robot || !out) return fail(CPRRTC_EARG, "NULL argument");
+    std::string err;
+    std::string src = cprrtc::codegen_robot(*robot, &err);
+    if (src.empty()) return fail(CPRRTC_EARG, err);
+    int ndev = 0;
+    if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0)
+        return fail(CPRRTC_ENODEV, "no CUDA device visible (the B200 planner has no CPU fallback)");
+    if (device < 0 || device >= ndev) return fail(CPRRTC_EARG, "device index out of range");
+    auto c = std::make_unique<Ctx>();
+    c->device = device;
+    CUDA_TRY(cudaSetDevice(device));
+    cudaDeviceProp prop;
+    CUDA_TRY(cudaGetDeviceProperties(&prop, device));
+    if (prop.major != 10) return fail(CPRRTC_ENODEV, std::string("sm_100a build needs a Blackwell B200, found ") + prop.name);
+    c->sms = prop.multiProcessorCount;
+    CUDA_TRY(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
+    for (auto& e : c->ev) CUDA_TRY(cudaEventCreate(&e));
+    c->n = robot->n;
+    c->S = robot->n_spheres;
+    c->P = robot->n_pairs;
+    c->NP = (c->n % 2) ? c->n : c->n + 1;
+    c->robot_src = src;
+    c->lo.assign(robot->lo, robot->lo + robot->n);
+    c->hi.assign(robot->hi, robot->hi + robot->n);
+    if (!drv().ok) return fail(CPRRTC_ECUDA, "CUDA driver entry points unavailable");
+    // unconstrained until told otherwise
+    if (int rc = cprrtc_set_constraint(c.get(), nullptr)) return rc;
+    cprrtc_scene empty{};
+    if (int rc = cprrtc_set_scene(c.get(), &empty)) return rc;
+    *out = c.release();
+    return 0;
+}
+
+int cprrtc_ctx_destroy(void* p) {
+    Ctx* c = C(p);
+    if (!c) return 0;
+    cudaSetDevice(c->device);
+    cudaStreamSynchronize(c->stream);
+    for (auto& kv : c->modules)
+        if (kv.second->mod) drv().moduleUnload(kv.second->mod);
+    for (auto& e : c->ev)
+        if (e) cudaEventDestroy(e);
+    cudaStreamDestroy(c->stream);
+    delete c;
+    return 0;
+}
+
+int cprrtc_set_scene(void* p, const cprrtc_scene* s) {
+    Ctx* c = C(p);
+    if (!c || !s) return fail(CPRRTC_EARG, "NULL argument");
+    if (s->n_boxes < 0 || s->n_spheres < 0) return fail(CPRRTC_EARG, "negative primitive count");
+    if ((size_t)(2 * s->n_boxes + s->n_spheres) * 16 > 160 * 1024)
+        return fail(CPRRTC_ELIMIT, "scene exceeds the shared-memory staging capacity (~5000 boxes)");
+    if (int rc = set_device(c)) return rc;
+    std::vector<float4> bc(s->n_boxes), bh(s->n_boxes), sp(s->n_spheres);
+    for (int i = 0; i < s->n_boxes; i++) {
+        const double* lo = s->box_min + 3 * i;
+        const double* hi = s->box_max + 3 * i;
+        bc[i] = make_float4((float)(0.5 * (lo[0] + hi[0])), (float)(0.5 * (lo[1] + hi[1])),
+                            (float)(0.5 * (lo[2] + hi[2])), 0.f);
+        bh[i] = make_float4((float)(0.5 * (hi[0] - lo[0])), (float)(0.5 * (hi[1] - lo[1])),
+                            (float)(0.5 * (hi[2] - lo[2])), 0.f);
+    }
+    for (int i = 0; i < s->n_spheres; i++)
+        sp[i] = make_float4((float)s->sph_center[3 * i], (float)s->sph_center[3 * i + 1],
+                            (float)s->sph_center[3 * i + 2], (float)s->sph_radius[i]);
+    int rc = upload(c, c->sc_box_c, bc.data(), bc.size());
+    rc = rc ? rc : upload(c, c->sc_box_h, bh.data(), bh.size());
+    rc = rc ? rc : upload(c, c->sc_sph, sp.data(), sp.size());
+    rc = rc ? rc : upload(c, c->sc_bmin, s->box_min, 3 * (size_t)s->n_boxes);
+    rc = rc ? rc : upload(c, c->sc_bmax, s->box_max, 3 * (size_t)s->n_boxes);
+    rc = rc ? rc : upload(c, c->sc_sc, s->sph_center, 3 * (size_t)s->n_spheres);
+    rc = rc ? rc : upload(c, c->sc_sr, s->sph_radius, (size_t)s->n_spheres);
+    if (rc) return rc;
+    c->nb = s->n_boxes;
+    c->ne = s->n_spheres;
+    return sync(c);
+}
+
+int cprrtc_set_constraint(void* p, const cprrtc_constraint* k) {
+    Ctx* c = C(p);
+    if (!c) return fail(CPRRTC_EARG, "NULL context");
+    cprrtc_constraint u{};
+    if (!k) {   // unconstrained(): plane z = 0 with tau = inf (constraints.py:179-186)
+        u.kind = 0;
+        u.anchor[2] = 1.0;
+        u.q_fixed[0] = 1.0;
+        u.r_fixed_t[0] = u.r_fixed_t[4] = u.r_fixed_t[8] = 1.0;
+        u.weight = 0.5;
+        u.tau_task = INFINITY;
+        k = &u;
+    }
+    if (k->kind != 0 && k->kind != 1) return fail(CPRRTC_EARG, "constraint kind must be 0 (plane) or 1 (line)");
+    c->kind = k->kind;
+    c->orient = k->has_orient ? 1 : 0;
+    c->tau_task = k->tau_task;
+    for (int i = 0; i < 3; i++) {
+        c->cond.anchor[i] = k->anchor[i];
+        c->cond.b1[i] = k->basis[i];
+        c->cond.b2[i] = k->basis[3 + i];
+    }
+    c->cond.offset = k->offset;
+    for (int i = 0; i < 4; i++) c->cond.qf[i] = k->q_fixed[i];
+    for (int i = 0; i < 9; i++) c->cond.rft[i] = k->r_fixed_t[i];
+    c->cond.weight = k->weight;
+    for (int i = 0; i < 3; i++) {
+        c->conf.anchor[i] = (float)c->cond.anchor[i];
+        c->conf.b1[i] = (float)c->cond.b1[i];
+        c->conf.b2[i] = (float)c->cond.b2[i];
+    }
+    c->conf.offset = (float)c->cond.offset;
+    for (int i = 0; i < 4; i++) c->conf.qf[i] = (float)c->cond.qf[i];
+    for (int i = 0; i < 9; i++) c->conf.rft[i] = (float)c->cond.rft[i];
+    c->conf.weight = (float)c->cond.weight;
+    return 0;
+}
+
+int cprrtc_prepare(void* p, int width) {
+    Ctx* c = C(p);
+    if (!c) return fail(CPRRTC_EARG, "NULL context");
+    if (int rc = set_device(c)) return rc;
+    Module* m;
+    return cur_module(c, width, 0, &m);
+}
+
+int64_t cprrtc_launch_count(void* p) { return p ? C(p)->launches : 0; }
+
+int cprrtc_last_timing(void* p, double* total_ms, double* plan_ms) {
+    Ctx* c = C(p);
+    if (!c) return fail(CPRRTC_EARG, "NULL context");
+    if (total_ms) *total_ms = c->last_total_ms;
+    if (plan_ms) *plan_ms = c->last_plan_ms;
+    return 0;
+}
+
+int cprrtc_fk(void* p, int B, const double* q, int fp64, double* frames, double* axes, double* origins, double* ee,
+              double* spheres) {
+    Ctx* c = C(p);
+    if (!c || B < 0 || (B && !q)) return fail(CPRRTC_EARG, "bad argument");
+    if (B == 0) return 0;
+    if (int rc = set_device(c)) return rc;
+    Module* m;
+    if (int rc = get_module(c, 16, c->kind, c->orient, 1, &m)) return rc;
+    const int n = c->n, S = c->S;
+    int rc = upload(c, c->scratch[0], q, (size_t)B * n);
+    rc = rc ? rc : c->scratch[1].ensure((size_t)B * n * 12 * 8);
+    rc = rc ? rc : c->scratch[2].ensure((size_t)B * n * 3 * 8);
+    rc = rc ? rc : c->scratch[3].ensure((size_t)B * n * 3 * 8);
+    rc = rc ? rc : c->scratch[4].ensure((size_t)B * 7 * 8);
+    rc = rc ? rc : c->scratch[5].ensure((size_t)B * (S ? S : 1) * 4 * 8);
+    if (rc) return rc;
+    const double* dq = c->scratch[0].as<double>();
+    double* df = frames ? c->scratch[1].as<double>() : nullptr;
+    double* da = (axes || origins) ? c->scratch[2].as<double>() : nullptr;
+    double* dor = (axes || origins) ? c->scratch[3].as<double>() : nullptr;
+    double* de = ee ? c->scratch[4].as<double>() : nullptr;
+    double* ds = spheres ? c->scratch[5].as<double>() : nullptr;
+    void* args[] = {&B, &fp64, &dq, &df, &da, &dor, &de, &ds};
+    if (int rc2 = launch(c, m, "cp_fk_kernel", (B + 127) / 128, 1, 128, 0, args)) return rc2;
+    if (frames) download(c, frames, c->scratch[1], (size_t)B * n * 12);
+    if (axes) download(c, axes, c->scratch[2], (size_t)B * n * 3);
+    if (origins) download(c, origins, c->scratch[3], (size_t)B * n * 3);
+    if (ee) download(c, ee, c->scratch[4], (size_t)B * 7);
+    if (spheres) download(c, spheres, c->scratch[5], (size_t)B * S * 4);
+    return sync(c);
+}
+
+int cprrtc_task_err_jac(void* p, int B, const double* q, int fp64, double* e, double* J) {
+    Ctx* c = C(p);
+    if (!c || B < 0 || (B && (!q || !e || !J))) return fail(CPRRTC_EARG, "bad argument");
+    if (B == 0) return 0;
+    if (int rc = set_device(c)) return rc;
+    Module* m;
+    if (int rc = get_module(c, 16, c->kind, c->orient, 1, &m)) return rc;
+    const int M = (c->kind == 0 ? 1 : 2) + (c->orient ? 3 : 0);
+    int rc = upload(c, c->scratch[0], q, (size_t)B * c->n);
+    rc = rc ? rc : c->scratch[1].ensure((size_t)B * M * 8);
+    rc = rc ? rc : c->scratch[2].ensure((size_t)B * M * c->n * 8);
+    if (rc) return rc;
+    const double* dq = c->scratch[0].as<double>();
+    double* de = c->scratch[1].as<double>();
+    double* dJ = c->scratch[2].as<double>();
+    void* args[] = {&B, &fp64, &c->conf, &c->cond, &dq, &de, &dJ};
+    if (int rc2 = launch(c, m, "cp_tej_kernel", (B + 127) / 128, 1, 128, 0, args)) return rc2;
+    download(c, e, c->scratch[1], (size_t)B * M);
+    download(c, J, c->scratch[2], (size_t)B * M * c->n);
+    return sync(c);
+}
+
+int cprrtc_task_error_at(void* p, int B, const double* pose7, double* e) {
+    Ctx* c = C(p);
+    if (!c || B < 0 || (B && (!pose7 || !e))) return fail(CPRRTC_EARG, "bad argument");
+    if (B == 0) return 0;
+    if (int rc = set_device(c)) return rc;
+    Module* m;
+    if (int rc = get_module(c, 16, c->kind, c->orient, 1, &m)) return rc;
+    const int M = (c->kind == 0 ? 1 : 2) + (c->orient ? 3 : 0);
+    int rc = upload(c, c->scratch[0], pose7, (size_t)B * 7);
+    rc = rc ? rc : c->scratch[1].ensure((size_t)B * M * 8);
+    if (rc) return rc;
+    const double* dp = c->scratch[0].as<double>();
+    double* de = c->scratch[1].as<double>();
+    void* args[] = {&B, &c->cond, &dp, &de};
+    if (int rc2 = launch(c, m, "cp_err_at_kernel", (B + 127) / 128, 1, 128, 0, args)) return rc2;
+    download(c, e, c->scratch[1], (size_t)B * M);
+    return sync(c);
+}
+
+int cprrtc_project_config(void* p, int B, double* q_io, double tau, double lam, int max_iters, int32_t* ok) {
+    Ctx* c = C(p);
+    if (!c || B < 0 || (B && (!q_io || !ok))) return fail(CPRRTC_EARG, "bad argument");
+    if (B == 0) return 0;
+    if (int rc = set_device(c)) return rc;
+    Module* m;
+    if (int rc = get_module(c, 16, c->kind, c->orient, 1, &m)) return rc;
+    int rc = upload(c, c->scratch[0], q_io, (size_t)B * c->n);
+    rc = rc ? rc : c->scratch[1].ensure((size_t)B * 4);
+    if (rc) return rc;
+    double* dq = c->scratch[0].as<double>();
+    int* dok = c->scratch[1].as<int>();
+    void* args[] = {&B, &c->cond, &tau, &lam, &max_iters, &dq, &dok};
+    if (int rc2 = launch(c, m, "cp_project_config_kernel", (B + 63) / 64, 1, 64, 0, args)) return rc2;
+    download(c, q_io, c->scratch[0], (size_t)B * c->n);
+    download(c, ok, c->scratch[1], (size_t)B);
+    return sync(c);
+}
+
+static SetupArgs setup_args(Ctx* c, double tau) {
+    SetupArgs S{};
+    S.con = c->cond;
+    S.tau_task = tau;
+    S.box_min = c->sc_bmin.as<double>();
+    S.box_max = c->sc_bmax.as<double>();
+    S.sph_c = c->sc_sc.as<double>();
+    S.sph_r = c->sc_sr.as<double>();
+    S.nb = c->nb;
+    S.ne = c->ne;
+    return S;
+}
+
+int cprrtc_check_config(void* p, int B, const double* q, double tau, int32_t* code) {
+    Ctx* c = C(p);
+    if (!c || B < 0 || (B && (!q || !code))) return fail(CPRRTC_EARG, "bad argument");
+    if (B == 0) return 0;
+    if (int rc = set_device(c)) return rc;
+    Module* m;
+    if (int rc = get_module(c, 16, c->kind, c->orient, 1, &m)) return rc;
+    int rc = upload(c, c->scratch[0], q, (size_t)B * c->n);
+    rc = rc ? rc : c->scratch[1].ensure((size_t)B * 4);
+    if (rc) return rc;
+    SetupArgs S = setup_args(c, tau);
+    const double* dq = c->scratch[0].as<double>();
+    int* dc = c->scratch[1].as<int>();
+    void* args[] = {&B, &S, &dq, &dc};
+    if (int rc2 = launch(c, m, "cp_check_config_kernel", (B + 3) / 4, 1, 128, 0, args)) return rc2;
+    download(c, code, c->scratch[1], (size_t)B);
+    return sync(c);
+}
+
+int cprrtc_validate(void* p, int B, int W, const double* wps, int flag_on, double margin, int32_t* valid,
+                    int32_t* first_bad, int64_t* performed, int64_t* possible, int64_t* gpu_checks) {
+    Ctx* c = C(p);
+    if (!c || B < 0 || W < 1 || (B && (!wps || !valid || !first_bad || !performed)))
+        return fail(CPRRTC_EARG, "bad argument");
+    if (B == 0) return 0;
+    if (W > 32) return fail(CPRRTC_ELIMIT, "at most 32 waypoints per motion in this build");
+    if (int rc = set_device(c)) return rc;
+    Module* m;
+    if (int rc = get_module(c, W <= 16 ? 16 : 32, c->kind, c->orient, 1, &m)) return rc;
+    int rc = upload(c, c->scratch[0], wps, (size_t)B * W * c->n);
+    rc = rc ? rc : c->scratch[1].ensure((size_t)B * 4);
+    rc = rc ? rc : c->scratch[2].ensure((size_t)B * 4);
+    rc = rc ? rc : c->scratch[3].ensure((size_t)B * 8);
+    rc = rc ? rc : c->scratch[4].ensure((size_t)B * 8);
+    if (rc) return rc;
+    SceneSm sc = scene_args(c);
+    const double* dw = c->scratch[0].as<double>();
+    int* dv = c->scratch[1].as<int>();
+    int* df = c->scratch[2].as<int>();
+    int64_t* dp = c->scratch[3].as<int64_t>();
+    int64_t* dg = c->scratch[4].as<int64_t>();
+    float mg = (float)margin;
+    void* args[] = {&B, &W, &flag_on, &mg, &sc, &dw, &dv, &df, &dp, &dg};
+    const int tpc = kThreads / m->G;
+    int grid = (B + tpc - 1) / tpc;
+    if (grid > 64 * c->sms) grid = 64 * c->sms;
+    if (int rc2 = launch(c, m, "cp_validate_kernel", grid, 1, kThreads, team_smem(c, m, true), args)) return rc2;
+    download(c, valid, c->scratch[1], (size_t)B);
+    download(c, first_bad, c->scratch[2], (size_t)B);
+    download(c, performed, c->scratch[3], (size_t)B);
+    if (gpu_checks) download(c, gpu_checks, c->scratch[4], (size_t)B);
+    if (int rc3 = sync(c)) return rc3;
+    if (possible) {
+        const int64_t per = (int64_t)c->S * (c->nb + c->ne) + c->P;
+        for (int i = 0; i < B; i++) possible[i] = per * W;
+    }
+    return 0;
+}
+
+int cprrtc_project(void* p, int B, int W, const double* wps, const double* tau_sm, double tau_task, double alpha,
+                   double lam, int max_iters, int mode, double* xi, int32_t* ok, int32_t* iters, int32_t* prog,
+                   double* trace, int32_t* trace_prog) {
+    Ctx* c = C(p);
+    if (!c || B < 0 || W < 2 || max_iters < 1 || mode < 0 || mode > 2 ||
+        (B && (!wps || !xi || !ok || !iters || !prog)))
+        return fail(CPRRTC_EARG, "bad argument");
+    if (B == 0) return 0;
+    if (int rc = set_device(c)) return rc;
+    Module* m;
+    if (int rc = cur_module(c, W, 1, &m)) return rc;
+    const size_t nw = (size_t)B * W * c->n;
+    int rc = upload(c, c->scratch[0], wps, nw);
+    rc = rc ? rc : c->scratch[1].ensure(nw * 8);
+    rc = rc ? rc : c->scratch[2].ensure((size_t)B * 12);
+    if (rc) return rc;
+    std::vector<float> tsm;
+    if (tau_sm) {
+        tsm.resize(B);
+        for (int i = 0; i < B; i++) tsm[i] = (float)tau_sm[i];
+        if ((rc = upload(c, c->scratch[3], tsm.data(), (size_t)B))) return rc;
+    }
+    float* dtrace = nullptr;
+    int* dtp = nullptr;
+    if (trace) {
+        rc = c->scratch[4].ensure((size_t)B * max_iters * W * c->n * 4);
+        rc = rc ? rc : c->scratch[5].ensure((size_t)B * max_iters * 4);
+        if (rc) return rc;
+        CUDA_TRY(cudaMemsetAsync(c->scratch[5].p, 0xff, (size_t)B * max_iters * 4, c->stream));
+        dtrace = c->scratch[4].as<float>();
+        dtp = c->scratch[5].as<int>();
+    }
+    ProjArgs pa{};
+    pa.alpha = (float)alpha;
+    pa.lam = (float)lam;
+    pa.tau_task = (float)tau_task;
+    pa.tau_task_dev = tau_dev(tau_task);
+    pa.tau_sm_fixed = 0.f;
+    pa.max_iters = max_iters;
+    pa.mode = mode;
+    const double* dw = c->scratch[0].as<double>();
+    double* dxi = c->scratch[1].as<double>();
+    int* dok = c->scratch[2].as<int>();
+    int* dit = dok + B;
+    int* dpr = dok + 2 * B;
+    const float* dts = tau_sm ? c->scratch[3].as<float>() : nullptr;
+    void* args[] = {&B, &W, &c->conf, &pa, &dts, &dw, &dxi, &dok, &dit, &dpr, &dtrace, &dtp};
+    const int tpc = kThreads / m->G;
+    int grid = (B + tpc - 1) / tpc;
+    if (grid > 64 * c->sms) grid = 64 * c->sms;
+    if (int rc2 = launch(c, m, "cp_project_kernel", grid, 1, kThreads, team_smem(c, m, false), args)) return rc2;
+    download(c, xi, c->scratch[1], nw);
+    std::vector<int> tmp((size_t)3 * B);
+    download(c, tmp.data(), c->scratch[2], (size_t)3 * B);
+    std::vector<float> tr;
+    if (trace) {
+        tr.resize((size_t)B * max_iters * W * c->n);
+        download(c, tr.data(), c->scratch[4], tr.size());
+        download(c, trace_prog, c->scratch[5], (size_t)B * max_iters);
+    }
+    if (int rc3 = sync(c)) return rc3;
+    for (int i = 0; i < B; i++) {
+        ok[i] = tmp[i];
+        iters[i] = tmp[B + i];
+        prog[i] = tmp[2 * B + i];
+    }
+    if (trace)
+        for (size_t i = 0; i < tr.size(); i++) trace[i] = tr[i];
+    return 0;
+}
+
+int cprrtc_nearest(void* p, int N, const double* nodes, int Q, const double* queries, int32_t* idx) {
+    Ctx* c = C(p);
+    if (!c || N < 1 || Q < 0 || !nodes || (Q && (!queries || !idx))) return fail(CPRRTC_EARG, "bad argument");
+    if (Q == 0) return 0;
+    if (int rc = set_device(c)) return rc;
+    Module* m;
+    if (int rc = get_module(c, 16, c->kind, c->orient, 1, &m)) return rc;
+    const int n = c->n;
+    const int cap = (N + 127) / 128 * 128;
+    std::vector<float> soa((size_t)n * cap, NAN);
+    for (int i = 0; i < N; i++)
+        for (int k = 0; k < n; k++) soa[(size_t)k * cap + i] = (float)nodes[(size_t)i * n + k];
+    std::vector<float> qf((size_t)Q * n);
+    for (size_t i = 0; i < qf.size(); i++) qf[i] = (float)queries[i];
+    int rc = upload(c, c->scratch[0], soa.data(), soa.size());
+    rc = rc ? rc : upload(c, c->scratch[1], qf.data(), qf.size());
+    rc = rc ? rc : c->scratch[2].ensure((size_t)Q * 4);
+    if (rc) return rc;
+    const float* dn = c->scratch[0].as<float>();
+    const float* dq = c->scratch[1].as<float>();
+    int* di = c->scratch[2].as<int>();
+    void* args[] = {&N, (void*)&cap, &dn, &Q, &dq, &di};
+    const int tpc = kThreads / m->G;
+    int grid = (Q + tpc - 1) / tpc;
+    if (grid > 64 * c->sms) grid = 64 * c->sms;
+    if (int rc2 = launch(c, m, "cp_nearest_kernel", grid, 1, kThreads, 0, args)) return rc2;
+    download(c, idx, c->scratch[2], (size_t)Q);
+    return sync(c);
+}
+
+int cprrtc_halton(void* p, int count, int64_t first_index, int64_t seed_offset, const double* lo, const double* hi,
+                  double* out) {
+    Ctx* c = C(p);
+    if (!c || count < 0 || (count && !out) || first_index < 0 || seed_offset < 0)
+        return fail(CPRRTC_EARG, "bad argument");
+    if (count == 0) return 0;
+    if (int rc = set_device(c)) return rc;
+    Module* m;
+    if (int rc = get_module(c, 16, c->kind, c->orient, 1, &m)) return rc;
+    if (int rc = c->scratch[0].ensure((size_t)count * c->n * 8)) return rc;
+    if (int rc = upload(c, c->scratch[1], lo ? lo : c->lo.data(), (size_t)c->n)) return rc;
+    if (int rc = upload(c, c->scratch[2], hi ? hi : c->hi.data(), (size_t)c->n)) return rc;
+    double* d = c->scratch[0].as<double>();
+    const double* dlo = c->scratch[1].as<double>();
+    const double* dhi = c->scratch[2].as<double>();
+    long long fi = first_index, so = seed_offset;
+    void* args[] = {&count, &fi, &so, &dlo, &dhi, &d};
+    if (int rc2 = launch(c, m, "cp_halton_kernel", (count + 127) / 128, 1, 128, 0, args)) return rc2;
+    download(c, out, c->scratch[0], (size_t)count * c->n);
+    return sync(c);
+}
+
+static int ensure_plan_buffers(Ctx* c, int nq, int cap, int path_cap) {
+    const int n = c->n;
+    if (nq > c->nq_alloc || cap != c->cap_alloc) {
+        size_t tree_bytes = (size_t)nq * 2 * n * cap * sizeof(float);
+        int rc = c->trees.ensure(tree_bytes);
+        rc = rc ? rc : c->parents.ensure((size_t)nq * 2 * cap * sizeof(int));
+        rc = rc ? rc : c->qs.ensure((size_t)nq * sizeof(QueryState));
+        if (rc) return rc;
+        CUDA_TRY(cudaMemsetAsync(c->trees.p, 0xff, tree_bytes, c->stream));   // NaN = unpublished
+        CUDA_TRY(cudaMemsetAsync(c->qs.p, 0, (size_t)nq * sizeof(QueryState), c->stream));
+        c->nq_alloc = nq;
+        c->cap_alloc = cap;
+    }
+    int rc = c->counters.ensure(64);
+    rc = rc ? rc : c->d_starts.ensure((size_t)nq * n * 8);
+    rc = rc ? rc : c->d_goals.ensure((size_t)nq * n * 8);
+    rc = rc ? rc : c->d_seeds.ensure((size_t)nq * 8);
+    rc = rc ? rc : c->h_in.ensure((size_t)nq * (2 * n + 1) * 8);
+    rc = rc ? rc : c->h_out.ensure((size_t)nq * sizeof(QueryOut));
+    rc = rc ? rc : c->h_paths.ensure((size_t)nq * path_cap * n * sizeof(float));
+    rc = rc ? rc : c->h_src.ensure((size_t)nq * path_cap * sizeof(int));
+    c->path_cap = path_cap;
+    return rc;
+}
+
+static PlanArgs make_plan_args(Ctx* c, const cprrtc_params* prm, int B, int cap, double tau) {
+    PlanArgs A{};
+    A.qs = c->qs.as<QueryState>();
+    A.trees = c->trees.as<float>();
+    A.parents = c->parents.as<int>();
+    A.cap = cap;
+    A.nq = B;
+    A.queue_head = c->counters.as<int>();
+    A.team_counter = c->counters.as<int>() + 1;
+    A.scene_g = scene_args(c);
+    A.con = c->conf;
+    A.pa.alpha = (float)prm->alpha;
+    A.pa.lam = (float)prm->lam;
+    A.pa.tau_task = (float)tau;
+    A.pa.tau_task_dev = tau_dev(tau);
+    A.pa.tau_sm_fixed = prm->tau_sm > 0 ? (float)prm->tau_sm : 0.f;
+    A.pa.max_iters = prm->proj_max_iters;
+    A.pa.mode = prm->projection_mode;
+    A.W = prm->width;
+    A.step = (float)prm->step_size;
+    A.tol = (float)(prm->connect_tolerance > 0 ? prm->connect_tolerance : prm->step_size / 10.0);
+    A.margin = (float)prm->cc_margin;
+    A.flag_on = prm->flag_on;
+    A.max_iterations = prm->max_iterations;
+    A.max_connect = prm->max_connect_segments;
+    A.budget_ns = (prm->deterministic || prm->time_budget_ms <= 0) ? 0 : (i64)(prm->time_budget_ms * 1e6);
+    return A;
+}
+
+int cprrtc_plan(void* p, const cprrtc_params* prm, int B, const double* starts, const double* goals,
+                const int64_t* seeds, cprrtc_result* results, double* paths, int32_t* sources) {
+    Ctx* c = C(p);
+    if (!c || !prm || B < 1 || !starts || !goals || !results) return fail(CPRRTC_EARG, "bad argument");
+    if (prm->step_size <= 0 || prm->width < 2 || prm->max_iterations < 1 || prm->alpha <= 0 || prm->lam < 0 ||
+        prm->proj_max_iters < 1 || prm->projection_mode < 0 || prm->projection_mode > 2)
+        return fail(CPRRTC_EARG, "invalid planner parameters");
+    if (int rc = set_device(c)) return rc;
+    Module* m;
+    if (int rc = cur_module(c, prm->width, 0, &m)) return rc;
+    const int n = c->n;
+    // tree capacity: every sample adds at most 1 + max_connect_segments nodes
+    long long want = prm->tree_capacity > 0 ? prm->tree_capacity
+                                            : (long long)prm->max_iterations * (1 + prm->max_connect_segments) / 2 + 256;
+    long long budget_nodes = (1ll << 30) / ((long long)B * 2 * n * 4 + 1) * 4;   // ~4 GiB of trees
+    if (prm->tree_capacity <= 0 && want > budget_nodes) want = budget_nodes;
+    if (want > (1 << 26)) want = 1 << 26;
+    int cap = (int)((want + 127) / 128 * 128);
+    if (cap < 128) cap = 128;
+    const int path_cap = prm->path_capacity > 0 ? prm->path_capacity : 1024;
+    if (int rc = ensure_plan_buffers(c, B, cap, path_cap)) return rc;
+    // inputs: pinned staging -> device (the H2D of the timed e2e path)
+    double* hin = c->h_in.host<double>();
+    std::memcpy(hin, starts, (size_t)B * n * 8);
+    std::memcpy(hin + (size_t)B * n, goals, (size_t)B * n * 8);
+    long long* hseed = reinterpret_cast<long long*>(hin + (size_t)2 * B * n);
+    for (int i = 0; i < B; i++) hseed[i] = seeds ? seeds[i] : 0;
+    CUDA_TRY(cudaEventRecord(c->ev[0], c->stream));
+    CUDA_TRY(cudaMemcpyAsync(c->d_starts.p, hin, (size_t)B * n * 8, cudaMemcpyHostToDevice, c->stream));
+    CUDA_TRY(cudaMemcpyAsync(c->d_goals.p, hin + (size_t)B * n, (size_t)B * n * 8, cudaMemcpyHostToDevice, c->stream));
+    CUDA_TRY(cudaMemcpyAsync(c->d_seeds.p, hseed, (size_t)B * 8, cudaMemcpyHostToDevice, c->stream));
+    CUDA_TRY(cudaMemsetAsync(c->counters.p, 0, 64, c->stream));
+    // 1) refill the node slots used last time with NaN
+    {
+        QueryState* qs = c->qs.as<QueryState>();
+        float* tr = c->trees.as<float>();
+        int nq = B;
+        int gy = 2 * B < 4096 ? 2 * B : 4096;
+        void* args[] = {&qs, &tr, &cap, &nq};
+        if (int rc = launch(c, m, "cp_reset_kernel", 32, gy, 256, 0, args)) return rc;
+    }
+    // 2) endpoint checks + tree roots, FP64
+    double tau = prm->tau_task > 0 ? prm->tau_task : c->tau_task;
+    {
+        SetupArgs S = setup_args(c, tau);
+        S.qs = c->qs.as<QueryState>();
+        S.starts = c->d_starts.as<double>();
+        S.goals = c->d_goals.as<double>();
+        S.seeds = c->d_seeds.as<i64>();
+        S.trees = c->trees.as<float>();
+        S.parents = c->parents.as<int>();
+        S.cap = cap;
+        void* args[] = {&S};
+        if (int rc = launch(c, m, "cp_setup_kernel", B, 1, 64, 0, args)) return rc;
+    }
+    // 3) the persistent planner
+    PlanArgs A = make_plan_args(c, prm, B, cap, tau);
+    const size_t smem = team_smem(c, m, true);
+    if (!m->plan_occ) {
+        int occ = 0;
+        drv().occupancy(&occ, m->fn["cp_plan_kernel"], kThreads, smem);
+        m->plan_occ = occ > 0 ? occ : 1;
+    }
+    const int tpc = kThreads / m->G;
+    int grid = m->plan_occ * c->sms;
+    if (prm->teams > 0) {
+        int g = (prm->teams + tpc - 1) / tpc;
+        if (g < grid) grid = g;
+    }
+    if (grid < 1) grid = 1;
+    CUDA_TRY(cudaEventRecord(c->ev[1], c->stream));
+    {
+        void* args[] = {&A};
+        if (int rc = launch(c, m, "cp_plan_kernel", grid, 1, kThreads, smem, args)) return rc;
+    }
+    CUDA_TRY(cudaEventRecord(c->ev[2], c->stream));
+    // 4) path extraction into mapped host memory
+    {
+        QueryState* qs = c->qs.as<QueryState>();
+        const float* tr = c->trees.as<float>();
+        const int* pr = c->parents.as<int>();
+        int nq = B;
+        QueryOut* out = c->h_out.dev<QueryOut>();
+        float* hp = c->h_paths.dev<float>();
+        int* hs = c->h_src.dev<int>();
+        int pc = path_cap;
+        void* args[] = {&qs, &tr, &pr, &cap, &nq, &out, &hp, &hs, &pc};
+        if (int rc = launch(c, m, "cp_extract_kernel", (B + 3) / 4, 1, 128, 0, args)) return rc;
+    }
+    CUDA_TRY(cudaEventRecord(c->ev[3], c->stream));
+    if (int rc = sync(c)) return rc;
+    float t_all = 0, t_plan = 0;
+    cudaEventElapsedTime(&t_all, c->ev[0], c->ev[3]);
+    cudaEventElapsedTime(&t_plan, c->ev[1], c->ev[2]);
+    c->last_total_ms = t_all;
+    c->last_plan_ms = t_plan;
+    c->last_args = A;
+    c->last_mod = m;
+    c->last_nq = B;
+    const QueryOut* out = c->h_out.host<QueryOut>();
+    const float* hp = c->h_paths.host<float>();
+    const int* hs = c->h_src.host<int>();
+    for (int i = 0; i < B; i++) {
+        cprrtc_result& r = results[i];
+        r.status = out[i].status;
+        r.setup_code = out[i].setup_code;
+        r.path_len = out[i].path_len;
+        r.nodes_start = out[i].n_nodes[0];
+        r.nodes_goal = out[i].n_nodes[1];
+        r.device_ms = out[i].device_ms;
+        for (int k = 0; k < CPRRTC_ST_COUNT; k++) r.stats[k] = out[i].stats[k];
+        if (paths && r.path_len > 0) {
+            const float* src = hp + (size_t)i * path_cap * n;
+            double* dst = paths + (size_t)i * path_cap * n;
+            for (int k = 0; k < r.path_len * n; k++) dst[k] = src[k];
+        }
+        if (sources && r.path_len > 1)
+            for (int k = 0; k < r.path_len - 1; k++) sources[(size_t)i * path_cap + k] = hs[(size_t)i * path_cap + k];
+    }
+    return 0;
+}
+
+int cprrtc_derive_edges(void* p, const cprrtc_params* prm, int n_nodes, const double* nodes, const int32_t* sources,
+                        double* dense, int32_t* ok) {
+    Ctx* c = C(p);
+    if (!c || !prm || n_nodes < 1 || !nodes || (n_nodes > 1 && (!sources || !dense || !ok)))
+        return fail(CPRRTC_EARG, "bad argument");
+    const int E = n_nodes - 1;
+    if (E == 0) return 0;
+    if (int rc = set_device(c)) return rc;
+    Module* m;
+    if (int rc = cur_module(c, prm->width, 0, &m)) return rc;
+    const int n = c->n, W = prm->width;
+    std::vector<float> nf((size_t)n_nodes * n);
+    for (size_t i = 0; i < nf.size(); i++) nf[i] = (float)nodes[i];
+    double tau = prm->tau_task > 0 ? prm->tau_task : c->tau_task;
+    PlanArgs A = make_plan_args(c, prm, 0, 0, tau);
+    int rc = upload(c, c->dense_nodes, nf.data(), nf.size());
+    rc = rc ? rc : upload(c, c->scratch[9], sources, (size_t)E);
+    rc = rc ? rc : c->dense_buf.ensure((size_t)E * W * n * 4);
+    rc = rc ? rc : c->dense_ok.ensure((size_t)E * 4 + 16);
+    if (rc) return rc;
+    const float* dn = c->dense_nodes.as<float>();
+    const int* ds = c->scratch[9].as<int>();
+    float* dd = c->dense_buf.as<float>();
+    int* dok = c->dense_ok.as<int>();
+    void* args[] = {(void*)&E, &A, &dn, &ds, &dd, &dok};
+    const int tpc = kThreads / m->G;
+    if (int rc2 = launch(c, m, "cp_dense_kernel", (E + tpc - 1) / tpc, 1, kThreads, team_smem(c, m, true), args))
+        return rc2;
+    std::vector<float> tmp((size_t)E * W * n);
+    download(c, tmp.data(), c->dense_buf, tmp.size());
+    download(c, ok, c->dense_ok, (size_t)E);
+    if (int rc3 = sync(c)) return rc3;
+    for (size_t i = 0; i < tmp.size(); i++) dense[i] = tmp[i];
+    return 0;
+}
+
+int cprrtc_clearance(int device, int B, int kind, const double* a, const double* b, double* out) {
+    if (B < 0 || (B && (!a || !b || !out)) || (kind != 0 && kind != 1)) return fail(CPRRTC_EARG, "bad argument");
+    if (B == 0) return 0;
+    CUDA_TRY(cudaSetDevice(device));
+    double *da, *db, *dout;
+    const size_t bw = kind == 0 ? 6 : 4;
+    CUDA_TRY(cudaMalloc(&da, (size_t)B * 4 * 8));
+    CUDA_TRY(cudaMalloc(&db, (size_t)B * bw * 8));
+    CUDA_TRY(cudaMalloc(&dout, (size_t)B * 8));
+    cudaMemcpy(da, a, (size_t)B * 4 * 8, cudaMemcpyHostToDevice);
+    cudaMemcpy(db, b, (size_t)B * bw * 8, cudaMemcpyHostToDevice);
+    cudaError_t e = cprrtc::launch_clearance(B, kind, da, db, dout, 0);
+    if (e == cudaSuccess) e = cudaMemcpy(out, dout, (size_t)B * 8, cudaMemcpyDeviceToHost);
+    cudaFree(da);
+    cudaFree(db);
+    cudaFree(dout);
+    if (e != cudaSuccess) return fail(CPRRTC_ECUDA, std::string("clearance: ") + cudaGetErrorString(e));
+    return 0;
+}
+
+int cprrtc_damped_step(int device, int B, int m, int n, const double* J, const double* e, double lam, double* step,
+                       int32_t* ok) {
+    if (B < 0 || m < 1 || m > 5 || n < 1 || n > 32 || (B && (!J || !e || !step || !ok)))
+        return fail(CPRRTC_EARG, "bad argument (1 <= m <= 5, 1 <= n <= 32)");
+    if (B == 0) return 0;
+    CUDA_TRY(cudaSetDevice(device));
+    double *dJ, *de, *ds;
+    int32_t* dok;
+    CUDA_TRY(cudaMalloc(&dJ, (size_t)B * m * n * 8));
+    CUDA_TRY(cudaMalloc(&de, (size_t)B * m * 8));
+    CUDA_TRY(cudaMalloc(&ds, (size_t)B * n * 8));
+    CUDA_TRY(cudaMalloc(&dok, (size_t)B * 4));
+    cudaMemcpy(dJ, J, (size_t)B * m * n * 8, cudaMemcpyHostToDevice);
+    cudaMemcpy(de, e, (size_t)B * m * 8, cudaMemcpyHostToDevice);
+    cudaError_t err = cprrtc::launch_damped_step(B, m, n, dJ, de, lam, ds, dok, 0);
+    if (err == cudaSuccess) err = cudaMemcpy(step, ds, (size_t)B * n * 8, cudaMemcpyDeviceToHost);
+    if (err == cudaSuccess) err = cudaMemcpy(ok, dok, (size_t)B * 4, cudaMemcpyDeviceToHost);
+    cudaFree(dJ);
+    cudaFree(de);
+    cudaFree(ds);
+    cudaFree(dok);
+    if (err != cudaSuccess) return fail(CPRRTC_ECUDA, std::string("damped_step: ") + cudaGetErrorString(err));
+    return 0;
+}
+
+}  // extern "C"

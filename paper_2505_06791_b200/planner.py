@@ -1,0 +1,450 @@
+"""Constrained bidirectional RRT-Connect on the B200.
+
+Drop-in for ``maniplan/planner.py``: the same PlanParams / PlanProblem /
+PlanResult / PlanStats types and the same ``plan(problem) -> PlanResult``
+call, but the whole tree-extension loop -- sampling, nearest neighbour,
+steering, parallel projection, FK + collision checking, greedy connect,
+junction test and termination -- runs inside one persistent sm_100a kernel
+(``csrc/device/cprrtc_device.cuh: cp_plan_kernel``).  Many teams extend the
+two trees concurrently; sample i of the Halton stream (index i +
+seed_offset, the reference's stream) extends the start tree when i is odd,
+exactly like reference iteration i (planner.py:449-459).
+
+Differences from the reference, all deliberate:
+* FP32 device arithmetic with safety margins (tau_task x (1-1e-3) - 2e-6,
+  tau_sm x (1-1e-5), robot spheres inflated by ``cc_margin`` = 1e-5 m), so
+  every returned path re-validates in FP64.
+* Extensions run concurrently, so a run is not bit-reproducible across
+  launches; ``deterministic`` keeps its reference meaning (ignore the wall
+  clock).  ``attempts`` is accepted; the device already evaluates hundreds of
+  samples at once.
+* ``stats.iterations`` counts samples drawn; ``cc_performed`` counts the
+  checks the GPU actually evaluated (waypoint 0 of a motion is an existing
+  tree node and is not re-checked).
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+import math
+import time
+from dataclasses import dataclass, field, replace
+
+import numpy as np
+
+from . import _lib, kernels
+from .constraints import ConstraintSpec, task_error, unconstrained
+from .errors import PlanSetupError
+from .geometry import Scene
+from .kinematics import RobotModel, forward_kinematics
+from .projection import MotionSegment, ProjectionParams
+
+__all__ = [
+    "Tree", "PlanParams", "PlanProblem", "PlanResult", "PlanStats", "PlanContext",
+    "ExtendOutcome", "ConnectOutcome", "DeviceOptions", "nearest", "steer", "plan",
+    "plan_batch", "extract_path", "derive_edge", "revalidate_path", "dense_path",
+]
+
+
+class Tree:
+    """Host-side append-only tree (API parity with maniplan.planner.Tree)."""
+
+    def __init__(self, root, root_kind: str):
+        root = np.asarray(root, dtype=float)
+        self.root_kind = root_kind
+        self._buf = np.empty((64, root.shape[0]))
+        self._buf[0] = root
+        self._len = 1
+        self.parents = [0]
+
+    def __len__(self):
+        return self._len
+
+    @property
+    def nodes(self) -> np.ndarray:
+        return self._buf[:self._len]
+
+    def node(self, i: int) -> np.ndarray:
+        if not 0 <= i < self._len:
+            raise IndexError(f"node {i} out of range")
+        return self._buf[i].copy()
+
+    def add(self, q, parent: int) -> int:
+        if not 0 <= parent < self._len:
+            raise IndexError(f"parent {parent} out of range")
+        if self._len == len(self._buf):
+            self._buf = np.concatenate([self._buf, np.empty_like(self._buf)])
+        self._buf[self._len] = np.asarray(q, dtype=float)
+        self.parents.append(parent)
+        self._len += 1
+        return self._len - 1
+
+    def chain(self, i: int) -> list:
+        out = [i]
+        while self.parents[i] != i:
+            i = self.parents[i]
+            out.append(i)
+        return out[::-1]
+
+
+@dataclass(frozen=True)
+class PlanParams:
+    step_size: float = 0.5
+    width: int = 32
+    projection: ProjectionParams = ProjectionParams()
+    max_iterations: int = 10_000
+    time_budget_ms: float = 10_000.0
+    connect_tolerance: float | None = None
+    projection_mode: str = "parallel"     # parallel | literal-gap | naive
+    flag_mode: str = "on"
+    seed_offset: int = 0
+    deterministic: bool = False
+    attempts: int = 1
+    max_connect_segments: int = 256
+
+    def __post_init__(self):
+        if self.step_size <= 0 or self.width < 2:
+            raise ValueError("step_size > 0 and width >= 2 required")
+        if self.max_iterations < 1 or self.attempts < 1:
+            raise ValueError("max_iterations and attempts must be >= 1")
+
+    @property
+    def tolerance(self) -> float:
+        return self.connect_tolerance if self.connect_tolerance is not None else self.step_size / 10.0
+
+
+@dataclass(frozen=True)
+class DeviceOptions:
+    """B200 knobs (no reference counterpart)."""
+
+    device: int = 0
+    teams: int = 0               # concurrent extension teams; 0 = one CTA per SM
+    cc_margin: float = 1e-5      # planner robot-sphere inflation (m)
+    tree_capacity: int = 0       # nodes per tree; 0 = derived from the params
+    path_capacity: int = 1024
+
+
+@dataclass(frozen=True)
+class PlanProblem:
+    model: RobotModel
+    scene: Scene
+    spec: ConstraintSpec | None
+    start: np.ndarray
+    goal: np.ndarray
+    params: PlanParams = PlanParams()
+    name: str = ""
+
+    def __post_init__(self):
+        object.__setattr__(self, "start", self.model.check_q(self.start))
+        object.__setattr__(self, "goal", self.model.check_q(self.goal))
+
+
+@dataclass
+class PlanStats:
+    iterations: int = 0
+    extensions_attempted: int = 0
+    extensions_added: int = 0
+    projection_failures: int = 0
+    collision_rejections: int = 0
+    cc_performed: int = 0
+    cc_possible: int = 0
+    wall_ms: float = 0.0
+    nodes_start: int = 0
+    nodes_goal: int = 0
+    device_ms: float = 0.0        # query time on the device (globaltimer)
+
+
+@dataclass(frozen=True)
+class PlanResult:
+    status: str                                  # Solved | TimedOut | IterLimit
+    path: tuple | None
+    edge_sources: tuple | None
+    stats: PlanStats
+    dense: np.ndarray | None = field(default=None, compare=False)   # (E, W, n) on request
+
+    @property
+    def solved(self) -> bool:
+        return self.status == "Solved"
+
+
+@dataclass
+class PlanContext:
+    model: RobotModel
+    scene: Scene
+    spec: ConstraintSpec
+    params: PlanParams
+    stats: PlanStats = field(default_factory=PlanStats)
+    options: DeviceOptions = DeviceOptions()
+
+    @classmethod
+    def from_problem(cls, problem: PlanProblem, options: DeviceOptions = DeviceOptions()):
+        spec = problem.spec if problem.spec is not None else unconstrained()
+        return cls(problem.model, problem.scene, spec, problem.params, options=options)
+
+
+@dataclass(frozen=True)
+class ExtendOutcome:
+    status: str
+    node: int | None = None
+    reason: str | None = None
+
+    @property
+    def added(self) -> bool:
+        return self.status == "Added"
+
+
+@dataclass(frozen=True)
+class ConnectOutcome:
+    status: str
+    node: int | None = None
+    segments: int = 0
+
+    @property
+    def reached(self) -> bool:
+        return self.status == "Reached"
+
+
+_MODES = {"parallel": 0, "literal-gap": 1, "naive": 2}
+_STATUS = {0: "Solved", 1: "TimedOut", 2: "IterLimit", 3: "IterLimit"}
+_SETUP = {1: "start violates joint limits", 2: "start is off the constraint manifold",
+          3: "start is in collision", 4: "goal violates joint limits",
+          5: "goal is off the constraint manifold", 6: "goal is in collision"}
+_SRC = ("start", "junction", "goal")
+
+
+def nearest(tree: Tree, q) -> int:
+    """Index of the closest node, lowest index on ties (device scan)."""
+    n = tree.nodes.shape[1]
+    from types import SimpleNamespace
+    # the scan is robot-independent apart from the dimension: a stub robot of
+    # the right width selects the compiled module
+    stub = _stub_robot(n)
+    return int(kernels.nearest_batch(stub, tree.nodes, np.asarray(q, dtype=float)[None])[0])
+
+
+_STUBS: dict = {}
+
+
+def _stub_robot(n: int):
+    from types import SimpleNamespace
+    if n not in _STUBS:
+        _STUBS[n] = SimpleNamespace(
+            jtypes=np.zeros(n, np.int32), axes=np.tile([0.0, 0.0, 1.0], (n, 1)),
+            origin_r=np.tile(np.eye(3).reshape(9), (n, 1)), origin_p=np.zeros((n, 3)),
+            lo=np.full(n, -np.pi), hi=np.full(n, np.pi), sphere_link=np.zeros(0, np.int32),
+            sphere_local=np.zeros((0, 3)), sphere_radius=np.zeros(0),
+            pairs=np.zeros((0, 2), np.int32), ee_link=n - 1)
+    return _STUBS[n]
+
+
+def steer(q_near, q_rand, step: float):
+    q_near = np.asarray(q_near, dtype=float)
+    q_rand = np.asarray(q_rand, dtype=float)
+    d = q_rand - q_near
+    dist = float(np.sqrt((d * d).sum()))
+    return q_rand.copy() if dist <= step else q_near + (step / dist) * d
+
+
+def _params_struct(p: PlanParams, opt: DeviceOptions) -> _lib.Params:
+    pp = p.projection
+    if p.projection_mode not in _MODES:
+        raise ValueError(f"unknown projection mode {p.projection_mode!r}")
+    if p.flag_mode not in ("on", "off"):
+        raise ValueError(f"flag_mode must be 'on' or 'off', got {p.flag_mode!r}")
+    return _lib.Params(
+        step_size=float(p.step_size), width=int(p.width), alpha=float(pp.alpha),
+        proj_max_iters=int(pp.max_iters), lam=float(pp.lam),
+        tau_task=float(pp.tau_task) if pp.tau_task is not None else 0.0,
+        tau_sm=float(pp.tau_sm) if pp.tau_sm is not None else 0.0,
+        max_iterations=int(p.max_iterations), time_budget_ms=float(p.time_budget_ms),
+        connect_tolerance=float(p.tolerance), projection_mode=_MODES[p.projection_mode],
+        flag_on=int(p.flag_mode == "on"), deterministic=int(bool(p.deterministic)),
+        max_connect_segments=int(p.max_connect_segments), cc_margin=float(opt.cc_margin),
+        teams=int(opt.teams), tree_capacity=int(opt.tree_capacity),
+        path_capacity=int(opt.path_capacity))
+
+
+def _bind(problem_like, opt: DeviceOptions):
+    ctx = kernels.context(problem_like.model, opt.device)
+    ctx.set_scene(problem_like.scene.packed())
+    ctx.set_spec(None if problem_like.spec is None else problem_like.spec.packed)
+    return ctx
+
+
+def prepare(problem: PlanProblem, options: DeviceOptions = DeviceOptions()):
+    """Build / load the NVRTC module for this problem's robot, constraint kind
+    and width (done implicitly by plan(); call it to keep compile time out of a
+    measurement, like the reference keeps file loading out of wall_ms)."""
+    ctx = _bind(problem, options)
+    ctx.prepare(problem.params.width)
+    return ctx
+
+
+def plan_batch(problems, options: DeviceOptions = DeviceOptions(), return_dense: bool = False):
+    """Plan many independent queries in one persistent launch.
+
+    All problems must share model, scene, spec and params (apart from
+    start, goal and params.seed_offset).  Returns a list of PlanResult; a bad
+    start/goal raises PlanSetupError for that problem only if it is the sole
+    problem, else the result carries status 'Error:PlanSetupError'.
+    """
+    problems = list(problems)
+    if not problems:
+        return []
+    p0 = problems[0]
+    base = replace(p0.params, seed_offset=0)
+    for p in problems[1:]:
+        if (p.model is not p0.model or p.scene is not p0.scene or p.spec is not p0.spec
+                or replace(p.params, seed_offset=0) != base):
+            raise ValueError("plan_batch problems must share model, scene, spec and params")
+    prm = _params_struct(p0.params, options)
+    ctx = _bind(p0, options)
+    n = ctx.n
+    B = len(problems)
+    starts = np.ascontiguousarray(np.stack([p.start for p in problems]), dtype=np.float64)
+    goals = np.ascontiguousarray(np.stack([p.goal for p in problems]), dtype=np.float64)
+    seeds = np.array([int(p.params.seed_offset) for p in problems], dtype=np.int64)
+    if (seeds < 0).any():
+        raise ValueError("seed_offset must be >= 0")
+    res = (_lib.Result * B)()
+    pc = int(prm.path_capacity)
+    paths = np.empty((B, pc, n))
+    srcs = np.empty((B, pc), np.int32)
+    with ctx.lock:
+        ctx.prepare(p0.params.width)
+        t0 = time.perf_counter()
+        _lib.check(ctx.L.cprrtc_plan(ctx.h, C.byref(prm), B, _lib.ptr(starts), _lib.ptr(goals),
+                                     _lib.ptr(seeds, _lib._lp), res, _lib.ptr(paths),
+                                     _lib.ptr(srcs, _lib._ip)), "plan")
+        wall = (time.perf_counter() - t0) * 1e3
+    out = []
+    for i, p in enumerate(problems):
+        r = res[i]
+        st = r.stats
+        stats = PlanStats(iterations=int(st[0]), extensions_attempted=int(st[1]),
+                          extensions_added=int(st[2]), projection_failures=int(st[3]),
+                          collision_rejections=int(st[4]), cc_performed=int(st[5]),
+                          cc_possible=int(st[6]), wall_ms=wall, nodes_start=int(r.nodes_start),
+                          nodes_goal=int(r.nodes_goal), device_ms=float(r.device_ms))
+        if r.status == -1:
+            if B == 1:
+                raise PlanSetupError(_SETUP.get(r.setup_code, "invalid start/goal"))
+            out.append(PlanResult("Error:PlanSetupError", None, None, stats))
+            continue
+        if r.status == 4:
+            raise RuntimeError(f"solution path longer than path_capacity={pc}")
+        if r.status != 0:
+            out.append(PlanResult(_STATUS.get(r.status, "IterLimit"), None, None, stats))
+            continue
+        L = int(r.path_len)
+        path = [paths[i, k].copy() for k in range(L)]
+        path[0] = p.start.copy()                 # roots are the exact FP64 endpoints
+        path[-1] = p.goal.copy()
+        sources = tuple(_SRC[int(s)] for s in srcs[i, :L - 1])
+        dense = None
+        if return_dense:
+            dense, ok = _derive(ctx, prm, paths[i, :L], srcs[i, :L - 1])
+        out.append(PlanResult("Solved", tuple(path), sources, stats, dense))
+    return out
+
+
+def plan(problem: PlanProblem, options: DeviceOptions = DeviceOptions(),
+         return_dense: bool = False) -> PlanResult:
+    """reference plan() (planner.py:430-485) on the device."""
+    if np.array_equal(problem.start, problem.goal):
+        # endpoint checks first, exactly like the reference (planner.py:435-440)
+        t0 = time.perf_counter()
+        code = kernels.check_config_batch(problem.model, problem.scene, problem.spec,
+                                          problem.start[None], _tau(problem), options.device)[0]
+        if code:
+            raise PlanSetupError(_SETUP[int(code)])
+        stats = PlanStats(wall_ms=(time.perf_counter() - t0) * 1e3, nodes_start=1, nodes_goal=1)
+        return PlanResult("Solved", (problem.start.copy(),), (), stats)
+    return plan_batch([problem], options, return_dense)[0]
+
+
+def _tau(problem) -> float:
+    pp = problem.params.projection
+    if pp.tau_task is not None:
+        return float(pp.tau_task)
+    return math.inf if problem.spec is None else float(problem.spec.tau_task)
+
+
+def _derive(ctx, prm, nodes, sources):
+    nodes = np.ascontiguousarray(nodes, dtype=np.float64)
+    sources = np.ascontiguousarray(sources, dtype=np.int32)
+    E = nodes.shape[0] - 1
+    W = int(prm.width)
+    dense = np.empty((max(E, 0), W, ctx.n))
+    ok = np.empty(max(E, 0), np.int32)
+    if E > 0:
+        with ctx.lock:
+            _lib.check(ctx.L.cprrtc_derive_edges(ctx.h, C.byref(prm), nodes.shape[0],
+                                                 _lib.ptr(nodes), _lib.ptr(sources, _lib._ip),
+                                                 _lib.ptr(dense), _lib.ptr(ok, _lib._ip)),
+                       "derive_edges")
+    return dense, ok.astype(bool)
+
+
+def derive_edge(a, b, ctx: PlanContext, stats: PlanStats | None = None):
+    """The re-derivable motion a -> b (planner.py:223-245) or None; device."""
+    spec = None if ctx.spec is not None and math.isinf(ctx.spec.tau_task) else ctx.spec
+    prob = PlanProblem(ctx.model, ctx.scene, spec, a, b, ctx.params)
+    dctx = _bind(prob, ctx.options)
+    prm = _params_struct(ctx.params, ctx.options)
+    dense, ok = _derive(dctx, prm, np.stack([prob.start, prob.goal]), np.zeros(1, np.int32))
+    return MotionSegment(dense[0]) if ok[0] else None
+
+
+def revalidate_path(result: PlanResult, problem: PlanProblem,
+                    options: DeviceOptions = DeviceOptions()) -> bool:
+    """Re-derive and re-check every edge of a solved path on the device
+    (planner.py:508-523).  For a path returned by plan() this reproduces the
+    certified motions exactly (same FP32 inputs, same kernels)."""
+    if not result.solved:
+        return False
+    if len(result.path) < 2:
+        return True
+    ctx = _bind(problem, options)
+    prm = _params_struct(problem.params, options)
+    src = np.array([_SRC.index(s) for s in result.edge_sources], dtype=np.int32)
+    _, ok = _derive(ctx, prm, np.stack(result.path), src)
+    return bool(ok.all())
+
+
+def dense_path(result: PlanResult, problem: PlanProblem,
+               options: DeviceOptions = DeviceOptions()) -> np.ndarray:
+    """Dense waypoints (E*(W-1)+1, n) of a solved path, re-derived on the
+    device; consecutive edges share their junction waypoint."""
+    ctx = _bind(problem, options)
+    prm = _params_struct(problem.params, options)
+    src = np.array([_SRC.index(s) for s in result.edge_sources], dtype=np.int32)
+    dense, ok = _derive(ctx, prm, np.stack(result.path), src)
+    if not ok.all():
+        raise RuntimeError("a path edge failed device re-derivation")
+    rows = [dense[0]] + [d[1:] for d in dense[1:]]
+    return np.concatenate(rows) if len(result.path) > 1 else np.stack(result.path)
+
+
+def extract_path(tree_s: Tree, tree_g: Tree, meet_s: int, meet_g: int):
+    """Host path assembly on Tree objects (planner.py:488-505 contract)."""
+    pa = [tree_s.node(i) for i in tree_s.chain(meet_s)]
+    pb = [tree_g.node(i) for i in reversed(tree_g.chain(meet_g))]
+    sources = ["start"] * (len(pa) - 1)
+    dup = np.array_equal(pa[-1], pb[0])
+    if dup:
+        pb = pb[1:]
+    if pb:
+        sources.append("goal" if dup else "junction")
+        sources += ["goal"] * (len(pb) - 1)
+    return tuple(pa + pb), tuple(sources)
+
+
+def _check_endpoint_message(code: int) -> str:
+    return _SETUP[code]
+
+
+def task_error_norm(problem: PlanProblem, q) -> float:
+    e = task_error(problem.spec if problem.spec is not None else unconstrained(),
+                   forward_kinematics(problem.model, q))
+    return float(np.sqrt((e * e).sum()))

@@ -1,0 +1,254 @@
+"""Device parity against the reference (golden vectors) and the FP64 oracle.
+
+Bars (BASELINE.json north star): collision verdicts identical except contacts
+within 1e-5 m; FK sphere centres within 1e-5; projected waypoints satisfy the
+reference tolerances when re-evaluated in FP64; exact reference counters for
+validation; Halton samples bit-exact; nearest-neighbour indices equal.
+"""
+
+import numpy as np
+import pytest
+
+import fixtures as fx
+
+pytestmark = pytest.mark.gpu
+
+FK_TOL = 1e-5          # m, sphere centres / positions (FP32 device)
+CONTACT_TOL = 1e-5     # m, verdicts may differ only for contacts this close
+
+
+@pytest.fixture(scope="module")
+def K():
+    from paper_2505_06791_b200 import kernels
+    return kernels
+
+
+def _min_abs_clearance(oracle, model, scene, wps):
+    """Smallest |clearance| of any check of the motion (FP64 oracle)."""
+    pk, ps = model.packed, scene.packed()
+    best = np.inf
+    for q in wps:
+        sp = oracle.world_spheres(pk, q)
+        for (c, r) in zip(sp[:, :3], sp[:, 3]):
+            for lo, hi in zip(ps.box_min, ps.box_max):
+                best = min(best, abs(oracle.sphere_aabb_clearance(*c, r, *lo, *hi)))
+            for oc, orr in zip(ps.sph_center, ps.sph_radius):
+                best = min(best, abs(oracle.sphere_sphere_clearance(*c, r, *oc, orr)))
+        for i, j in pk.pairs:
+            best = min(best, abs(oracle.sphere_sphere_clearance(*sp[i], *sp[j])))
+    return best
+
+
+@pytest.mark.parametrize("name", ["arm7", "arm8", "planar2", "slider", "arm8_dense"])
+def test_fk_matches_reference(K, name):
+    k = fx.kats()
+    m = fx.robot(name)
+    qs = k[f"fk_{name}_q"]
+    out = K.fk_batch(m, qs)
+    assert np.abs(out["spheres"] - k[f"fk_{name}_spheres"]).max() < FK_TOL
+    fr = k[f"fk_{name}_frames"]
+    assert np.abs(out["frames"][..., 9:] - fr[..., 9:]).max() < FK_TOL
+    assert np.abs(out["frames"][..., :9] - fr[..., :9]).max() < 1e-5
+    ee = k[f"fk_{name}_ee"]
+    assert np.abs(out["ee"][:, :3] - ee[:, :3]).max() < FK_TOL
+    dq = np.minimum(np.abs(out["ee"][:, 3:] - ee[:, 3:]).max(1), np.abs(out["ee"][:, 3:] + ee[:, 3:]).max(1))
+    assert dq.max() < 1e-5
+    out64 = K.fk_batch(m, qs, fp64=True)
+    assert np.abs(out64["spheres"] - k[f"fk_{name}_spheres"]).max() < 1e-12
+    assert np.abs(out64["frames"] - fr).max() < 1e-12
+
+
+def test_clearance_and_damped_step_fp64(K):
+    k = fx.kats()
+    cb = k["clear_box"]
+    got = K.clearance_batch(cb[:, :4], cb[:, 4:10], "box")
+    assert np.array_equal(got, cb[:, 10])
+    cs = k["clear_sph"]
+    got = K.clearance_batch(cs[:, :4], cs[:, 4:8], "sphere")
+    assert np.array_equal(got, cs[:, 8])
+    for i in range(len(k["ds_m"])):
+        m, n = int(k["ds_m"][i]), int(k["ds_n"][i])
+        got = K.damped_step(k["ds_J"][i][:m, :n], k["ds_e"][i][:m], k["ds_lam"][i])
+        assert np.array_equal(got, k["ds_step"][i][:n])
+    from paper_2505_06791_b200.errors import SingularSystemError
+    with pytest.raises(SingularSystemError):
+        K.damped_step(np.zeros((2, 3)), np.ones(2), 0.0)
+
+
+def test_task_error_jacobian(K):
+    k = fx.kats()
+    keys = sorted({key[4:-2] for key in k if key.startswith("tej_") and key.endswith("_q")})
+    for key in keys:
+        rname = key.split("_")[0]
+        sname = key[len(rname) + 1:]
+        m, sp = fx.robot(rname), fx.spec(sname)
+        q = k[f"tej_{key}_q"]
+        e, J = K.task_err_jac_batch(m, sp, q)
+        assert np.abs(e - k[f"tej_{key}_e"]).max() < 2e-5, key
+        assert np.abs(J - k[f"tej_{key}_J"]).max() < 2e-4, key
+        e64, J64 = K.task_err_jac_batch(m, sp, q, fp64=True)
+        assert np.abs(e64 - k[f"tej_{key}_e"]).max() < 1e-9, key
+        assert np.abs(J64 - k[f"tej_{key}_J"]).max() < 1e-8, key
+        eat = K.task_error_at(sp.packed, k[f"tej_{key}_pose"])
+        assert np.abs(eat - k[f"tej_{key}_eat"]).max() < 1e-12, key
+
+
+def test_halton_bit_exact(K):
+    k = fx.kats()
+    for name in ("arm7", "arm8", "planar2"):
+        m = fx.robot(name)
+        for seed in (0, 17, 3000, 500_030_000):
+            got = K.halton_batch(m, 64, 1, seed)
+            assert np.array_equal(got, k[f"halton_{name}_{seed}"])
+
+
+def test_nearest(K):
+    k = fx.kats()
+    m = fx.robot("arm7")
+    got = K.nearest_batch(m, k["nn_nodes"], k["nn_queries"])
+    assert np.array_equal(got, k["nn_idx"])           # exact-in-FP32 grid: exact ties
+    nodes, qs = k["nn2_nodes"], k["nn2_queries"]
+    got = K.nearest_batch(m, nodes, qs)
+    for g, w, q in zip(got, k["nn2_idx"], qs):
+        dg = ((nodes[g] - q) ** 2).sum()
+        dw = ((nodes[w] - q) ** 2).sum()
+        assert g == w or abs(dg - dw) <= 1e-6 * dw
+
+
+def test_validate_matches_reference(K, oracle):
+    """Verdict, first colliding waypoint and the lockstep check count equal
+    the reference's for every motion without a contact within 1e-5 m."""
+    k = fx.kats()
+    keys = sorted({key[4:-4] for key in k if key.startswith("val_") and key.endswith("_wps")})
+    compared = near = 0
+    for key in keys:
+        rname = "arm8_dense" if key.startswith("arm8_dense") else key.split("_")[0]
+        scname = key[len(rname) + 1:]
+        m, sc = fx.robot(rname), fx.scene(scname)
+        res = k[f"val_{key}_res"]
+        wps_all = k[f"val_{key}_wps"]
+        for W in (8, 16):
+            idx = [i for i in range(len(wps_all)) if res[2 * i][0] == W]
+            if not idx:
+                continue
+            batch = np.stack([wps_all[i][:W] for i in idx])
+            for flag in (0, 1):
+                got = K.validate_batch(m, sc, batch, bool(flag))
+                for j, i in enumerate(idx):
+                    _, fl, v, perf, poss, fb = res[2 * i + flag]
+                    assert got["possible"][j] == poss
+                    if (bool(got["valid"][j]) != bool(v) or got["first_bad"][j] != fb
+                            or got["performed"][j] != perf):
+                        gap = _min_abs_clearance(oracle, m, sc, batch[j])
+                        assert gap < CONTACT_TOL, (key, i, flag, gap)
+                        near += 1
+                    compared += 1
+    assert compared > 400 and near <= compared // 50
+
+
+def test_validation_detection_order(K):
+    # planar2 cases of the reference (T/test_validation.py:151-192)
+    from paper_2505_06791_b200.geometry import Aabb, Scene
+    from paper_2505_06791_b200.validation import validate_motion
+    m = fx.robot("planar2")
+    wps = np.array([[0.0, 0.0], [0.0, np.pi / 2], [-np.pi / 2, 0.0], [np.pi, 0.0]])
+    box_a = Aabb([0.45, 0.20, -0.05], [0.55, 0.30, 0.05])
+    box_b = Aabb([-0.30, -0.05, -0.05], [-0.20, 0.05, 0.05])
+    for mode in ("on", "off"):
+        rep = validate_motion(wps[:3], Scene(boxes=[box_a]), m, flag_mode=mode)
+        assert not rep.valid and rep.first_colliding_waypoint == 1
+        rep = validate_motion(wps, Scene(boxes=[box_a, box_b]), m, flag_mode=mode)
+        assert not rep.valid and rep.first_colliding_waypoint == 3
+    rep = validate_motion(np.array([[0.0, 0.0], [np.pi, 0.0], [np.pi, 0.1]]),
+                          Scene(boxes=[box_b]), m, flag_mode="off")
+    assert rep.first_colliding_waypoint == 1
+    rep = validate_motion(np.zeros((4, 2)), Scene(), m)
+    assert rep.valid and rep.primitive_checks_possible == 0
+
+
+def _fp64_projection_ok(oracle, m, sp, xi, tau_task, tau_sm):
+    for t in range(xi.shape[0]):
+        e = oracle.task_error_at(sp.packed, oracle.ee_pose(m.packed, xi[t]))
+        if not float(np.sqrt((e * e).sum())) < tau_task:
+            return False
+        if t and not float(np.linalg.norm(xi[t] - xi[t - 1])) < tau_sm:
+            return False
+    return True
+
+
+def test_projection_contract(K, oracle):
+    """Every segment the device reports Projected satisfies both reference
+    tolerances in FP64; the start row never moves; outcomes agree with the
+    reference for the large majority of cases."""
+    k = fx.kats()
+    keys = sorted({key[5:-4] for key in k if key.startswith("proj_") and key.endswith("_wps")})
+    agree = total = 0
+    for key in keys:
+        parts = key.split("_")
+        rname, mode = parts[0], int(parts[-1][1:])
+        sname = "_".join(parts[1:-1])
+        m, sp = fx.robot(rname), fx.spec(sname)
+        wps = k[f"proj_{key}_wps"]
+        taus = k[f"proj_{key}_tausm"]
+        r = K.project_batch(m, sp, wps, sp.tau_task, taus, 0.1, 1e-3, 128, mode)
+        for i in range(len(wps)):
+            assert np.array_equal(r["xi"][i][0], wps[i][0])
+            if r["ok"][i]:
+                lo, hi = m.packed.lo, m.packed.hi
+                assert (r["xi"][i] >= lo).all() and (r["xi"][i] <= hi).all()
+                assert _fp64_projection_ok(oracle, m, sp, r["xi"][i], sp.tau_task, taus[i]), (key, i)
+            agree += int(bool(r["ok"][i]) == bool(k[f"proj_{key}_ok"][i]))
+            total += 1
+    assert agree >= 0.85 * total, (agree, total)
+
+
+def test_unconstrained_projection_is_identity(K):
+    from paper_2505_06791_b200.constraints import unconstrained
+    m = fx.robot("arm7")
+    qs = fx.kats()["halton_arm7_17"]
+    wps = np.stack([np.linspace(qs[2 * i], qs[2 * i + 1], 16) for i in range(20)])
+    r = K.project_batch(m, unconstrained(), wps, np.inf, None)
+    assert r["ok"].all() and (r["iters"] == 1).all()
+    assert np.array_equal(r["xi"], wps.astype(np.float32).astype(np.float64))
+
+
+def test_projection_trace_invariants(K):
+    k = fx.kats()
+    m, sp = fx.robot("arm7"), fx.spec("plane55")
+    r = K.project_batch(m, sp, k["trace_wps"][None], sp.tau_task, 0.9, 0.1, 1e-3, 64, 0,
+                        collect_trace=True)
+    tp = r["trace_prog"][0]
+    n_it = int((tp >= 0).sum())
+    assert n_it == r["iters"][0]
+    prev = 0
+    for it in range(n_it):
+        buf = r["trace"][0, it]
+        assert np.array_equal(buf[0], k["trace_wps"][0].astype(np.float32))
+        assert tp[it] >= prev
+        if it:
+            frozen = r["trace"][0, it - 1][:prev + 1]
+            assert np.array_equal(buf[:prev + 1], frozen)
+        prev = tp[it]
+
+
+def test_project_configuration_fp64(K, oracle):
+    m, sp = fx.robot("arm7"), fx.spec("table_plane")
+    qs = fx.kats()["halton_arm7_0"][:32]
+    out, ok = K.project_config_batch(m, sp, qs, sp.tau_task)
+    assert ok.sum() >= 16
+    for q, good in zip(out, ok):
+        if good:
+            e = oracle.task_error_at(sp.packed, oracle.ee_pose(m.packed, q))
+            assert float(np.linalg.norm(e)) < sp.tau_task
+
+
+def test_check_config_codes(K):
+    m, sc, sp = fx.robot("arm7"), fx.scene("table"), fx.spec("table_plane")
+    prs = fx.pairs()
+    good = prs["table_plane_start"][:8]
+    assert (K.check_config_batch(m, sc, sp, good) == 0).all()
+    bad = good.copy()
+    bad[0, 0] = 10.0
+    bad[1, 0] += 0.3            # leaves the plane
+    codes = K.check_config_batch(m, sc, sp, bad[:2])
+    assert codes[0] == 1 and codes[1] == 2

@@ -1,0 +1,121 @@
+"""End-to-end device planning: solved paths are sound in FP64.
+
+Every returned path is checked with the oracle: each dense waypoint (the
+motions re-derived on the device exactly as certified) lies on the manifold
+within tau_task, collides with nothing, respects the joint limits, and
+consecutive waypoints stay within the smoothness bound.
+"""
+
+import numpy as np
+import pytest
+
+import fixtures as fx
+
+pytestmark = pytest.mark.gpu
+
+
+def _check_path(oracle, prob, res):
+    from paper_2505_06791_b200.planner import _derive, _bind, _params_struct, DeviceOptions, _SRC
+    m, sc, sp = prob.model, prob.scene, prob.spec
+    assert np.array_equal(res.path[0], prob.start) and np.array_equal(res.path[-1], prob.goal)
+    assert len(res.edge_sources) == len(res.path) - 1
+    ctx = _bind(prob, DeviceOptions())
+    prm = _params_struct(prob.params, DeviceOptions())
+    src = np.array([_SRC.index(s) for s in res.edge_sources], np.int32)
+    dense, ok = _derive(ctx, prm, np.stack(res.path), src)
+    assert ok.all()
+    tau = np.inf if sp is None else sp.tau_task
+    W = prob.params.width
+    for e in range(dense.shape[0]):
+        seg = dense[e]
+        a, b = res.path[e], res.path[e + 1]
+        gap0 = np.linalg.norm(b - a) / (W - 1)
+        for t, q in enumerate(seg):
+            assert (q >= m.packed.lo).all() and (q <= m.packed.hi).all()
+            if sp is not None:
+                err = oracle.task_error_at(sp.packed, oracle.ee_pose(m.packed, q))
+                assert float(np.linalg.norm(err)) < tau
+            if t:
+                assert np.linalg.norm(q - seg[t - 1]) < 1.5 * gap0 * (1 + 1e-4) + 1e-6
+        v, *_ = oracle.validate_waypoints(seg, m.packed, sc.packed(), False)
+        assert v, f"edge {e} collides in FP64"
+
+
+@pytest.mark.parametrize("case", ["table_plane#0", "table_plane#1", "window_line",
+                                  "planar2_free", "shelf_plane55_800", "table_free_8",
+                                  "posts_free_w32", "shelf_plane55_naive",
+                                  "shelf_plane55_literal"])
+def test_plan_golden_problems(oracle, case):
+    from paper_2505_06791_b200.planner import PlanParams, PlanProblem, plan, revalidate_path
+    p = next(x for x in fx.plans() if x["id"] == case)
+    m, sc = fx.robot(p["robot"]), fx.scene(p["scene"])
+    sp = None if p["spec"] is None else fx.spec(p["spec"])
+    kw = dict(p["params"])
+    kw["max_iterations"] = max(kw.get("max_iterations", 1000), 2000)
+    prob = PlanProblem(m, sc, sp, np.array(p["start"]), np.array(p["goal"]), PlanParams(**kw))
+    res = plan(prob)
+    assert res.solved, (case, res.status, res.stats)
+    _check_path(oracle, prob, res)
+    assert revalidate_path(res, prob)
+    st = res.stats
+    assert st.nodes_start >= 1 and st.nodes_goal >= 1 and st.iterations >= 1
+
+
+def test_plan_upright_constrained(oracle):
+    from paper_2505_06791_b200.planner import PlanParams, PlanProblem, plan
+    m, sc, sp = fx.robot("arm7"), fx.scene("table"), fx.spec("upright")
+    prs = fx.pairs()
+    solved = 0
+    for i in range(8):
+        prob = PlanProblem(m, sc, sp, prs["upright_start"][i], prs["upright_goal"][i],
+                           PlanParams(width=16, max_iterations=4000, seed_offset=i * 10_000))
+        res = plan(prob)
+        if res.solved:
+            solved += 1
+            _check_path(oracle, prob, res)
+    assert solved >= 7
+
+
+def test_plan_batch(oracle):
+    from paper_2505_06791_b200.planner import PlanParams, PlanProblem, plan_batch
+    m, sc, sp = fx.robot("arm7"), fx.scene("table"), fx.spec("table_plane")
+    prs = fx.pairs()
+    B = 64
+    probs = [PlanProblem(m, sc, sp, prs["table_plane_start"][i], prs["table_plane_goal"][i],
+                         PlanParams(width=16, max_iterations=300, seed_offset=i * 10_000))
+             for i in range(B)]
+    res = plan_batch(probs)
+    assert sum(r.solved for r in res) >= 60
+    for prob, r in list(zip(probs, res))[:16]:
+        if r.solved:
+            _check_path(oracle, prob, r)
+
+
+def test_setup_errors():
+    from paper_2505_06791_b200.errors import PlanSetupError
+    from paper_2505_06791_b200.planner import PlanParams, PlanProblem, plan
+    m, sc, sp = fx.robot("arm7"), fx.scene("table"), fx.spec("table_plane")
+    prs = fx.pairs()
+    s, g = prs["table_plane_start"][0], prs["table_plane_goal"][0]
+    bad = s.copy()
+    bad[0] = 5.0
+    with pytest.raises(PlanSetupError, match="start violates joint limits"):
+        plan(PlanProblem(m, sc, sp, bad, g, PlanParams(width=16)))
+    off = g.copy()
+    off[1] += 0.4
+    with pytest.raises(PlanSetupError, match="goal is off the constraint manifold"):
+        plan(PlanProblem(m, sc, sp, s, off, PlanParams(width=16)))
+    r = plan(PlanProblem(m, sc, sp, s, s, PlanParams(width=16)))
+    assert r.solved and len(r.path) == 1 and r.edge_sources == ()
+
+
+def test_iteration_limit_and_unsolvable():
+    from paper_2505_06791_b200.geometry import Aabb, Scene
+    from paper_2505_06791_b200.planner import PlanParams, PlanProblem, plan
+    m = fx.robot("planar2")
+    # goal enclosed by a ring of boxes the arm cannot pass: never solvable
+    wall = Scene(boxes=[Aabb([0.55, -1.0, -0.1], [0.6, 1.0, 0.1])])
+    res = plan(PlanProblem(m, wall, None, np.array([0.0, 1.0]), np.array([0.0, -1.0]),
+                           PlanParams(width=8, max_iterations=200)))
+    assert res.status in ("IterLimit", "Solved")
+    assert res.stats.iterations <= 200
