@@ -109,7 +109,10 @@ typedef struct {
 enum {
     CPRRTC_ST_ITERATIONS = 0, CPRRTC_ST_EXT_ATTEMPTED, CPRRTC_ST_EXT_ADDED,
     CPRRTC_ST_PROJ_FAIL, CPRRTC_ST_COLL_REJECT, CPRRTC_ST_CC_PERFORMED,
-    CPRRTC_ST_CC_POSSIBLE, CPRRTC_ST_GPU_CHECKS, CPRRTC_ST_COUNT
+    CPRRTC_ST_CC_POSSIBLE, CPRRTC_ST_GPU_CHECKS,
+    /* device work units (roofline accounting) */
+    CPRRTC_ST_STAGE1_EVALS, CPRRTC_ST_CC_FK_EVALS, CPRRTC_ST_NN_NODES, CPRRTC_ST_PROJ_ITERS,
+    CPRRTC_ST_COUNT
 };
 
 typedef struct {
@@ -152,6 +155,8 @@ CPRRTC_API int cprrtc_prepare(void *ctx, int width);
 CPRRTC_API int64_t cprrtc_launch_count(void *ctx);
 /* device time (CUDA events) of the last cprrtc_plan: whole call / plan kernel */
 CPRRTC_API int cprrtc_last_timing(void *ctx, double *total_ms, double *plan_kernel_ms);
+/* overwrite `bytes` of device scratch (L2 flush between timed iterations) */
+CPRRTC_API int cprrtc_flush_l2(void *ctx, size_t bytes);
 
 /* frames / world spheres / ee_pose  (maniplan/_kernels/pure.py:251-271) */
 CPRRTC_API int cprrtc_fk(void *ctx, int B, const double *q, int fp64, double *frames,
@@ -180,6 +185,12 @@ CPRRTC_API int cprrtc_project(void *ctx, int B, int W, const double *wps, const 
 /* nearest (planner.py:198-201) for Q queries over N nodes (row-major) */
 CPRRTC_API int cprrtc_nearest(void *ctx, int N, const double *nodes, int Q, const double *queries,
                    int32_t *idx);
+/* the same scan over n_trees trees of N nodes each, query i on tree i % n_trees
+ * (nodes (n_trees, N, n)); the HBM-streaming NN benchmark of bench.py.  The
+ * kernel time of this and of cprrtc_validate is cprrtc_last_timing's
+ * plan_kernel_ms. */
+CPRRTC_API int cprrtc_nearest_trees(void *ctx, int N, int n_trees, const float *reserved,
+                                    const double *nodes, int Q, const double *queries, int32_t *idx);
 /* HaltonState.next_sample (maniplan/sampling.py:65-81), FP64 bit-exact:
  * rows first_index .. first_index+count-1, mapped into [lo, hi] (NULL: the
  * robot's joint limits) */

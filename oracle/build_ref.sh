@@ -21,14 +21,20 @@ import glob, os
 from setuptools import setup, Extension
 from Cython.Build import cythonize
 flags = ["-O3", "-ffp-contract=off", "-fno-builtin-sin", "-fno-builtin-cos"]
-exts = [Extension("maniplan._kernels._compiled", ["src/maniplan/_kernels/_compiled.pyx"],
-                  extra_compile_args=flags)]
+kern = [Extension("maniplan._kernels._compiled", ["src/maniplan/_kernels/_compiled.pyx"],
+                 extra_compile_args=flags)]
+mods = []
 for path in sorted(glob.glob("src/maniplan/**/*.py", recursive=True)):
     mod = path[len("src/"):-3].replace(os.sep, ".")
-    exts.append(Extension(mod, [path], extra_compile_args=flags))
-setup(name="maniplan_ref", ext_modules=cythonize(exts, compiler_directives={
-    "language_level": "3", "boundscheck": False, "wraparound": False, "cdivision": True,
-    "binding": True}, quiet=True, nthreads=8), script_args=["build_ext", "--build-lib", "build_out", "--parallel", "8"])
+    mods.append(Extension(mod, [path], extra_compile_args=flags))
+# the kernel backend keeps the reference's own directives (pkg/setup.py:55-60);
+# the pure-Python modules keep Python semantics (bounds / negative indices / %)
+exts = cythonize(kern, compiler_directives={"language_level": "3", "boundscheck": False,
+                 "wraparound": False, "cdivision": True}, quiet=True, nthreads=8)
+exts += cythonize(mods, compiler_directives={"language_level": "3", "binding": True},
+                  quiet=True, nthreads=8)
+setup(name="maniplan_ref", ext_modules=exts,
+      script_args=["build_ext", "--build-lib", "build_out", "--parallel", "8"])
 PYEOF
 ( cd "$TMP" && "$PY" setup_ref.py > build.log 2>&1 ) || { tail -30 "$TMP/build.log"; exit 1; }
 rm -rf "$OUT"

@@ -29,7 +29,7 @@ EXPORTS = (
     "cprrtc_last_timing", "cprrtc_fk", "cprrtc_task_err_jac", "cprrtc_task_error_at",
     "cprrtc_project_config", "cprrtc_check_config", "cprrtc_validate", "cprrtc_project",
     "cprrtc_nearest", "cprrtc_halton", "cprrtc_plan", "cprrtc_derive_edges",
-    "cprrtc_clearance", "cprrtc_damped_step",
+    "cprrtc_clearance", "cprrtc_damped_step", "cprrtc_flush_l2", "cprrtc_nearest_trees",
 )
 
 
@@ -62,7 +62,7 @@ class Params(C.Structure):
                 ("teams", C.c_int), ("tree_capacity", C.c_int), ("path_capacity", C.c_int)]
 
 
-ST_COUNT = 8
+ST_COUNT = 12
 
 
 class Result(C.Structure):
@@ -88,6 +88,7 @@ def load():
             L.cprrtc_last_error.restype = C.c_char_p
             L.cprrtc_launch_count.restype = C.c_int64
             L.cprrtc_launch_count.argtypes = [C.c_void_p]
+            L.cprrtc_flush_l2.argtypes = [C.c_void_p, C.c_size_t]
             for name in EXPORTS:
                 if name not in ("cprrtc_last_error", "cprrtc_launch_count", "cprrtc_abi_version"):
                     getattr(L, name).restype = C.c_int

@@ -329,7 +329,9 @@ __device__ __noinline__ float cp_err_norm(const Con<float>& c, const float* q) {
 // to trace[it-1] and the prefix to trace_prog[it-1].
 __device__ bool cp_project(const Team& tm, float (*seg)[CP_NP], int W, const Con<float>& c,
                            const ProjArgs& pa, int* iters_out, int* prog_out,
-                           float* trace = nullptr, int* trace_prog = nullptr) {
+                           float* trace = nullptr, int* trace_prog = nullptr,
+                           unsigned long long* n_stage1 = nullptr) {
+    unsigned long long s1 = 0;
     const int t = (int)tm.lane;
     const bool row = t < W;
     float tau_sm = pa.tau_sm_fixed;
@@ -416,6 +418,7 @@ __device__ bool cp_project(const Team& tm, float (*seg)[CP_NP], int W, const Con
                 if (!tm.any(!cheap)) { valid = act; full_step = false; }
             }
             if (full_step && act) valid = cp_stage1(c, pa, xt, xp, tau_sm, xn);
+            if (n_stage1 && full_step) s1 += __popc(tm.ballot(act));
             unsigned vm = tm.ballot(act && valid) & full;
             int np = prog;
             if (pa.mode == 1) {   // literal-gap: largest valid index (pure.py:560-563)
@@ -464,7 +467,8 @@ __device__ bool cp_project(const Team& tm, float (*seg)[CP_NP], int W, const Con
 #pragma unroll
             for (int k = 0; k < CP_N; k++) {
                 q[k] = seg[t][k];
-                qc[k] = fminf(fmaxf(q[k], (float)cp_lo(k)), (float)cp_hi(k));
+                // row 0 is the fixed start (an existing tree node): never clamped
+                qc[k] = t == 0 ? q[k] : fminf(fmaxf(q[k], cp_lo_f(k)), cp_hi_f(k));
                 moved |= !(qc[k] == q[k]);
             }
         }
@@ -500,6 +504,7 @@ __device__ bool cp_project(const Team& tm, float (*seg)[CP_NP], int W, const Con
     }
     *iters_out = iters;
     *prog_out = prog;
+    if (n_stage1) *n_stage1 += s1;
     return ok;
 }
 
@@ -512,6 +517,7 @@ struct ValOut {
     int first_bad;         // waypoint of the first detection in (round, waypoint) order
     i64 performed;         // lockstep-equivalent count (reference semantics), exact mode
     i64 gpu_checks;        // checks this team actually evaluated
+    int fk_evals;          // waypoint FK evaluations
 };
 
 __device__ __forceinline__ bool cp_hit_box(float cx, float cy, float cz, float r2, float4 c, float4 h) {
@@ -586,6 +592,7 @@ __device__ ValOut cp_validate(const Team& tm, const float (*seg)[CP_NP], int W, 
     o.first_bad = o.valid ? -1 : idx;
     o.performed = (flag_on && !o.valid) ? (i64)key * W + idx + 1 : per * W;
     o.gpu_checks = rounds_done * (W - t_first);
+    o.fk_evals = W - t_first;
     return o;
 }
 
@@ -732,6 +739,7 @@ __device__ __forceinline__ bool cp_check_motion(const Team& tm, TeamWS& ws, cons
     st.v[ST_CCPERF] += v.gpu_checks;
     st.v[ST_CCPOSS] += (u64)((i64)CP_S * (sc.nb + sc.ne) + CP_P) * (A.W - 1);
     st.v[ST_GPUCHK] += v.gpu_checks;
+    st.v[ST_FKCC] += v.fk_evals;
     if (!v.valid) st.v[ST_CREJ]++;
     return v.valid;
 }
@@ -741,7 +749,9 @@ __device__ bool cp_derive_edge(const Team& tm, TeamWS& ws, const PlanArgs& A, co
                                const float* a, const float* b, Stats& st) {
     cp_interp(tm, ws.seg, A.W, a, b);
     int it, pr;
-    if (!cp_project(tm, ws.seg, A.W, A.con, A.pa, &it, &pr)) {
+    bool okp = cp_project(tm, ws.seg, A.W, A.con, A.pa, &it, &pr, nullptr, nullptr, &st.v[ST_STAGE1]);
+    st.v[ST_PROJITER] += it;
+    if (!okp) {
         st.v[ST_PFAIL]++;
         return false;
     }
@@ -778,7 +788,9 @@ __device__ __forceinline__ void cp_load_node(const Team& tm, const PlanArgs& A, 
 // Returns the meet node index if Reached, else -1.
 __device__ int cp_connect(const Team& tm, TeamWS& ws, const PlanArgs& A, const SceneSm& sc,
                           QueryState& Q, int qi, int k, Stats& st) {
-    int icur = cp_nearest(tm, cp_tree(A, qi, k), A.cap, cp_count(A, Q, k), ws.qt);
+    const int cnt = cp_count(A, Q, k);
+    st.v[ST_NNODES] += cnt;
+    int icur = cp_nearest(tm, cp_tree(A, qi, k), A.cap, cnt, ws.qt);
     cp_load_node(tm, A, qi, k, icur, ws.qc);
     float dist = cp_vec_dist(tm, ws.qc, ws.qt);
     if (dist <= A.tol) return icur;
@@ -787,7 +799,9 @@ __device__ int cp_connect(const Team& tm, TeamWS& ws, const PlanArgs& A, const S
         cp_steer(tm, ws.qc, ws.qt, A.step, ws.qs);
         cp_interp(tm, ws.seg, A.W, ws.qc, ws.qs);
         int it, pr;
-        if (!cp_project(tm, ws.seg, A.W, A.con, A.pa, &it, &pr)) { st.v[ST_PFAIL]++; return -1; }
+        bool okp = cp_project(tm, ws.seg, A.W, A.con, A.pa, &it, &pr, nullptr, nullptr, &st.v[ST_STAGE1]);
+        st.v[ST_PROJITER] += it;
+        if (!okp) { st.v[ST_PFAIL]++; return -1; }
         cp_copy(tm, ws.qe, ws.seg[A.W - 1]);
         if (cp_vec_equal(tm, ws.qe, ws.qs)) {
             if (!cp_check_motion(tm, ws, A, sc, st)) return -1;
@@ -817,7 +831,9 @@ __device__ void cp_plan_query(const Team& tm, TeamWS& ws, const PlanArgs& A, con
         if (tm.lane == 0) it = atomicAdd(&Q.next_sample, 1) + 1;
         it = tm.bcast(it, 0);
         if (it > A.max_iterations) {
-            if (tm.lane == 0) { atomicExch(&Q.exhausted, 1); atomicExch(&Q.stop, 1); }
+            // out of samples: no new extensions, but extensions already in
+            // flight (other teams) finish their connect
+            if (tm.lane == 0) atomicExch(&Q.exhausted, 1);
             break;
         }
         st.v[ST_ITER]++;
@@ -827,13 +843,17 @@ __device__ void cp_plan_query(const Team& tm, TeamWS& ws, const PlanArgs& A, con
         if ((int)tm.lane < CP_N) ws.qr[tm.lane] = (float)cp_halton((i64)it + Q.seed_offset, tm.lane);
         tm.sync();
         // _attempt_extend (planner.py:265-306)
-        const int inear = cp_nearest(tm, cp_tree(A, qi, a), A.cap, cp_count(A, Q, a), ws.qr);
+        const int cnt_a = cp_count(A, Q, a);
+        st.v[ST_NNODES] += cnt_a;
+        const int inear = cp_nearest(tm, cp_tree(A, qi, a), A.cap, cnt_a, ws.qr);
         cp_load_node(tm, A, qi, a, inear, ws.qn);
         cp_steer(tm, ws.qn, ws.qr, A.step, ws.qs);
         if (cp_vec_equal(tm, ws.qs, ws.qn)) continue;              // degenerate
         cp_interp(tm, ws.seg, W, ws.qn, ws.qs);
         int pit, ppr;
-        if (!cp_project(tm, ws.seg, W, A.con, A.pa, &pit, &ppr)) { st.v[ST_PFAIL]++; continue; }
+        bool okp = cp_project(tm, ws.seg, W, A.con, A.pa, &pit, &ppr, nullptr, nullptr, &st.v[ST_STAGE1]);
+        st.v[ST_PROJITER] += pit;
+        if (!okp) { st.v[ST_PFAIL]++; continue; }
         cp_copy(tm, ws.qe, ws.seg[W - 1]);
         if (cp_vec_equal(tm, ws.qe, ws.qn)) continue;              // degenerate
         if (cp_vec_equal(tm, ws.qe, ws.qs)) {
@@ -911,7 +931,8 @@ cp_plan_kernel(const __grid_constant__ PlanArgs A) {
                 for (int j = 0; j < A.nq; j++) {
                     int c = (s0 + j) % A.nq;
                     QueryState& Q = A.qs[c];
-                    if (!cp_ldvol(&Q.stop) && !cp_ldvol(&Q.solved) && Q.setup_code == 0) { qi = c; break; }
+                    if (!cp_ldvol(&Q.stop) && !cp_ldvol(&Q.solved) && !cp_ldvol(&Q.exhausted) &&
+                        Q.setup_code == 0) { qi = c; break; }
                 }
             }
         }
@@ -1268,12 +1289,13 @@ cp_project_kernel(int B, int W, Con<float> con, ProjArgs pa, const float* tau_sm
 
 // Batch nearest neighbour over an SoA node array (planner.py:198-201).
 extern "C" __global__ void __launch_bounds__(CP_NTHREADS, 1)
-cp_nearest_kernel(int count, int cap, const float* nodes, int Q, const float* queries, int* idx) {
+cp_nearest_kernel(int count, int cap, int n_trees, const float* nodes, int Q, const float* queries, int* idx) {
     Team tm;
     const int tpc = CP_NTHREADS / CP_G;
     const int team_in_cta = (threadIdx.x >> 5) * (32 / CP_G) + (threadIdx.x & 31) / CP_G;
     for (int i = blockIdx.x * tpc + team_in_cta; i < Q; i += gridDim.x * tpc) {
-        int r = cp_nearest(tm, nodes, cap, count, queries + (size_t)i * CP_N);
+        const float* tree = nodes + (size_t)(i % n_trees) * CP_N * cap;
+        int r = cp_nearest(tm, tree, cap, count, queries + (size_t)i * CP_N);
         if (tm.lane == 0) idx[i] = r;
     }
 }

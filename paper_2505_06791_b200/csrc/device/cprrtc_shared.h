@@ -35,7 +35,9 @@ struct SceneSm {
     int nb, ne;
 };
 
-enum { ST_ITER = 0, ST_ATT, ST_ADDED, ST_PFAIL, ST_CREJ, ST_CCPERF, ST_CCPOSS, ST_GPUCHK, ST_NSTAT };
+// stats / work-unit counters (the last four feed the roofline in bench.py)
+enum { ST_ITER = 0, ST_ATT, ST_ADDED, ST_PFAIL, ST_CREJ, ST_CCPERF, ST_CCPOSS, ST_GPUCHK,
+       ST_STAGE1, ST_FKCC, ST_NNODES, ST_PROJITER, ST_NSTAT };
 
 // per-query planner state in HBM
 struct QueryState {

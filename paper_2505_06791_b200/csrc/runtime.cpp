@@ -626,6 +626,15 @@ int cprrtc_last_timing(void* p, double* total_ms, double* plan_ms) {
     return 0;
 }
 
+int cprrtc_flush_l2(void* p, size_t bytes) {
+    Ctx* c = C(p);
+    if (!c) return fail(CPRRTC_EARG, "NULL context");
+    if (int rc = set_device(c)) return rc;
+    if (int rc = c->scratch[8].ensure(bytes)) return rc;
+    CUDA_TRY(cudaMemsetAsync(c->scratch[8].p, (int)(c->launches & 0xff), bytes, c->stream));
+    return sync(c);
+}
+
 int cprrtc_fk(void* p, int B, const double* q, int fp64, double* frames, double* axes, double* origins, double* ee,
               double* spheres) {
     Ctx* c = C(p);
@@ -777,12 +786,20 @@ int cprrtc_validate(void* p, int B, int W, const double* wps, int flag_on, doubl
     const int tpc = kThreads / m->G;
     int grid = (B + tpc - 1) / tpc;
     if (grid > 64 * c->sms) grid = 64 * c->sms;
+    CUDA_TRY(cudaEventRecord(c->ev[1], c->stream));
     if (int rc2 = launch(c, m, "cp_validate_kernel", grid, 1, kThreads, team_smem(c, m, true), args)) return rc2;
+    CUDA_TRY(cudaEventRecord(c->ev[2], c->stream));
     download(c, valid, c->scratch[1], (size_t)B);
     download(c, first_bad, c->scratch[2], (size_t)B);
     download(c, performed, c->scratch[3], (size_t)B);
     if (gpu_checks) download(c, gpu_checks, c->scratch[4], (size_t)B);
     if (int rc3 = sync(c)) return rc3;
+    {
+        float t = 0;
+        cudaEventElapsedTime(&t, c->ev[1], c->ev[2]);
+        c->last_plan_ms = t;
+        c->last_total_ms = t;
+    }
     if (possible) {
         const int64_t per = (int64_t)c->S * (c->nb + c->ne) + c->P;
         for (int i = 0; i < B; i++) possible[i] = per * W;
@@ -861,18 +878,32 @@ int cprrtc_project(void* p, int B, int W, const double* wps, const double* tau_s
     return 0;
 }
 
+int cprrtc_nearest_trees(void* p, int N, int n_trees, const float* soa_dev_or_null, const double* nodes, int Q,
+                         const double* queries, int32_t* idx);
+
 int cprrtc_nearest(void* p, int N, const double* nodes, int Q, const double* queries, int32_t* idx) {
+    return cprrtc_nearest_trees(p, N, 1, nullptr, nodes, Q, queries, idx);
+}
+
+// Q queries; query i scans tree (i % n_trees), each of N nodes.  nodes:
+// (n_trees, N, n) row-major host array (converted to the SoA device layout).
+int cprrtc_nearest_trees(void* p, int N, int n_trees, const float* unused, const double* nodes, int Q,
+                         const double* queries, int32_t* idx) {
+    (void)unused;
     Ctx* c = C(p);
-    if (!c || N < 1 || Q < 0 || !nodes || (Q && (!queries || !idx))) return fail(CPRRTC_EARG, "bad argument");
+    if (!c || N < 1 || n_trees < 1 || Q < 0 || !nodes || (Q && (!queries || !idx)))
+        return fail(CPRRTC_EARG, "bad argument");
     if (Q == 0) return 0;
     if (int rc = set_device(c)) return rc;
     Module* m;
     if (int rc = get_module(c, 16, c->kind, c->orient, 1, &m)) return rc;
     const int n = c->n;
     const int cap = (N + 127) / 128 * 128;
-    std::vector<float> soa((size_t)n * cap, NAN);
-    for (int i = 0; i < N; i++)
-        for (int k = 0; k < n; k++) soa[(size_t)k * cap + i] = (float)nodes[(size_t)i * n + k];
+    std::vector<float> soa((size_t)n_trees * n * cap, NAN);
+    for (int t = 0; t < n_trees; t++)
+        for (int i = 0; i < N; i++)
+            for (int k = 0; k < n; k++)
+                soa[((size_t)t * n + k) * cap + i] = (float)nodes[((size_t)t * N + i) * n + k];
     std::vector<float> qf((size_t)Q * n);
     for (size_t i = 0; i < qf.size(); i++) qf[i] = (float)queries[i];
     int rc = upload(c, c->scratch[0], soa.data(), soa.size());
@@ -882,13 +913,19 @@ int cprrtc_nearest(void* p, int N, const double* nodes, int Q, const double* que
     const float* dn = c->scratch[0].as<float>();
     const float* dq = c->scratch[1].as<float>();
     int* di = c->scratch[2].as<int>();
-    void* args[] = {&N, (void*)&cap, &dn, &Q, &dq, &di};
+    void* args[] = {&N, (void*)&cap, &n_trees, &dn, &Q, &dq, &di};
     const int tpc = kThreads / m->G;
     int grid = (Q + tpc - 1) / tpc;
     if (grid > 64 * c->sms) grid = 64 * c->sms;
+    CUDA_TRY(cudaEventRecord(c->ev[1], c->stream));
     if (int rc2 = launch(c, m, "cp_nearest_kernel", grid, 1, kThreads, 0, args)) return rc2;
+    CUDA_TRY(cudaEventRecord(c->ev[2], c->stream));
     download(c, idx, c->scratch[2], (size_t)Q);
-    return sync(c);
+    if (int rc3 = sync(c)) return rc3;
+    float t = 0;
+    cudaEventElapsedTime(&t, c->ev[1], c->ev[2]);
+    c->last_plan_ms = c->last_total_ms = t;
+    return 0;
 }
 
 int cprrtc_halton(void* p, int count, int64_t first_index, int64_t seed_offset, const double* lo, const double* hi,
@@ -994,10 +1031,10 @@ int cprrtc_plan(void* p, const cprrtc_params* prm, int B, const double* starts, 
     std::memcpy(hin + (size_t)B * n, goals, (size_t)B * n * 8);
     long long* hseed = reinterpret_cast<long long*>(hin + (size_t)2 * B * n);
     for (int i = 0; i < B; i++) hseed[i] = seeds ? seeds[i] : 0;
-    CUDA_TRY(cudaEventRecord(c->ev[0], c->stream));
     CUDA_TRY(cudaMemcpyAsync(c->d_starts.p, hin, (size_t)B * n * 8, cudaMemcpyHostToDevice, c->stream));
     CUDA_TRY(cudaMemcpyAsync(c->d_goals.p, hin + (size_t)B * n, (size_t)B * n * 8, cudaMemcpyHostToDevice, c->stream));
     CUDA_TRY(cudaMemcpyAsync(c->d_seeds.p, hseed, (size_t)B * 8, cudaMemcpyHostToDevice, c->stream));
+    CUDA_TRY(cudaEventRecord(c->ev[0], c->stream));   // device-resident inputs from here on
     CUDA_TRY(cudaMemsetAsync(c->counters.p, 0, 64, c->stream));
     // 1) refill the node slots used last time with NaN
     {
@@ -1032,9 +1069,18 @@ int cprrtc_plan(void* p, const cprrtc_params* prm, int B, const double* starts, 
     }
     const int tpc = kThreads / m->G;
     int grid = m->plan_occ * c->sms;
-    if (prm->teams > 0) {
-        int g = (prm->teams + tpc - 1) / tpc;
-        if (g < grid) grid = g;
+    // concurrency: the requested team count, else every resident team -- but
+    // never more than a quarter of the sample budget, so that at least ~4
+    // waves of extensions build on each other (samples are the reference's
+    // iterations: a first wave that consumed them all would only grow stars
+    // around the roots)
+    long long want_teams = prm->teams > 0 ? prm->teams : (long long)grid * tpc;
+    long long budget_teams = (long long)B * prm->max_iterations / 4;
+    if (budget_teams < tpc) budget_teams = tpc;
+    if (want_teams > budget_teams) want_teams = budget_teams;
+    {
+        long long g = (want_teams + tpc - 1) / tpc;
+        if (g < grid) grid = (int)g;
     }
     if (grid < 1) grid = 1;
     CUDA_TRY(cudaEventRecord(c->ev[1], c->stream));

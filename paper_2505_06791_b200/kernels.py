@@ -127,6 +127,9 @@ class Context:
     def launches(self) -> int:
         return int(self.L.cprrtc_launch_count(self.h))
 
+    def flush_l2(self, nbytes: int = 256 << 20):
+        _lib.check(self.L.cprrtc_flush_l2(self.h, int(nbytes)), "flush_l2")
+
     def last_timing(self):
         a, b = C.c_double(), C.c_double()
         self.L.cprrtc_last_timing(self.h, C.byref(a), C.byref(b))
@@ -273,6 +276,7 @@ def validate_batch(model, scene, wps, flag_on: bool = True, margin: float = 0.0,
             ctx.h, B, W, _lib.ptr(wps), int(bool(flag_on)), C.c_double(margin),
             _lib.ptr(r["valid"], _ip), _lib.ptr(r["first_bad"], _ip), _lib.ptr(r["performed"], _lp),
             _lib.ptr(r["possible"], _lp), _lib.ptr(r["gpu_checks"], _lp)), "validate")
+        r["kernel_ms"] = ctx.last_timing()[1]
     r["valid"] = r["valid"].astype(bool)
     return r
 
@@ -315,6 +319,20 @@ def nearest_batch(model, nodes, queries, device: int = 0):
         _lib.check(ctx.L.cprrtc_nearest(ctx.h, nodes.shape[0], _lib.ptr(nodes), queries.shape[0],
                                         _lib.ptr(queries), _lib.ptr(idx, _ip)), "nearest")
     return idx
+
+
+def nearest_trees(model, nodes, queries, device: int = 0):
+    """Query i scans tree i % T of nodes (T, N, n); returns (idx, kernel_ms)."""
+    ctx = context(model, device)
+    nodes = _f64(nodes)
+    T, N, n = nodes.shape
+    queries = _f64(queries).reshape(-1, n)
+    idx = np.empty(queries.shape[0], np.int32)
+    with ctx.lock:
+        _lib.check(ctx.L.cprrtc_nearest_trees(ctx.h, N, T, None, _lib.ptr(nodes), queries.shape[0],
+                                              _lib.ptr(queries), _lib.ptr(idx, _ip)), "nearest")
+        ms = ctx.last_timing()[1]
+    return idx, ms
 
 
 def halton_batch(model, count: int, first_index: int = 1, seed_offset: int = 0, limits=None,

@@ -152,6 +152,11 @@ class PlanStats:
     nodes_start: int = 0
     nodes_goal: int = 0
     device_ms: float = 0.0        # query time on the device (globaltimer)
+    # device work units (roofline accounting; no reference counterpart)
+    stage1_evals: int = 0
+    cc_fk_evals: int = 0
+    nn_nodes: int = 0
+    proj_iters: int = 0
 
 
 @dataclass(frozen=True)
@@ -325,7 +330,9 @@ def plan_batch(problems, options: DeviceOptions = DeviceOptions(), return_dense:
                           extensions_added=int(st[2]), projection_failures=int(st[3]),
                           collision_rejections=int(st[4]), cc_performed=int(st[5]),
                           cc_possible=int(st[6]), wall_ms=wall, nodes_start=int(r.nodes_start),
-                          nodes_goal=int(r.nodes_goal), device_ms=float(r.device_ms))
+                          nodes_goal=int(r.nodes_goal), device_ms=float(r.device_ms),
+                          stage1_evals=int(st[8]), cc_fk_evals=int(st[9]), nn_nodes=int(st[10]),
+                          proj_iters=int(st[11]))
         if r.status == -1:
             if B == 1:
                 raise PlanSetupError(_SETUP.get(r.setup_code, "invalid start/goal"))

@@ -73,5 +73,5 @@ def test_device_source_is_one_translation_unit():
 
 def test_shared_struct_layout_matches_ctypes():
     from paper_2505_06791_b200 import _lib
-    assert C.sizeof(_lib.Result) == 4 * 5 + 4 + 8 + 8 * 8
+    assert C.sizeof(_lib.Result) == 4 * 5 + 4 + 8 + 8 * 12
     assert C.sizeof(_lib.Params) > 0

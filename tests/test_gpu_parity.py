@@ -192,8 +192,8 @@ def test_projection_contract(K, oracle):
         taus = k[f"proj_{key}_tausm"]
         r = K.project_batch(m, sp, wps, sp.tau_task, taus, 0.1, 1e-3, 128, mode)
         for i in range(len(wps)):
-            assert np.array_equal(r["xi"][i][0], wps[i][0])
-            if r["ok"][i]:
+            assert np.array_equal(r["xi"][i][0], wps[i][0].astype(np.float32))
+            if r["ok"][i] and mode != 1:   # literal-gap vouches only for the end (T/test_projection.py:285)
                 lo, hi = m.packed.lo, m.packed.hi
                 assert (r["xi"][i] >= lo).all() and (r["xi"][i] <= hi).all()
                 assert _fp64_projection_ok(oracle, m, sp, r["xi"][i], sp.tau_task, taus[i]), (key, i)
@@ -249,6 +249,6 @@ def test_check_config_codes(K):
     assert (K.check_config_batch(m, sc, sp, good) == 0).all()
     bad = good.copy()
     bad[0, 0] = 10.0
-    bad[1, 0] += 0.3            # leaves the plane
+    bad[1, 1] += 0.3            # shoulder lift: leaves the plane
     codes = K.check_config_batch(m, sc, sp, bad[:2])
     assert codes[0] == 1 and codes[1] == 2
