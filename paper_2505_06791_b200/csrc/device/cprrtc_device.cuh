@@ -327,7 +327,7 @@ __device__ __noinline__ float cp_err_norm(const Con<float>& c, const float* q) {
 // seg rows [0, W) live in shared memory; lane t owns row t.
 // trace (optional, parity only): after every iteration the buffer is copied
 // to trace[it-1] and the prefix to trace_prog[it-1].
-__device__ bool cp_project(const Team& tm, float (*seg)[CP_NP], int W, const Con<float>& c,
+__device__ __noinline__ bool cp_project(const Team& tm, float (*seg)[CP_NP], int W, const Con<float>& c,
                            const ProjArgs& pa, int* iters_out, int* prog_out,
                            float* trace = nullptr, int* trace_prog = nullptr,
                            unsigned long long* n_stage1 = nullptr) {
@@ -536,12 +536,14 @@ __device__ __forceinline__ bool cp_hit_sph(float cx, float cy, float cz, float r
 // self pairs), so a team vote after every CP_CHUNK rounds both implements the
 // early-exit flag and yields the reference's first detection exactly.
 // margin inflates every robot sphere (planner safety margin; 0 for parity).
-__device__ ValOut cp_validate(const Team& tm, const float (*seg)[CP_NP], int W, int t_first,
-                              bool flag_on, float margin, const SceneSm& sc) {
+// Out of line and with rolled sphere / pair loops: one compact copy of the
+// check loop keeps the planner's instruction footprint inside the I-cache.
+__device__ __noinline__ ValOut cp_validate(const Team& tm, const float (*seg)[CP_NP], int W, int t_first,
+                                           bool flag_on, float margin, const SceneSm& sc) {
     const int t = (int)tm.lane;
     const bool mine = t >= t_first && t < W;
     const int E = sc.nb + sc.ne;
-    float sx[CP_S > 0 ? CP_S : 1], sy[CP_S > 0 ? CP_S : 1], sz[CP_S > 0 ? CP_S : 1];
+    float4 sp[CP_S > 0 ? CP_S : 1];   // world sphere centres of my waypoint (local memory)
     {
         float q[CP_N];
 #pragma unroll
@@ -549,36 +551,36 @@ __device__ ValOut cp_validate(const Team& tm, const float (*seg)[CP_NP], int W, 
         float R[CP_N * 9], P[CP_N * 3], AX[CP_N * 3], OR[CP_N * 3], SPH[(CP_S > 0 ? CP_S : 1) * 3];
         cp_fk<float>(q, R, P, AX, OR, SPH);
 #pragma unroll
-        for (int s = 0; s < CP_S; s++) { sx[s] = SPH[3 * s]; sy[s] = SPH[3 * s + 1]; sz[s] = SPH[3 * s + 2]; }
+        for (int s = 0; s < CP_S; s++) sp[s] = make_float4(SPH[3 * s], SPH[3 * s + 1], SPH[3 * s + 2], 0.f);
     }
     int first_r = CP_INTMAX;
     i64 rounds_done = 0;
     bool stop = false;
-#pragma unroll
-    for (int s = 0; s < CP_S; s++) {
-        if (!stop) {
-            const float r = (float)cp_rad(s) + margin, r2 = r * r;
-            const float cx = sx[s], cy = sy[s], cz = sz[s];
-            const int rbase = s * E;
-            for (int p0 = 0; p0 < E; p0 += CP_CHUNK) {
-                const int p1 = min(p0 + CP_CHUNK, E);
-                for (int p = p0; p < p1; p++) {
-                    bool hit = p < sc.nb ? cp_hit_box(cx, cy, cz, r2, sc.box_c[p], sc.box_h[p])
-                                         : cp_hit_sph(cx, cy, cz, r, sc.sph[p - sc.nb]);
-                    if (mine && hit && first_r == CP_INTMAX) first_r = rbase + p;
-                }
-                rounds_done = rbase + p1;
-                if (flag_on && tm.any(first_r != CP_INTMAX)) { stop = true; break; }
+#pragma unroll 1
+    for (int s = 0; s < CP_S && !stop; s++) {
+        const float4 c = sp[s];
+        const float r = cp_rad_tab[s] + margin, r2 = r * r;
+        const int rbase = s * E;
+#pragma unroll 1
+        for (int p0 = 0; p0 < E; p0 += CP_CHUNK) {
+            const int p1 = min(p0 + CP_CHUNK, E);
+            for (int p = p0; p < p1; p++) {
+                bool hit = p < sc.nb ? cp_hit_box(c.x, c.y, c.z, r2, sc.box_c[p], sc.box_h[p])
+                                     : cp_hit_sph(c.x, c.y, c.z, r, sc.sph[p - sc.nb]);
+                if (mine && hit && first_r == CP_INTMAX) first_r = rbase + p;
             }
+            rounds_done = rbase + p1;
+            if (flag_on && tm.any(first_r != CP_INTMAX)) { stop = true; break; }
         }
     }
     if (!stop && CP_P > 0) {
         const int rbase = CP_S * E;
-#pragma unroll
+#pragma unroll 1
         for (int k = 0; k < CP_P; k++) {
-            const int a = cp_pair_a(k), b = cp_pair_b(k);
-            const float rr = (float)(cp_rad(a) + cp_rad(b)) + 2.f * margin;
-            float dx = sx[a] - sx[b], dy = sy[a] - sy[b], dz = sz[a] - sz[b];
+            const int a = cp_pair_tab[2 * k], b = cp_pair_tab[2 * k + 1];
+            const float rr = cp_rad_tab[a] + cp_rad_tab[b] + 2.f * margin;
+            const float4 pa = sp[a], pb = sp[b];
+            float dx = pa.x - pb.x, dy = pa.y - pb.y, dz = pa.z - pb.z;
             bool hit = fmaf(dx, dx, fmaf(dy, dy, dz * dz)) < rr * rr;
             if (mine && hit && first_r == CP_INTMAX) first_r = rbase + k;
         }
@@ -601,7 +603,7 @@ __device__ ValOut cp_validate(const Team& tm, const float (*seg)[CP_NP], int W, 
 // nodes: coordinate d of node i at nodes[d * cap + i]; never-written slots are
 // NaN and drop out of the comparison.  Ties go to the lowest index.
 // ---------------------------------------------------------------------------
-__device__ int cp_nearest(const Team& tm, const float* nodes, int cap, int count, const float* q) {
+__device__ __noinline__ int cp_nearest(const Team& tm, const float* nodes, int cap, int count, const float* q) {
     float qq[CP_N];
 #pragma unroll
     for (int k = 0; k < CP_N; k++) qq[k] = q[k];
@@ -745,7 +747,7 @@ __device__ __forceinline__ bool cp_check_motion(const Team& tm, TeamWS& ws, cons
 }
 
 // derive_edge (planner.py:223-245): the motion a->b re-derivable from its endpoints
-__device__ bool cp_derive_edge(const Team& tm, TeamWS& ws, const PlanArgs& A, const SceneSm& sc,
+__device__ __noinline__ bool cp_derive_edge(const Team& tm, TeamWS& ws, const PlanArgs& A, const SceneSm& sc,
                                const float* a, const float* b, Stats& st) {
     cp_interp(tm, ws.seg, A.W, a, b);
     int it, pr;
@@ -786,7 +788,7 @@ __device__ __forceinline__ void cp_load_node(const Team& tm, const PlanArgs& A, 
 
 // connect (planner.py:361-409): greedy walk of tree k toward ws.qt.
 // Returns the meet node index if Reached, else -1.
-__device__ int cp_connect(const Team& tm, TeamWS& ws, const PlanArgs& A, const SceneSm& sc,
+__device__ __noinline__ int cp_connect(const Team& tm, TeamWS& ws, const PlanArgs& A, const SceneSm& sc,
                           QueryState& Q, int qi, int k, Stats& st) {
     const int cnt = cp_count(A, Q, k);
     st.v[ST_NNODES] += cnt;

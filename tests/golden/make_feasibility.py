@@ -1,6 +1,6 @@
 """Which upright pairs does the reference (C oracle port) solve with a long budget?"""
 import sys, os, json
-ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+ROOT = os.path.dirname(os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 sys.path[:0] = [ROOT, os.path.join(ROOT, "tests")]
 from concurrent.futures import ProcessPoolExecutor
 
@@ -20,6 +20,6 @@ def job(k):
 if __name__ == "__main__":
     with ProcessPoolExecutor(8) as ex:
         res = list(ex.map(job, range(100)))
-    json.dump(res, open(os.path.join(ROOT, "build", "feasibility.json"), "w"))
+    json.dump({"generated_by": "tests/golden/make_feasibility.py (C oracle, 3 seeds x 20 s)", "upright_solved_by_reference": [bool(r[1]) for r in res], "reference_wall_ms": [r[2] for r in res]}, open(os.path.join(ROOT, "tests", "golden", "upright_feasibility.json"), "w"))
     print(sum(r[1] for r in res), "solved of", len(res))
     print([r[0] for r in res if not r[1]])

@@ -67,15 +67,17 @@ def test_plan_upright_constrained(oracle):
     from paper_2505_06791_b200.planner import PlanParams, PlanProblem, plan
     m, sc, sp = fx.robot("arm7"), fx.scene("table"), fx.spec("upright")
     prs = fx.pairs()
+    feas = np.nonzero(fx.upright_feasible())[0][:12]
     solved = 0
-    for i in range(8):
+    for i in feas:
         prob = PlanProblem(m, sc, sp, prs["upright_start"][i], prs["upright_goal"][i],
-                           PlanParams(width=16, max_iterations=4000, seed_offset=i * 10_000))
+                           PlanParams(width=16, max_iterations=200_000, time_budget_ms=3000.0,
+                                      seed_offset=int(i) * 10_000))
         res = plan(prob)
         if res.solved:
             solved += 1
             _check_path(oracle, prob, res)
-    assert solved >= 7
+    assert solved == len(feas)
 
 
 def test_plan_batch(oracle):
