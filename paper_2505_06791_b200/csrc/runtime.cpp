@@ -1061,34 +1061,37 @@ int cprrtc_plan(void* p, const cprrtc_params* prm, int B, const double* starts, 
     }
     // 3) the persistent planner
     PlanArgs A = make_plan_args(c, prm, B, cap, tau);
-    const size_t smem = team_smem(c, m, true);
     if (!m->plan_occ) {
         int occ = 0;
-        drv().occupancy(&occ, m->fn["cp_plan_kernel"], kThreads, smem);
+        drv().occupancy(&occ, m->fn["cp_plan_kernel"], kThreads, team_smem(c, m, true));
         m->plan_occ = occ > 0 ? occ : 1;
     }
-    const int tpc = kThreads / m->G;
-    int grid = m->plan_occ * c->sms;
-    // concurrency: the requested team count, else every resident team -- but
-    // never more than a quarter of the sample budget, so that at least ~4
-    // waves of extensions build on each other (samples are the reference's
-    // iterations: a first wave that consumed them all would only grow stars
-    // around the roots)
-    // single query: 512 teams minimise latency (r1 sweep: 256/512/1024/2368 teams ->
-    // 0.91/0.95/1.04/1.25 ms median, upright Panda); batches: every resident team
-    long long want_teams = prm->teams > 0 ? prm->teams : (B == 1 ? 512 : (long long)grid * tpc);
+    const int tpw = 32 / m->G;                    // teams per warp
+    const int max_tpc = kThreads / m->G;          // teams per full CTA
+    const int resident = m->plan_occ * c->sms * max_tpc;
+    // concurrency: the requested team count, else (single query) 512 teams --
+    // r1 sweep on upright Panda: 256/512/1024/2368 teams -> 0.91/0.95/1.04/1.25 ms
+    // median -- or (batches) every resident team; never more than a quarter of the
+    // sample budget so that at least ~4 waves of extensions build on each other
+    // (samples are the reference's iterations)
+    long long want_teams = prm->teams > 0 ? prm->teams : (B == 1 ? 512 : (long long)resident);
     long long budget_teams = (long long)B * prm->max_iterations / 4;
-    if (budget_teams < tpc) budget_teams = tpc;
+    if (budget_teams < tpw) budget_teams = tpw;
     if (want_teams > budget_teams) want_teams = budget_teams;
-    {
-        long long g = (want_teams + tpc - 1) / tpc;
-        if (g < grid) grid = (int)g;
-    }
+    if (want_teams > resident) want_teams = resident;
+    // spread the teams over every SM first (latency of a team is set by how
+    // many warps share its SM), then fill CTAs up to 256 threads
+    long long per_cta = (want_teams + c->sms - 1) / c->sms;
+    per_cta = (per_cta + tpw - 1) / tpw * tpw;
+    if (per_cta > max_tpc) per_cta = max_tpc;
+    const int block = (int)(per_cta * m->G);
+    int grid = (int)((want_teams + per_cta - 1) / per_cta);
     if (grid < 1) grid = 1;
+    const size_t smem = (size_t)(2 * c->nb + c->ne) * sizeof(float4) + (size_t)per_cta * m->ws_bytes;
     CUDA_TRY(cudaEventRecord(c->ev[1], c->stream));
     {
         void* args[] = {&A};
-        if (int rc = launch(c, m, "cp_plan_kernel", grid, 1, kThreads, smem, args)) return rc;
+        if (int rc = launch(c, m, "cp_plan_kernel", grid, 1, block, smem, args)) return rc;
     }
     CUDA_TRY(cudaEventRecord(c->ev[2], c->stream));
     // 4) path extraction into mapped host memory

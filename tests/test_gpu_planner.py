@@ -31,7 +31,8 @@ def _check_path(oracle, prob, res):
         a, b = res.path[e], res.path[e + 1]
         gap0 = np.linalg.norm(b - a) / (W - 1)
         for t, q in enumerate(seg):
-            assert (q >= m.packed.lo).all() and (q <= m.packed.hi).all()
+            # FP32 storage of an in-limit FP64 endpoint may sit one ulp outside
+            assert (q >= m.packed.lo - 4e-7).all() and (q <= m.packed.hi + 4e-7).all()
             if sp is not None and prob.params.projection_mode != "literal-gap":
                 # literal-gap vouches for the last waypoint only (reference
                 # T/test_projection.py:285-301); its interior may leave tau
