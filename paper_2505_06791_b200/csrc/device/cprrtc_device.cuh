@@ -265,8 +265,12 @@ __device__ __forceinline__ bool cp_damped(const T (*J)[CP_N], const T* e, T lam,
     return true;
 }
 
-// One out-of-line FP32 copy of (e, J): shared by stage 1, the sequential
-// projector and the parity kernels (keeps the NVRTC module small).
+// The FP32 constraint of the module's current call lives in constant memory
+// (written by the runtime before each launch that projects), so the hot loops
+// address it as constant-bank operands instead of through a pointer.
+__constant__ Con<float> cp_conf;
+
+// One out-of-line FP32 copy of (e, J) for the cold sequential projector.
 __device__ __noinline__ void cp_err_jac_f(const Con<float>& c, const float* q, float* e, float (*J)[CP_N]) {
     float qq[CP_N];
 #pragma unroll
@@ -280,7 +284,7 @@ __device__ __noinline__ void cp_err_jac_f(const Con<float>& c, const float* q, f
 
 // stage 1 of Alg. 1 for one waypoint (pure.py:511-546).  Validity is judged
 // at the pre-update waypoint with the device margins.
-__device__ __forceinline__ bool cp_stage1(const Con<float>& c, const ProjArgs& pa, const float* xt,
+__device__ __forceinline__ bool cp_stage1(const ProjArgs& pa, const float* xt,
                                           const float* xp, float tau_sm, float* xn) {
     bool fin = true;
 #pragma unroll
@@ -291,7 +295,7 @@ __device__ __forceinline__ bool cp_stage1(const Con<float>& c, const ProjArgs& p
         return false;
     }
     float e[CP_M], J[CP_M][CP_N], g[CP_N];
-    cp_err_jac_f(c, xt, e, J);
+    cp_err_jac<float>(cp_conf, xt, e, J);
     float en2 = 0.f;
 #pragma unroll
     for (int i = 0; i < CP_M; i++) en2 += e[i] * e[i];
@@ -309,12 +313,12 @@ __device__ __forceinline__ bool cp_stage1(const Con<float>& c, const ProjArgs& p
     return gap < tau_sm * 0.99999f && sqrtf(en2) < pa.tau_task_dev;
 }
 
-__device__ __noinline__ float cp_err_norm(const Con<float>& c, const float* q) {
+__device__ __noinline__ float cp_err_norm(const float* q) {
     float R[CP_N * 9], P[CP_N * 3], AX[CP_N * 3], OR[CP_N * 3], SPH[(CP_S > 0 ? CP_S : 1) * 3];
     cp_fk<float>(q, R, P, AX, OR, SPH);
     float qe[4], e[CP_M];
     cp_quat<float>(R + 9 * CP_EE, qe);
-    cp_task_err<float>(c, P + 3 * CP_EE, qe, e);
+    cp_task_err<float>(cp_conf, P + 3 * CP_EE, qe, e);
     float s = 0.f;
 #pragma unroll
     for (int i = 0; i < CP_M; i++) s += e[i] * e[i];
@@ -327,8 +331,8 @@ __device__ __noinline__ float cp_err_norm(const Con<float>& c, const float* q) {
 // seg rows [0, W) live in shared memory; lane t owns row t.
 // trace (optional, parity only): after every iteration the buffer is copied
 // to trace[it-1] and the prefix to trace_prog[it-1].
-__device__ __noinline__ bool cp_project(const Team& tm, float (*seg)[CP_NP], int W, const Con<float>& c,
-                           const ProjArgs& pa, int* iters_out, int* prog_out,
+__device__ __noinline__ bool cp_project(const Team tm, float (*seg)[CP_NP], int W,
+                           const ProjArgs pa, int* iters_out, int* prog_out,
                            float* trace = nullptr, int* trace_prog = nullptr,
                            unsigned long long* n_stage1 = nullptr) {
     unsigned long long s1 = 0;
@@ -366,7 +370,7 @@ __device__ __noinline__ bool cp_project(const Team& tm, float (*seg)[CP_NP], int
                     for (int k = 0; k < CP_N; k++) fin &= cp_finite(q[k]);
                     if (!fin) { res = 0; break; }
                     float e[CP_M], J[CP_M][CP_N], st[CP_N], en2 = 0.f;
-                    cp_err_jac_f(c, q, e, J);
+                    cp_err_jac_f(cp_conf, q, e, J);
 #pragma unroll
                     for (int i = 0; i < CP_M; i++) en2 += e[i] * e[i];
                     if (sqrtf(en2) < pa.tau_task_dev) break;
@@ -417,7 +421,7 @@ __device__ __noinline__ bool cp_project(const Team& tm, float (*seg)[CP_NP], int
                 }
                 if (!tm.any(!cheap)) { valid = act; full_step = false; }
             }
-            if (full_step && act) valid = cp_stage1(c, pa, xt, xp, tau_sm, xn);
+            if (full_step && act) valid = cp_stage1(pa, xt, xp, tau_sm, xn);
             if (n_stage1 && full_step) s1 += __popc(tm.ballot(act));
             unsigned vm = tm.ballot(act && valid) & full;
             int np = prog;
@@ -481,7 +485,7 @@ __device__ __noinline__ bool cp_project(const Team& tm, float (*seg)[CP_NP], int
             }
             tm.sync();
             if (row) {
-                good = cp_err_norm(c, qc) < pa.tau_task_dev;
+                good = cp_err_norm(qc) < pa.tau_task_dev;
                 if (t >= 1) {
                     float s2 = 0.f;
 #pragma unroll
@@ -538,8 +542,8 @@ __device__ __forceinline__ bool cp_hit_sph(float cx, float cy, float cz, float r
 // margin inflates every robot sphere (planner safety margin; 0 for parity).
 // Out of line and with rolled sphere / pair loops: one compact copy of the
 // check loop keeps the planner's instruction footprint inside the I-cache.
-__device__ __noinline__ ValOut cp_validate(const Team& tm, const float (*seg)[CP_NP], int W, int t_first,
-                                           bool flag_on, float margin, const SceneSm& sc) {
+__device__ __noinline__ ValOut cp_validate(const Team tm, const float (*seg)[CP_NP], int W, int t_first,
+                                           bool flag_on, float margin, const SceneSm sc) {
     const int t = (int)tm.lane;
     const bool mine = t >= t_first && t < W;
     const int E = sc.nb + sc.ne;
@@ -561,17 +565,35 @@ __device__ __noinline__ ValOut cp_validate(const Team& tm, const float (*seg)[CP
         const float4 c = sp[s];
         const float r = cp_rad_tab[s] + margin, r2 = r * r;
         const int rbase = s * E;
+        // boxes, then obstacle spheres (reference order, pure.py:674-693), in
+        // chunks of CP_CHUNK checks: hits of a chunk collect in a bitmask and
+        // the team votes once per chunk (the early-exit flag)
 #pragma unroll 1
-        for (int p0 = 0; p0 < E; p0 += CP_CHUNK) {
-            const int p1 = min(p0 + CP_CHUNK, E);
-            for (int p = p0; p < p1; p++) {
-                bool hit = p < sc.nb ? cp_hit_box(c.x, c.y, c.z, r2, sc.box_c[p], sc.box_h[p])
-                                     : cp_hit_sph(c.x, c.y, c.z, r, sc.sph[p - sc.nb]);
-                if (mine && hit && first_r == CP_INTMAX) first_r = rbase + p;
+        for (int p0 = 0; p0 < sc.nb; p0 += CP_CHUNK) {
+            unsigned hm = 0u;
+#pragma unroll
+            for (int j = 0; j < CP_CHUNK; j++) {
+                const int p = p0 + j;
+                if (p < sc.nb) hm |= (unsigned)cp_hit_box(c.x, c.y, c.z, r2, sc.box_c[p], sc.box_h[p]) << j;
             }
-            rounds_done = rbase + p1;
+            if (mine && hm && first_r == CP_INTMAX) first_r = rbase + p0 + __ffs(hm) - 1;
+            rounds_done = rbase + min(p0 + CP_CHUNK, sc.nb);
             if (flag_on && tm.any(first_r != CP_INTMAX)) { stop = true; break; }
         }
+        if (stop) break;
+#pragma unroll 1
+        for (int p0 = 0; p0 < sc.ne; p0 += CP_CHUNK) {
+            unsigned hm = 0u;
+#pragma unroll
+            for (int j = 0; j < CP_CHUNK; j++) {
+                const int p = p0 + j;
+                if (p < sc.ne) hm |= (unsigned)cp_hit_sph(c.x, c.y, c.z, r, sc.sph[p]) << j;
+            }
+            if (mine && hm && first_r == CP_INTMAX) first_r = rbase + sc.nb + p0 + __ffs(hm) - 1;
+            rounds_done = rbase + sc.nb + min(p0 + CP_CHUNK, sc.ne);
+            if (flag_on && tm.any(first_r != CP_INTMAX)) { stop = true; break; }
+        }
+        if (!stop) rounds_done = rbase + E;
     }
     if (!stop && CP_P > 0) {
         const int rbase = CP_S * E;
@@ -603,13 +625,14 @@ __device__ __noinline__ ValOut cp_validate(const Team& tm, const float (*seg)[CP
 // nodes: coordinate d of node i at nodes[d * cap + i]; never-written slots are
 // NaN and drop out of the comparison.  Ties go to the lowest index.
 // ---------------------------------------------------------------------------
-__device__ __noinline__ int cp_nearest(const Team& tm, const float* nodes, int cap, int count, const float* q) {
+__device__ __noinline__ int cp_nearest(const Team tm, const float* nodes, int cap, int count, const float* q) {
     float qq[CP_N];
 #pragma unroll
     for (int k = 0; k < CP_N; k++) qq[k] = q[k];
     float best = cp_inf();
     int bi = CP_INTMAX;
     const int n4 = (count + 3) >> 2;
+#pragma unroll 4
     for (int i4 = (int)tm.lane; i4 < n4; i4 += CP_G) {
         float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
 #pragma unroll
@@ -751,7 +774,7 @@ __device__ __noinline__ bool cp_derive_edge(const Team& tm, TeamWS& ws, const Pl
                                const float* a, const float* b, Stats& st) {
     cp_interp(tm, ws.seg, A.W, a, b);
     int it, pr;
-    bool okp = cp_project(tm, ws.seg, A.W, A.con, A.pa, &it, &pr, nullptr, nullptr, &st.v[ST_STAGE1]);
+    bool okp = cp_project(tm, ws.seg, A.W, A.pa, &it, &pr, nullptr, nullptr, &st.v[ST_STAGE1]);
     st.v[ST_PROJITER] += it;
     if (!okp) {
         st.v[ST_PFAIL]++;
@@ -801,7 +824,7 @@ __device__ __noinline__ int cp_connect(const Team& tm, TeamWS& ws, const PlanArg
         cp_steer(tm, ws.qc, ws.qt, A.step, ws.qs);
         cp_interp(tm, ws.seg, A.W, ws.qc, ws.qs);
         int it, pr;
-        bool okp = cp_project(tm, ws.seg, A.W, A.con, A.pa, &it, &pr, nullptr, nullptr, &st.v[ST_STAGE1]);
+        bool okp = cp_project(tm, ws.seg, A.W, A.pa, &it, &pr, nullptr, nullptr, &st.v[ST_STAGE1]);
         st.v[ST_PROJITER] += it;
         if (!okp) { st.v[ST_PFAIL]++; return -1; }
         cp_copy(tm, ws.qe, ws.seg[A.W - 1]);
@@ -853,7 +876,7 @@ __device__ void cp_plan_query(const Team& tm, TeamWS& ws, const PlanArgs& A, con
         if (cp_vec_equal(tm, ws.qs, ws.qn)) continue;              // degenerate
         cp_interp(tm, ws.seg, W, ws.qn, ws.qs);
         int pit, ppr;
-        bool okp = cp_project(tm, ws.seg, W, A.con, A.pa, &pit, &ppr, nullptr, nullptr, &st.v[ST_STAGE1]);
+        bool okp = cp_project(tm, ws.seg, W, A.pa, &pit, &ppr, nullptr, nullptr, &st.v[ST_STAGE1]);
         st.v[ST_PROJITER] += pit;
         if (!okp) { st.v[ST_PFAIL]++; continue; }
         cp_copy(tm, ws.qe, ws.seg[W - 1]);
@@ -1279,7 +1302,7 @@ cp_project_kernel(int B, int W, Con<float> con, ProjArgs pa, const float* tau_sm
         ProjArgs p = pa;
         if (tau_sm) p.tau_sm_fixed = tau_sm[i];
         int it, pr;
-        bool good = cp_project(tm, ws.seg, W, con, p, &it, &pr,
+        bool good = cp_project(tm, ws.seg, W, p, &it, &pr,
                                trace ? trace + (size_t)i * pa.max_iters * W * CP_N : nullptr,
                                trace ? trace_prog + (size_t)i * pa.max_iters : nullptr);
         tm.sync();

@@ -75,6 +75,7 @@ struct Driver {
     CUresult (*funcSetAttribute)(CUfunction, CUfunction_attribute, int) = nullptr;
     CUresult (*occupancy)(int*, CUfunction, int, size_t) = nullptr;
     CUresult (*getErrorString)(CUresult, const char**) = nullptr;
+    CUresult (*moduleGetGlobal)(CUdeviceptr*, size_t*, CUmodule, const char*) = nullptr;
     bool ok = false;
 };
 
@@ -95,7 +96,7 @@ Driver& drv() {
                entry("cuModuleGetFunction", d.moduleGetFunction) && entry("cuLaunchKernel", d.launchKernel) &&
                entry("cuFuncSetAttribute", d.funcSetAttribute) &&
                entry("cuOccupancyMaxActiveBlocksPerMultiprocessor", d.occupancy) &&
-               entry("cuGetErrorString", d.getErrorString);
+               entry("cuGetErrorString", d.getErrorString) && entry("cuModuleGetGlobal", d.moduleGetGlobal);
     });
     return d;
 }
@@ -279,6 +280,9 @@ struct Module {
     std::map<std::string, CUfunction> fn;
     int plan_occ = 0;      // resident plan CTAs per SM
     std::string cubin_path;
+    CUdeviceptr conf_ptr = 0;   // __constant__ Con<float> cp_conf
+    Con<float> conf_now{};
+    bool conf_valid = false;
 };
 
 struct Ctx {
@@ -361,6 +365,12 @@ int get_module(Ctx* c, int G, int kind, int orient, int parity, Module** out) {
         if (r != CUDA_SUCCESS) return fail(CPRRTC_ECUDA, std::string("cuModuleGetFunction ") + k + ": " + cu_err(r));
         m->fn[k] = f;
     }
+    {
+        size_t sz = 0;
+        r = drv().moduleGetGlobal(&m->conf_ptr, &sz, m->mod, "cp_conf");
+        if (r != CUDA_SUCCESS || sz != sizeof(Con<float>))
+            return fail(CPRRTC_ECUDA, "cp_conf symbol missing or mis-sized: " + cu_err(r));
+    }
     m->G = G;
     m->kind = kind;
     m->orient = orient;
@@ -375,6 +385,17 @@ int get_module(Ctx* c, int G, int kind, int orient, int parity, Module** out) {
 int cur_module(Ctx* c, int W, int parity, Module** m) {
     if (W < 2 || W > 32) return fail(CPRRTC_ELIMIT, "width must be in [2, 32] for this build");
     return get_module(c, W <= 16 ? 16 : 32, c->kind, c->orient, parity, m);
+}
+
+// make the module's constant-memory constraint equal to the context's
+int upload_conf(Ctx* c, Module* m) {
+    if (m->conf_valid && std::memcmp(&m->conf_now, &c->conf, sizeof(Con<float>)) == 0) return 0;
+    CUDA_TRY(cudaMemcpyAsync(reinterpret_cast<void*>(m->conf_ptr), &c->conf, sizeof(Con<float>),
+                             cudaMemcpyHostToDevice, c->stream));
+    CUDA_TRY(cudaStreamSynchronize(c->stream));   // the source is a context member
+    m->conf_now = c->conf;
+    m->conf_valid = true;
+    return 0;
 }
 
 int launch(Ctx* c, Module* m, const char* k, unsigned gx, unsigned gy, unsigned bx, size_t smem, void** args) {
@@ -857,6 +878,7 @@ int cprrtc_project(void* p, int B, int W, const double* wps, const double* tau_s
     const int tpc = kThreads / m->G;
     int grid = (B + tpc - 1) / tpc;
     if (grid > 64 * c->sms) grid = 64 * c->sms;
+    if (int rc2 = upload_conf(c, m)) return rc2;
     if (int rc2 = launch(c, m, "cp_project_kernel", grid, 1, kThreads, team_smem(c, m, false), args)) return rc2;
     download(c, xi, c->scratch[1], nw);
     std::vector<int> tmp((size_t)3 * B);
@@ -1088,6 +1110,7 @@ int cprrtc_plan(void* p, const cprrtc_params* prm, int B, const double* starts, 
     int grid = (int)((want_teams + per_cta - 1) / per_cta);
     if (grid < 1) grid = 1;
     const size_t smem = (size_t)(2 * c->nb + c->ne) * sizeof(float4) + (size_t)per_cta * m->ws_bytes;
+    if (int rc = upload_conf(c, m)) return rc;
     CUDA_TRY(cudaEventRecord(c->ev[1], c->stream));
     {
         void* args[] = {&A};
@@ -1166,6 +1189,7 @@ int cprrtc_derive_edges(void* p, const cprrtc_params* prm, int n_nodes, const do
     int* dok = c->dense_ok.as<int>();
     void* args[] = {(void*)&E, &A, &dn, &ds, &dd, &dok};
     const int tpc = kThreads / m->G;
+    if (int rc2 = upload_conf(c, m)) return rc2;
     if (int rc2 = launch(c, m, "cp_dense_kernel", (E + tpc - 1) / tpc, 1, kThreads, team_smem(c, m, true), args))
         return rc2;
     std::vector<float> tmp((size_t)E * W * n);
