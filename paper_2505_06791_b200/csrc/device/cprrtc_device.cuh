@@ -524,6 +524,15 @@ struct ValOut {
     int fk_evals;          // waypoint FK evaluations
 };
 
+// explicit shared-space 128-bit load (the staged scene is only known to the
+// compiler as a generic pointer, which would otherwise become LD.E.128)
+__device__ __forceinline__ float4 cp_lds4(const float4* p) {
+    float4 v;
+    const unsigned a = (unsigned)__cvta_generic_to_shared(p);
+    asm("ld.shared.v4.f32 {%0,%1,%2,%3}, [%4];" : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "r"(a));
+    return v;
+}
+
 __device__ __forceinline__ bool cp_hit_box(float cx, float cy, float cz, float r2, float4 c, float4 h) {
     float dx = fmaxf(fabsf(cx - c.x) - h.x, 0.f);
     float dy = fmaxf(fabsf(cy - c.y) - h.y, 0.f);
@@ -570,26 +579,26 @@ __device__ __noinline__ ValOut cp_validate(const Team tm, const float (*seg)[CP_
         // the team votes once per chunk (the early-exit flag)
 #pragma unroll 1
         for (int p0 = 0; p0 < sc.nb; p0 += CP_CHUNK) {
-            unsigned hm = 0u;
+            bool any = false;
 #pragma unroll
-            for (int j = 0; j < CP_CHUNK; j++) {
-                const int p = p0 + j;
-                if (p < sc.nb) hm |= (unsigned)cp_hit_box(c.x, c.y, c.z, r2, sc.box_c[p], sc.box_h[p]) << j;
+            for (int j = 0; j < CP_CHUNK; j++) any |= cp_hit_box(c.x, c.y, c.z, r2, cp_lds4(sc.box_c + p0 + j), cp_lds4(sc.box_h + p0 + j));
+            if (mine && any && first_r == CP_INTMAX) {       // rare: locate the first hit of the chunk
+                for (int j = 0; j < CP_CHUNK; j++)
+                    if (cp_hit_box(c.x, c.y, c.z, r2, sc.box_c[p0 + j], sc.box_h[p0 + j])) { first_r = rbase + p0 + j; break; }
             }
-            if (mine && hm && first_r == CP_INTMAX) first_r = rbase + p0 + __ffs(hm) - 1;
             rounds_done = rbase + min(p0 + CP_CHUNK, sc.nb);
             if (flag_on && tm.any(first_r != CP_INTMAX)) { stop = true; break; }
         }
         if (stop) break;
 #pragma unroll 1
         for (int p0 = 0; p0 < sc.ne; p0 += CP_CHUNK) {
-            unsigned hm = 0u;
+            bool any = false;
 #pragma unroll
-            for (int j = 0; j < CP_CHUNK; j++) {
-                const int p = p0 + j;
-                if (p < sc.ne) hm |= (unsigned)cp_hit_sph(c.x, c.y, c.z, r, sc.sph[p]) << j;
+            for (int j = 0; j < CP_CHUNK; j++) any |= cp_hit_sph(c.x, c.y, c.z, r, cp_lds4(sc.sph + p0 + j));
+            if (mine && any && first_r == CP_INTMAX) {
+                for (int j = 0; j < CP_CHUNK; j++)
+                    if (cp_hit_sph(c.x, c.y, c.z, r, sc.sph[p0 + j])) { first_r = rbase + sc.nb + p0 + j; break; }
             }
-            if (mine && hm && first_r == CP_INTMAX) first_r = rbase + sc.nb + p0 + __ffs(hm) - 1;
             rounds_done = rbase + sc.nb + min(p0 + CP_CHUNK, sc.ne);
             if (flag_on && tm.any(first_r != CP_INTMAX)) { stop = true; break; }
         }
@@ -921,12 +930,23 @@ __device__ void cp_plan_query(const Team& tm, TeamWS& ws, const PlanArgs& A, con
     }
 }
 
+__host__ __device__ __forceinline__ int cp_pad8(int x) { return (x + CP_CHUNK - 1) / CP_CHUNK * CP_CHUNK; }
+__device__ __forceinline__ int cp_scene_f4(const SceneSm& g) { return 2 * cp_pad8(g.nb) + cp_pad8(g.ne); }
+
+// Stage the scene into shared memory, padded to whole CP_CHUNKs with
+// primitives 1e18 m away (never hit), so the check loop has no bounds test.
 __device__ __forceinline__ SceneSm cp_stage_scene(const SceneSm& g, float4* sm) {
+    const int nbp = cp_pad8(g.nb), nep = cp_pad8(g.ne);
     float4* bc = sm;
-    float4* bh = sm + g.nb;
-    float4* sp = sm + 2 * g.nb;
-    for (int i = threadIdx.x; i < g.nb; i += blockDim.x) { bc[i] = g.box_c[i]; bh[i] = g.box_h[i]; }
-    for (int i = threadIdx.x; i < g.ne; i += blockDim.x) sp[i] = g.sph[i];
+    float4* bh = sm + nbp;
+    float4* sp = sm + 2 * nbp;
+    const float4 far = make_float4(1e18f, 1e18f, 1e18f, 0.f);
+    const float4 zero = make_float4(0.f, 0.f, 0.f, 0.f);
+    for (int i = threadIdx.x; i < nbp; i += blockDim.x) {
+        bc[i] = i < g.nb ? g.box_c[i] : far;
+        bh[i] = i < g.nb ? g.box_h[i] : zero;
+    }
+    for (int i = threadIdx.x; i < nep; i += blockDim.x) sp[i] = i < g.ne ? g.sph[i] : far;
     __syncthreads();
     SceneSm s;
     s.box_c = bc; s.box_h = bh; s.sph = sp; s.nb = g.nb; s.ne = g.ne;
@@ -939,7 +959,9 @@ extern "C" __global__ void __launch_bounds__(CP_NTHREADS, 1)
 cp_plan_kernel(const __grid_constant__ PlanArgs A) {
     extern __shared__ float4 cp_smem[];
     SceneSm sc = cp_stage_scene(A.scene_g, cp_smem);
-    TeamWS* wsa = reinterpret_cast<TeamWS*>(cp_smem + 2 * A.scene_g.nb + A.scene_g.ne);
+    TeamWS* wsa = reinterpret_cast<TeamWS*>(cp_smem + cp_scene_f4(A.scene_g));
+    // latency mode: one team per warp, so divergent teams never share a warp
+    if (A.solo && (int)(threadIdx.x & 31) >= CP_G) return;
     Team tm;
     const int team_in_cta = (threadIdx.x >> 5) * (32 / CP_G) + (threadIdx.x & 31) / CP_G;
     TeamWS& ws = wsa[team_in_cta];
@@ -1264,7 +1286,7 @@ cp_validate_kernel(int B, int W, int flag_on, float margin, SceneSm scg, const d
                    int* first_bad, i64* performed, i64* gpu_checks) {
     extern __shared__ float4 cp_smem[];
     SceneSm sc = cp_stage_scene(scg, cp_smem);
-    TeamWS* wsa = reinterpret_cast<TeamWS*>(cp_smem + 2 * scg.nb + scg.ne);
+    TeamWS* wsa = reinterpret_cast<TeamWS*>(cp_smem + cp_scene_f4(scg));
     Team tm;
     const int tpc = CP_NTHREADS / CP_G;
     const int team_in_cta = (threadIdx.x >> 5) * (32 / CP_G) + (threadIdx.x & 31) / CP_G;
@@ -1348,7 +1370,7 @@ cp_dense_kernel(int E, const __grid_constant__ PlanArgs A, const float* nodes, c
                 int* ok) {
     extern __shared__ float4 cp_smem[];
     SceneSm sc = cp_stage_scene(A.scene_g, cp_smem);
-    TeamWS* wsa = reinterpret_cast<TeamWS*>(cp_smem + 2 * A.scene_g.nb + A.scene_g.ne);
+    TeamWS* wsa = reinterpret_cast<TeamWS*>(cp_smem + cp_scene_f4(A.scene_g));
     Team tm;
     const int tpc = CP_NTHREADS / CP_G;
     const int team_in_cta = (threadIdx.x >> 5) * (32 / CP_G) + (threadIdx.x & 31) / CP_G;

@@ -69,6 +69,8 @@ struct PlanArgs {
     int flag_on;
     int max_iterations, max_connect;
     i64 budget_ns;         // <= 0: no time budget (deterministic)
+    int solo;              // 1: one team per warp (the other half-warp idles) -- latency mode
+    int pad_;
 };
 
 struct SetupArgs {

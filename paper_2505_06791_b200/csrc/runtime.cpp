@@ -185,8 +185,11 @@ int nvrtc_cubin(const std::string& src, const std::string& name, std::vector<cha
     if (!nv.ok) return fail(CPRRTC_ENVRTC, nv.why);
     int maj = 0, min = 0;
     nv.version(&maj, &min);
+    // FP32 division / sqrt approximate (2 ulp) and denormals flushed: the FP32
+    // planner has explicit tolerance margins; FP64 code is unaffected
     std::vector<const char*> opts = {kArch, "-std=c++17", "-lineinfo", "-default-device", "--dopt=on",
-                                     "--extra-device-vectorization"};
+                                     "--extra-device-vectorization", "-ftz=true", "-prec-div=false",
+                                     "-prec-sqrt=false"};
     std::string key = src + "|" + std::to_string(maj) + "." + std::to_string(min);
     for (auto o : opts) key += std::string("|") + o;
     char hex[32];
@@ -431,8 +434,12 @@ SceneSm scene_args(Ctx* c) {
     return s;
 }
 
+int pad8(int x) { return (x + 7) / 8 * 8; }
+
+size_t scene_smem(Ctx* c) { return (size_t)(2 * pad8(c->nb) + pad8(c->ne)) * sizeof(float4); }
+
 size_t team_smem(Ctx* c, Module* m, bool with_scene) {
-    size_t sc = with_scene ? (size_t)(2 * c->nb + c->ne) * sizeof(float4) : 0;
+    size_t sc = with_scene ? scene_smem(c) : 0;
     return sc + (size_t)(kThreads / m->G) * m->ws_bytes;
 }
 
@@ -1088,8 +1095,10 @@ int cprrtc_plan(void* p, const cprrtc_params* prm, int B, const double* starts, 
         drv().occupancy(&occ, m->fn["cp_plan_kernel"], kThreads, team_smem(c, m, true));
         m->plan_occ = occ > 0 ? occ : 1;
     }
-    const int tpw = 32 / m->G;                    // teams per warp
-    const int max_tpc = kThreads / m->G;          // teams per full CTA
+    // single queries run one team per warp (latency); batches pack two (G=16)
+    const bool solo = B == 1 && m->G == 16 && !(prm->teams < 0);
+    const int tpw = solo ? 1 : 32 / m->G;         // teams per warp
+    const int max_tpc = solo ? kThreads / 32 : kThreads / m->G;   // teams per full CTA
     const int resident = m->plan_occ * c->sms * max_tpc;
     // concurrency: the requested team count, else (single query) 512 teams --
     // r1 sweep on upright Panda: 256/512/1024/2368 teams -> 0.91/0.95/1.04/1.25 ms
@@ -1106,10 +1115,11 @@ int cprrtc_plan(void* p, const cprrtc_params* prm, int B, const double* starts, 
     long long per_cta = (want_teams + c->sms - 1) / c->sms;
     per_cta = (per_cta + tpw - 1) / tpw * tpw;
     if (per_cta > max_tpc) per_cta = max_tpc;
-    const int block = (int)(per_cta * m->G);
+    const int block = (int)(per_cta * 32 / tpw);
     int grid = (int)((want_teams + per_cta - 1) / per_cta);
     if (grid < 1) grid = 1;
-    const size_t smem = (size_t)(2 * c->nb + c->ne) * sizeof(float4) + (size_t)per_cta * m->ws_bytes;
+    const size_t smem = scene_smem(c) + (size_t)(block / m->G) * m->ws_bytes;
+    A.solo = solo ? 1 : 0;
     if (int rc = upload_conf(c, m)) return rc;
     CUDA_TRY(cudaEventRecord(c->ev[1], c->stream));
     {
