@@ -1055,17 +1055,31 @@ __device__ int cp_check_config_d(const SetupArgs& S, const double* q, int lane) 
 }
 
 #if !CP_PARITY
-extern "C" __global__ void __launch_bounds__(64) cp_setup_kernel(const __grid_constant__ SetupArgs S) {
+extern "C" __global__ void __launch_bounds__(256) cp_setup_kernel(const __grid_constant__ SetupArgs S) {
     const int qi = blockIdx.x;
     const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
     QueryState& Q = S.qs[qi];
     __shared__ int codes[2];
-    const double* q = (w == 0 ? S.starts : S.goals) + (size_t)qi * CP_N;
-    int code = cp_check_config_d(S, q, lane);
-    if (lane == 0) codes[w] = code;
-    // trees: roots (planner.py:442-443); slots past the root are NaN already
-    if (lane < CP_N) S.trees[((size_t)(2 * qi + w) * CP_N + lane) * S.cap + 0] = (float)q[lane];
-    if (lane == 0) S.parents[(size_t)(2 * qi + w) * S.cap] = 0;
+    if (S.reset_tree) {
+        // NaN-refill the node slots the previous run used (publication marker)
+        const float nan = __int_as_float(0x7fffffff);
+        for (int k = 0; k < 2; k++) {
+            const int h = min(Q.hwm[k], S.cap);
+            float* base = S.trees + (size_t)(2 * qi + k) * CP_N * S.cap;
+            for (int d = 0; d < CP_N; d++)
+                for (int i = threadIdx.x; i < h; i += blockDim.x) base[(size_t)d * S.cap + i] = nan;
+        }
+        __syncthreads();
+    }
+    if (qi == 0 && threadIdx.x < 16 && S.counters) S.counters[threadIdx.x] = 0;
+    if (w < 2) {
+        const double* q = (w == 0 ? S.starts : S.goals) + (size_t)qi * CP_N;
+        int code = cp_check_config_d(S, q, lane);
+        if (lane == 0) codes[w] = code;
+        // trees: roots (planner.py:442-443)
+        if (lane < CP_N) S.trees[((size_t)(2 * qi + w) * CP_N + lane) * S.cap + 0] = (float)q[lane];
+        if (lane == 0) S.parents[(size_t)(2 * qi + w) * S.cap] = 0;
+    }
     __syncthreads();
     if (threadIdx.x == 0) {
         int c = codes[0] ? codes[0] : (codes[1] ? 3 + codes[1] : 0);

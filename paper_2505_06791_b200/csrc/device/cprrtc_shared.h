@@ -88,6 +88,9 @@ struct SetupArgs {
     const double* sph_c;
     const double* sph_r;
     int nb, ne;
+    int* counters;          // planner queue counters, zeroed by block 0 (may be null)
+    int reset_tree;         // 1: NaN-refill the slots the previous run used
+    int pad_;
 };
 
 struct QueryOut {

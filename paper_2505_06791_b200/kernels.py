@@ -86,6 +86,8 @@ class Context:
         self.L = L
         self._scene = None
         self._spec = "none"
+        self._scene_obj = None
+        self._spec_obj = None
         self.kind = 0
         self.m = 1
         self.lock = threading.RLock()
@@ -100,7 +102,10 @@ class Context:
 
     # -- state -----------------------------------------------------------
     def set_scene(self, packed_scene):
+        if packed_scene is self._scene_obj:
+            return
         k = scene_key(packed_scene)
+        self._scene_obj = packed_scene      # kept alive: identity stays valid
         if k != self._scene:
             sh = _lib.SceneHandle(packed_scene)
             _lib.check(self.L.cprrtc_set_scene(self.h, C.byref(sh.s)), "set_scene")
@@ -109,7 +114,10 @@ class Context:
             self.ne = sh.s.n_spheres
 
     def set_spec(self, packed_spec):
+        if packed_spec is self._spec_obj and packed_spec is not None:
+            return
         k = spec_key(packed_spec)
+        self._spec_obj = packed_spec
         if k != self._spec:
             if packed_spec is None:
                 _lib.check(self.L.cprrtc_set_constraint(self.h, None), "set_constraint")
@@ -140,14 +148,22 @@ _CTX: dict = {}
 _CTX_LOCK = threading.Lock()
 
 
+_BY_ID: dict = {}
+
+
 def context(model_or_packed, device: int = 0) -> Context:
     packed = getattr(model_or_packed, "packed", model_or_packed)
-    key = (robot_key(packed), device, threading.get_ident())
+    tid = threading.get_ident()
+    hit = _BY_ID.get((id(packed), device, tid))
+    if hit is not None and hit[0] is packed:
+        return hit[1]
+    key = (robot_key(packed), device, tid)
     with _CTX_LOCK:
         ctx = _CTX.get(key)
         if ctx is None:
             ctx = Context(packed, device)
             _CTX[key] = ctx
+        _BY_ID[(id(packed), device, tid)] = (packed, ctx)   # strong ref: ids stay unique
     return ctx
 
 

@@ -250,7 +250,22 @@ def steer(q_near, q_rand, step: float):
     return q_rand.copy() if dist <= step else q_near + (step / dist) * d
 
 
+_PRM_CACHE: dict = {}
+
+
 def _params_struct(p: PlanParams, opt: DeviceOptions) -> _lib.Params:
+    key = (id(p), id(opt))
+    hit = _PRM_CACHE.get(key)
+    if hit is not None and hit[0] is p and hit[1] is opt:
+        return hit[2]
+    prm = _make_params(p, opt)
+    if len(_PRM_CACHE) > 4096:
+        _PRM_CACHE.clear()
+    _PRM_CACHE[key] = (p, opt, prm)
+    return prm
+
+
+def _make_params(p: PlanParams, opt: DeviceOptions) -> _lib.Params:
     pp = p.projection
     if p.projection_mode not in _MODES:
         raise ValueError(f"unknown projection mode {p.projection_mode!r}")
@@ -297,11 +312,12 @@ def plan_batch(problems, options: DeviceOptions = DeviceOptions(), return_dense:
     if not problems:
         return []
     p0 = problems[0]
-    base = replace(p0.params, seed_offset=0)
-    for p in problems[1:]:
-        if (p.model is not p0.model or p.scene is not p0.scene or p.spec is not p0.spec
-                or replace(p.params, seed_offset=0) != base):
-            raise ValueError("plan_batch problems must share model, scene, spec and params")
+    if len(problems) > 1:
+        base = replace(p0.params, seed_offset=0)
+        for p in problems[1:]:
+            if (p.model is not p0.model or p.scene is not p0.scene or p.spec is not p0.spec
+                    or replace(p.params, seed_offset=0) != base):
+                raise ValueError("plan_batch problems must share model, scene, spec and params")
     prm = _params_struct(p0.params, options)
     ctx = _bind(p0, options)
     n = ctx.n
@@ -313,8 +329,7 @@ def plan_batch(problems, options: DeviceOptions = DeviceOptions(), return_dense:
         raise ValueError("seed_offset must be >= 0")
     res = (_lib.Result * B)()
     pc = int(prm.path_capacity)
-    paths = np.empty((B, pc, n))
-    srcs = np.empty((B, pc), np.int32)
+    paths, srcs = _out_buffers(B, pc, n)
     with ctx.lock:
         ctx.prepare(p0.params.width)
         t0 = time.perf_counter()
@@ -353,6 +368,20 @@ def plan_batch(problems, options: DeviceOptions = DeviceOptions(), return_dense:
             dense, ok = _derive(ctx, prm, paths[i, :L], srcs[i, :L - 1])
         out.append(PlanResult("Solved", tuple(path), sources, stats, dense))
     return out
+
+
+_OUT: dict = {}
+
+
+def _out_buffers(B, pc, n):
+    """Reusable host result buffers (paths are copied out per result)."""
+    key = (B, pc, n, __import__("threading").get_ident())
+    buf = _OUT.get(key)
+    if buf is None:
+        if len(_OUT) > 64:
+            _OUT.clear()
+        buf = _OUT[key] = (np.empty((B, pc, n)), np.empty((B, pc), np.int32))
+    return buf
 
 
 def plan(problem: PlanProblem, options: DeviceOptions = DeviceOptions(),
