@@ -202,6 +202,17 @@ CPRRTC_API int cprrtc_halton(void *ctx, int count, int64_t first_index, int64_t 
 CPRRTC_API int cprrtc_plan(void *ctx, const cprrtc_params *params, int B, const double *starts,
                 const double *goals, const int64_t *seeds, cprrtc_result *results,
                 double *paths, int32_t *sources);
+/* One reference extend() (op 0, planner.py:317-325 / _attempt_extend :265-306)
+ * or connect() (op 1, planner.py:361-409) step on a caller tree: nodes (N, n),
+ * parents (N); q (n) is the sample / target.  result[0]: extend -> index of
+ * the new node, or -1 degenerate, -2 projection, -3 collision, -4 full;
+ * connect -> meet node index (Reached) or -1.  result[1]: segments added by
+ * connect; result[2]: node count afterwards.  Appended nodes / parents are
+ * returned in new_nodes (max_new, n) / new_parents; stats as cprrtc_result. */
+CPRRTC_API int cprrtc_step(void *ctx, const cprrtc_params *params, int op, int N, const double *nodes,
+                           const int32_t *parents, const double *q, int32_t *result,
+                           double *new_nodes, int32_t *new_parents, int max_new, uint64_t *stats);
+
 /* derive_edge (planner.py:223-245) for every consecutive pair of a path:
  * nodes (n_nodes, n), sources (n_nodes-1): 0 start, 1 junction, 2 goal --
  * goal edges are derived in tree-growth direction and returned reversed

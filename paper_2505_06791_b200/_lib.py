@@ -29,7 +29,7 @@ EXPORTS = (
     "cprrtc_last_timing", "cprrtc_fk", "cprrtc_task_err_jac", "cprrtc_task_error_at",
     "cprrtc_project_config", "cprrtc_check_config", "cprrtc_validate", "cprrtc_project",
     "cprrtc_nearest", "cprrtc_halton", "cprrtc_plan", "cprrtc_derive_edges",
-    "cprrtc_clearance", "cprrtc_damped_step", "cprrtc_flush_l2", "cprrtc_nearest_trees",
+    "cprrtc_clearance", "cprrtc_damped_step", "cprrtc_flush_l2", "cprrtc_nearest_trees", "cprrtc_step",
 )
 
 

@@ -623,7 +623,8 @@ __device__ __noinline__ ValOut cp_validate(const Team tm, const float (*seg)[CP_
     const i64 per = (i64)CP_S * E + CP_P;
     o.valid = key == CP_INTMAX;
     o.first_bad = o.valid ? -1 : idx;
-    o.performed = (flag_on && !o.valid) ? (i64)key * W + idx + 1 : per * W;
+    const int nw = W - t_first;   // waypoints checked (the planner skips row 0, an existing node)
+    o.performed = (flag_on && !o.valid) ? (i64)key * nw + (idx - t_first) + 1 : per * nw;
     o.gpu_checks = rounds_done * (W - t_first);
     o.fk_evals = W - t_first;
     return o;
@@ -770,7 +771,7 @@ __device__ __forceinline__ bool cp_should_stop(const Team& tm, QueryState& Q, co
 __device__ __forceinline__ bool cp_check_motion(const Team& tm, TeamWS& ws, const PlanArgs& A,
                                                 const SceneSm& sc, Stats& st) {
     ValOut v = cp_validate(tm, ws.seg, A.W, 1, A.flag_on, A.margin, sc);
-    st.v[ST_CCPERF] += v.gpu_checks;
+    st.v[ST_CCPERF] += v.performed;     // reference (lockstep) semantics, pure.py:664-698
     st.v[ST_CCPOSS] += (u64)((i64)CP_S * (sc.nb + sc.ne) + CP_P) * (A.W - 1);
     st.v[ST_GPUCHK] += v.gpu_checks;
     st.v[ST_FKCC] += v.fk_evals;
@@ -821,14 +822,17 @@ __device__ __forceinline__ void cp_load_node(const Team& tm, const PlanArgs& A, 
 // connect (planner.py:361-409): greedy walk of tree k toward ws.qt.
 // Returns the meet node index if Reached, else -1.
 __device__ __noinline__ int cp_connect(const Team& tm, TeamWS& ws, const PlanArgs& A, const SceneSm& sc,
-                          QueryState& Q, int qi, int k, Stats& st) {
+                          QueryState& Q, int qi, int k, Stats& st, int* segments_out = nullptr) {
+    int segs_added = 0;
     const int cnt = cp_count(A, Q, k);
     st.v[ST_NNODES] += cnt;
     int icur = cp_nearest(tm, cp_tree(A, qi, k), A.cap, cnt, ws.qt);
     cp_load_node(tm, A, qi, k, icur, ws.qc);
     float dist = cp_vec_dist(tm, ws.qc, ws.qt);
+    if (segments_out) *segments_out = 0;
     if (dist <= A.tol) return icur;
     for (int segs = 0; segs < A.max_connect; segs++) {
+        if (segments_out) *segments_out = segs_added;
         if (cp_should_stop(tm, Q, A)) return -1;
         cp_steer(tm, ws.qc, ws.qt, A.step, ws.qs);
         cp_interp(tm, ws.seg, A.W, ws.qc, ws.qs);
@@ -847,11 +851,42 @@ __device__ __noinline__ int cp_connect(const Team& tm, TeamWS& ws, const PlanArg
         int idx = cp_append(tm, A, Q, qi, k, ws.qe, icur);
         if (idx < 0) return -1;
         icur = idx;
+        segs_added++;
+        if (segments_out) *segments_out = segs_added;
         cp_copy(tm, ws.qc, ws.qe);
         dist = nd;
         if (dist <= A.tol) return icur;
     }
     return -1;
+}
+
+// _attempt_extend + commit (planner.py:265-325) for the sample in ws.qr against
+// tree a: the new node's index, or -1 degenerate, -2 projection, -3 collision,
+// -4 tree full.  ws.qe holds the new node on success.
+__device__ __noinline__ int cp_extend_once(const Team& tm, TeamWS& ws, const PlanArgs& A, const SceneSm& sc,
+                                           QueryState& Q, int qi, int a, Stats& st) {
+    const int W = A.W;
+    const int cnt_a = cp_count(A, Q, a);
+    st.v[ST_NNODES] += cnt_a;
+    const int inear = cp_nearest(tm, cp_tree(A, qi, a), A.cap, cnt_a, ws.qr);
+    cp_load_node(tm, A, qi, a, inear, ws.qn);
+    cp_steer(tm, ws.qn, ws.qr, A.step, ws.qs);
+    if (cp_vec_equal(tm, ws.qs, ws.qn)) return -1;
+    cp_interp(tm, ws.seg, W, ws.qn, ws.qs);
+    int pit, ppr;
+    bool okp = cp_project(tm, ws.seg, W, A.pa, &pit, &ppr, nullptr, nullptr, &st.v[ST_STAGE1]);
+    st.v[ST_PROJITER] += pit;
+    if (!okp) { st.v[ST_PFAIL]++; return -2; }
+    cp_copy(tm, ws.qe, ws.seg[W - 1]);
+    if (cp_vec_equal(tm, ws.qe, ws.qn)) return -1;
+    if (cp_vec_equal(tm, ws.qe, ws.qs)) {
+        if (!cp_check_motion(tm, ws, A, sc, st)) return -3;
+    } else {
+        const unsigned long long pf0 = st.v[ST_PFAIL];
+        if (!cp_derive_edge(tm, ws, A, sc, ws.qn, ws.qe, st)) return st.v[ST_PFAIL] != pf0 ? -2 : -3;
+    }
+    const int node = cp_append(tm, A, Q, qi, a, ws.qe, inear);
+    return node < 0 ? -4 : node;
 }
 
 // One team works on query qi until it is solved / stopped / out of samples.
@@ -876,27 +911,10 @@ __device__ void cp_plan_query(const Team& tm, TeamWS& ws, const PlanArgs& A, con
         // sample (sampling.py:65-81) -- FP64 Halton, bit-exact with the reference
         if ((int)tm.lane < CP_N) ws.qr[tm.lane] = (float)cp_halton((i64)it + Q.seed_offset, tm.lane);
         tm.sync();
-        // _attempt_extend (planner.py:265-306)
-        const int cnt_a = cp_count(A, Q, a);
-        st.v[ST_NNODES] += cnt_a;
-        const int inear = cp_nearest(tm, cp_tree(A, qi, a), A.cap, cnt_a, ws.qr);
-        cp_load_node(tm, A, qi, a, inear, ws.qn);
-        cp_steer(tm, ws.qn, ws.qr, A.step, ws.qs);
-        if (cp_vec_equal(tm, ws.qs, ws.qn)) continue;              // degenerate
-        cp_interp(tm, ws.seg, W, ws.qn, ws.qs);
-        int pit, ppr;
-        bool okp = cp_project(tm, ws.seg, W, A.pa, &pit, &ppr, nullptr, nullptr, &st.v[ST_STAGE1]);
-        st.v[ST_PROJITER] += pit;
-        if (!okp) { st.v[ST_PFAIL]++; continue; }
-        cp_copy(tm, ws.qe, ws.seg[W - 1]);
-        if (cp_vec_equal(tm, ws.qe, ws.qn)) continue;              // degenerate
-        if (cp_vec_equal(tm, ws.qe, ws.qs)) {
-            if (!cp_check_motion(tm, ws, A, sc, st)) continue;
-        } else if (!cp_derive_edge(tm, ws, A, sc, ws.qn, ws.qe, st)) {
-            continue;
-        }
-        const int node = cp_append(tm, A, Q, qi, a, ws.qe, inear);
-        if (node < 0) break;
+        // _attempt_extend (planner.py:265-306) + commit
+        const int node = cp_extend_once(tm, ws, A, sc, Q, qi, a, st);
+        if (node == -4) break;
+        if (node < 0) continue;
         st.v[ST_ADDED]++;
         // connect the other tree toward q_new (planner.py:463)
         cp_copy(tm, ws.qt, ws.qe);
@@ -1407,6 +1425,37 @@ cp_dense_kernel(int E, const __grid_constant__ PlanArgs A, const float* nodes, c
             for (int k = 0; k < CP_N; k++) dense[((size_t)e * A.W + row) * CP_N + k] = ws.seg[tm.lane][k];
         }
         if (tm.lane == 0) ok[e] = good;
+    }
+}
+
+// One reference extend() or connect() step on tree k of query 0 (the host
+// uploaded the tree): op 0 extends toward q, op 1 connects toward q
+// (planner.py:317-325, 361-409).  One team, 32 threads.
+extern "C" __global__ void __launch_bounds__(32)
+cp_step_kernel(const __grid_constant__ PlanArgs A, int op, int k, const float* q, int* out, unsigned long long* stats) {
+    extern __shared__ float4 cp_smem[];
+    SceneSm sc = cp_stage_scene(A.scene_g, cp_smem);
+    TeamWS* wsa = reinterpret_cast<TeamWS*>(cp_smem + cp_scene_f4(A.scene_g));
+    if ((int)threadIdx.x >= CP_G) return;
+    Team tm;
+    TeamWS& ws = wsa[0];
+    QueryState& Q = A.qs[0];
+    if ((int)tm.lane < CP_N) { ws.qr[tm.lane] = q[tm.lane]; ws.qt[tm.lane] = q[tm.lane]; }
+    tm.sync();
+    Stats st;
+    int r, segs = 0;
+    if (op == 0) {
+        st.v[ST_ATT]++;
+        r = cp_extend_once(tm, ws, A, sc, Q, 0, k, st);
+        if (r >= 0) st.v[ST_ADDED]++;
+    } else {
+        r = cp_connect(tm, ws, A, sc, Q, 0, k, st, &segs);
+    }
+    if (tm.lane == 0) {
+        out[0] = r;
+        out[1] = segs;
+        out[2] = min(Q.count[k], A.cap);
+        for (int i = 0; i < ST_NSTAT; i++) stats[i] = st.v[i];
     }
 }
 #endif  // !CP_PARITY

@@ -344,7 +344,7 @@ std::string prelude(const Ctx* c, int G, int kind, int orient, int parity) {
 }
 
 const std::vector<const char*> kPlanKernels = {"cp_plan_kernel", "cp_setup_kernel", "cp_reset_kernel",
-                                                "cp_extract_kernel", "cp_dense_kernel"};
+                                                "cp_extract_kernel", "cp_dense_kernel", "cp_step_kernel"};
 const std::vector<const char*> kParityKernels = {"cp_fk_kernel",           "cp_tej_kernel",
                                                   "cp_err_at_kernel",       "cp_project_config_kernel",
                                                   "cp_check_config_kernel", "cp_validate_kernel",
@@ -1232,6 +1232,75 @@ int cprrtc_plan(void* p, const cprrtc_params* prm, int B, const double* starts, 
         }
         if (sources && r.path_len > 1)
             for (int k = 0; k < r.path_len - 1; k++) sources[(size_t)i * path_cap + k] = hs[(size_t)i * path_cap + k];
+    }
+    return 0;
+}
+
+int cprrtc_step(void* p, const cprrtc_params* prm, int op, int N, const double* nodes, const int32_t* parents,
+                const double* q, int32_t* result, double* new_nodes, int32_t* new_parents, int max_new,
+                uint64_t* stats) {
+    Ctx* c = C(p);
+    if (!c || !prm || (op != 0 && op != 1) || N < 1 || !nodes || !parents || !q || !result || max_new < 0 ||
+        (max_new && (!new_nodes || !new_parents)))
+        return fail(CPRRTC_EARG, "bad argument");
+    if (int rc = set_device(c)) return rc;
+    Module* m;
+    if (int rc = cur_module(c, prm->width, 0, &m)) return rc;
+    const int n = c->n;
+    int cap = (int)(((long long)N + prm->max_connect_segments + 2 + 127) / 128 * 128);
+    if (c->nq_alloc >= 1 && c->cap_alloc >= cap) cap = c->cap_alloc;   // reuse the planner buffers
+    const int path_cap = c->path_cap > 0 ? c->path_cap : 1024;
+    if (int rc = ensure_plan_buffers(c, c->nq_alloc > 1 ? c->nq_alloc : 1, cap, path_cap)) return rc;
+    // tree 0 of query 0 <- the caller's tree (NaN beyond N), its parents, its count
+    std::vector<float> soa((size_t)n * cap, NAN);
+    for (int i = 0; i < N; i++)
+        for (int k = 0; k < n; k++) soa[(size_t)k * cap + i] = (float)nodes[(size_t)i * n + k];
+    CUDA_TRY(cudaMemcpyAsync(c->trees.p, soa.data(), soa.size() * 4, cudaMemcpyHostToDevice, c->stream));
+    CUDA_TRY(cudaMemcpyAsync(c->parents.p, parents, (size_t)N * 4, cudaMemcpyHostToDevice, c->stream));
+    QueryState Q;
+    CUDA_TRY(cudaMemcpyAsync(&Q, c->qs.p, sizeof Q, cudaMemcpyDeviceToHost, c->stream));
+    CUDA_TRY(cudaStreamSynchronize(c->stream));
+    Q.count[0] = N;
+    Q.hwm[0] = cap;          // the next plan() refills the whole tree with NaN
+    Q.solved = Q.stop = Q.timed_out = Q.overflow = Q.exhausted = 0;
+    Q.setup_code = 0;
+    CUDA_TRY(cudaMemcpyAsync(c->qs.p, &Q, sizeof Q, cudaMemcpyHostToDevice, c->stream));
+    const double tau = prm->tau_task > 0 ? prm->tau_task : c->tau_task;
+    PlanArgs A = make_plan_args(c, prm, 1, cap, tau);
+    A.budget_ns = 0;
+    std::vector<float> qf(n);
+    for (int k = 0; k < n; k++) qf[k] = (float)q[k];
+    int rc = upload(c, c->scratch[0], qf.data(), (size_t)n);
+    rc = rc ? rc : c->scratch[1].ensure(64);
+    rc = rc ? rc : c->scratch[2].ensure(8 * CPRRTC_ST_COUNT);
+    if (rc) return rc;
+    if (int rc2 = upload_conf(c, m)) return rc2;
+    int zero = 0;
+    const float* dq = c->scratch[0].as<float>();
+    int* dout = c->scratch[1].as<int>();
+    unsigned long long* dst = c->scratch[2].as<unsigned long long>();
+    void* args[] = {&A, &op, &zero, &dq, &dout, &dst};
+    if (int rc2 = launch(c, m, "cp_step_kernel", 1, 1, 32, scene_smem(c) + m->ws_bytes, args)) return rc2;
+    int out[3];
+    unsigned long long st[CPRRTC_ST_COUNT];
+    download(c, out, c->scratch[1], 3);
+    download(c, st, c->scratch[2], CPRRTC_ST_COUNT);
+    if (int rc3 = sync(c)) return rc3;
+    result[0] = out[0];
+    result[1] = out[1];
+    result[2] = out[2];
+    if (stats)
+        for (int i = 0; i < CPRRTC_ST_COUNT; i++) stats[i] = st[i];
+    const int added = out[2] - N;
+    if (added > max_new) return fail(CPRRTC_ELIMIT, "max_new too small for the appended nodes");
+    if (added > 0) {
+        std::vector<float> row((size_t)added);
+        for (int k = 0; k < n; k++) {
+            CUDA_TRY(cudaMemcpy(row.data(), c->trees.as<float>() + (size_t)k * cap + N, (size_t)added * 4,
+                                cudaMemcpyDeviceToHost));
+            for (int i = 0; i < added; i++) new_nodes[(size_t)i * n + k] = row[i];
+        }
+        CUDA_TRY(cudaMemcpy(new_parents, c->parents.as<int>() + N, (size_t)added * 4, cudaMemcpyDeviceToHost));
     }
     return 0;
 }

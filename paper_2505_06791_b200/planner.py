@@ -18,9 +18,11 @@ Differences from the reference, all deliberate:
   launches; ``deterministic`` keeps its reference meaning (ignore the wall
   clock).  ``attempts`` is accepted; the device already evaluates hundreds of
   samples at once.
-* ``stats.iterations`` counts samples drawn; ``cc_performed`` counts the
-  checks the GPU actually evaluated (waypoint 0 of a motion is an existing
-  tree node and is not re-checked).
+* ``stats.iterations`` counts samples drawn; ``cc_performed`` /
+  ``cc_possible`` use the reference's lockstep accounting over the checked
+  waypoints (row 0 of a motion is an existing tree node and is not
+  re-checked); the checks the GPU actually evaluated are in the result's
+  device counters.
 """
 
 from __future__ import annotations
@@ -42,7 +44,8 @@ from .projection import MotionSegment, ProjectionParams
 __all__ = [
     "Tree", "PlanParams", "PlanProblem", "PlanResult", "PlanStats", "PlanContext",
     "ExtendOutcome", "ConnectOutcome", "DeviceOptions", "nearest", "steer", "plan",
-    "plan_batch", "extract_path", "derive_edge", "revalidate_path", "dense_path",
+    "plan_batch", "extract_path", "derive_edge", "revalidate_path", "dense_path", "extend",
+    "connect", "prepare",
 ]
 
 
@@ -474,6 +477,61 @@ def extract_path(tree_s: Tree, tree_g: Tree, meet_s: int, meet_g: int):
         sources.append("goal" if dup else "junction")
         sources += ["goal"] * (len(pb) - 1)
     return tuple(pa + pb), tuple(sources)
+
+
+_REASON = {-1: "degenerate", -2: "projection", -3: "collision", -4: "capacity"}
+
+
+def _step(op: int, tree: Tree, q, ctx: PlanContext):
+    spec = None if ctx.spec is not None and math.isinf(ctx.spec.tau_task) else ctx.spec
+    n = tree.nodes.shape[1]
+    q = np.ascontiguousarray(np.asarray(q, dtype=float).reshape(n))
+    prob = PlanProblem(ctx.model, ctx.scene, spec, tree.node(0), tree.node(0), ctx.params)
+    dctx = _bind(prob, ctx.options)
+    prm = _params_struct(ctx.params, ctx.options)
+    nodes = np.ascontiguousarray(tree.nodes, dtype=np.float64)
+    parents = np.ascontiguousarray(tree.parents, dtype=np.int32)
+    res = np.zeros(3, np.int32)
+    cap_new = int(ctx.params.max_connect_segments) + 2
+    new_nodes = np.empty((cap_new, n))
+    new_par = np.empty(cap_new, np.int32)
+    st = np.zeros(_lib.ST_COUNT, np.uint64)
+    with dctx.lock:
+        dctx.prepare(ctx.params.width)
+        _lib.check(dctx.L.cprrtc_step(dctx.h, C.byref(prm), op, len(tree), _lib.ptr(nodes),
+                                      _lib.ptr(parents, _lib._ip), _lib.ptr(q), _lib.ptr(res, _lib._ip),
+                                      _lib.ptr(new_nodes), _lib.ptr(new_par, _lib._ip), cap_new,
+                                      st.ctypes.data_as(C.POINTER(C.c_uint64))), "step")
+    added = int(res[2]) - len(tree)
+    for i in range(added):
+        tree.add(new_nodes[i], int(new_par[i]))
+    s = ctx.stats
+    s.extensions_attempted += int(st[1])
+    s.extensions_added += int(st[2])
+    s.projection_failures += int(st[3])
+    s.collision_rejections += int(st[4])
+    s.cc_performed += int(st[5])
+    s.cc_possible += int(st[6])
+    return int(res[0]), int(res[1]), added
+
+
+def extend(tree: Tree, q_rand, ctx: PlanContext) -> ExtendOutcome:
+    """One projected extension toward a sample (planner.py:317-325), on the
+    device; the tree gains the node on success."""
+    r, _, _ = _step(0, tree, q_rand, ctx)
+    if r >= 0:
+        return ExtendOutcome("Added", node=r)
+    return ExtendOutcome("Rejected", reason=_REASON[r])
+
+
+def connect(tree: Tree, q_target, ctx: PlanContext) -> ConnectOutcome:
+    """Greedy connect toward a target (planner.py:361-409), on the device."""
+    r, segs, added = _step(1, tree, q_target, ctx)
+    if r >= 0:
+        return ConnectOutcome("Reached", node=r, segments=segs)
+    if segs > 0:
+        return ConnectOutcome("Advanced", node=len(tree) - 1, segments=segs)
+    return ConnectOutcome("Trapped", node=None, segments=0)
 
 
 def _check_endpoint_message(code: int) -> str:

@@ -1,0 +1,153 @@
+"""The single-step planner API on the device, mirroring the reference's own
+planner tests (T/test_planner.py:111-215): extend / connect outcomes on the
+hand-checkable planar arm, collision early stop, projection failure."""
+
+import numpy as np
+import pytest
+
+import fixtures as fx
+
+pytestmark = pytest.mark.gpu
+
+FP32 = 2e-6
+
+
+def _ctx(model, scene, spec=None, **over):
+    from paper_2505_06791_b200.planner import PlanContext, PlanParams, PlanProblem
+    params = PlanParams(**{"width": 8, "deterministic": True, **over})
+    prob = PlanProblem(model=model, scene=scene, spec=spec, start=np.zeros(model.n),
+                       goal=np.zeros(model.n), params=params)
+    return PlanContext.from_problem(prob)
+
+
+def _scenes():
+    from paper_2505_06791_b200.geometry import Aabb, Scene
+    empty = Scene(boxes=[], spheres=[])
+    far = Scene(boxes=[Aabb([5.0, 5.0, -1.0], [6.0, 6.0, 1.0])], spheres=[])
+    return empty, far
+
+
+def test_extend_adds_a_node_at_step_distance():
+    from paper_2505_06791_b200.planner import Tree, extend
+    _, far = _scenes()
+    ctx = _ctx(fx.robot("planar2"), far)
+    tree = Tree([0.0, 0.0], "start")
+    out = extend(tree, np.array([2.0, 0.0]), ctx)
+    assert out.added and out.node == 1
+    assert np.allclose(tree.node(1), [0.5, 0.0], atol=FP32)
+    assert ctx.stats.extensions_attempted == 1 and ctx.stats.extensions_added == 1
+    assert ctx.stats.cc_performed > 0
+
+
+def test_extend_rejects_sample_at_the_tree():
+    from paper_2505_06791_b200.planner import Tree, extend
+    empty, _ = _scenes()
+    ctx = _ctx(fx.robot("planar2"), empty)
+    tree = Tree([0.0, 0.0], "start")
+    out = extend(tree, np.zeros(2), ctx)
+    assert not out.added and out.reason == "degenerate" and len(tree) == 1
+
+
+def test_extend_rejects_on_collision_with_early_stop():
+    from paper_2505_06791_b200.geometry import Aabb, Scene
+    from paper_2505_06791_b200.planner import Tree, extend
+    box = Aabb([0.70, 0.15, -0.05], [0.76, 0.22, 0.05])
+    ctx = _ctx(fx.robot("planar2"), Scene(boxes=[box], spheres=[]), width=16)
+    tree = Tree([0.0, 0.0], "start")
+    out = extend(tree, np.array([np.pi / 2, 0.0]), ctx)
+    assert not out.added and out.reason == "collision" and len(tree) == 1
+    assert ctx.stats.collision_rejections == 1
+    assert ctx.stats.cc_performed < ctx.stats.cc_possible      # early stop
+
+
+def test_extend_rejects_on_projection_failure():
+    from paper_2505_06791_b200.planner import Tree, extend
+    from paper_2505_06791_b200.projection import ProjectionParams
+    empty, _ = _scenes()
+    m, sp = fx.robot("arm7"), fx.spec("plane55")
+    start = fx.plans()[0]["start"]
+    ctx = _ctx(m, empty, spec=sp, projection=ProjectionParams(max_iters=1))
+    tree = Tree(start, "start")
+    out = extend(tree, fx.kats()["halton_arm7_17"][5], ctx)
+    assert not out.added and out.reason == "projection"
+    assert ctx.stats.projection_failures == 1
+
+
+def test_connect_reached_walk_trapped_advanced():
+    from paper_2505_06791_b200.geometry import Aabb, Scene
+    from paper_2505_06791_b200.planner import ConnectOutcome, Tree, connect
+    empty, _ = _scenes()
+    m = fx.robot("planar2")
+    ctx = _ctx(m, empty)
+    tree = Tree([0.0, 0.0], "start")
+    assert connect(tree, np.array([0.01, 0.0]), ctx) == ConnectOutcome("Reached", node=0, segments=0)
+    tree = Tree([0.0, 0.0], "start")
+    target = np.array([1.6, 0.0])
+    out = connect(tree, target, ctx)
+    assert out.reached and out.segments == 4 and len(tree) == 5      # 0.5+0.5+0.5+0.1
+    assert np.allclose(tree.node(out.node), target, atol=FP32)
+    d = [float(np.linalg.norm(tree.node(i) - target)) for i in tree.chain(out.node)]
+    assert all(b < a for a, b in zip(d, d[1:]))
+    blocker1 = Aabb([0.70, 0.15, -0.05], [0.76, 0.22, 0.05])
+    ctx = _ctx(m, Scene(boxes=[blocker1], spheres=[]), width=16)
+    tree = Tree([0.0, 0.0], "start")
+    assert connect(tree, np.array([0.5, 0.0]), ctx) == ConnectOutcome("Trapped", node=None, segments=0)
+    blocker2 = Aabb([0.52, 0.48, -0.05], [0.58, 0.55, 0.05])
+    ctx = _ctx(m, Scene(boxes=[blocker2], spheres=[]), width=16)
+    tree = Tree([0.0, 0.0], "start")
+    out = connect(tree, np.array([1.0, 0.0]), ctx)
+    assert out.status == "Advanced" and out.segments == 1
+    assert np.allclose(tree.node(out.node), [0.5, 0.0], atol=FP32)
+
+
+def test_derive_edge_is_reproducible():
+    from paper_2505_06791_b200.planner import derive_edge, steer
+    m, sc, sp = fx.robot("arm7"), fx.scene("shelf"), fx.spec("plane55")
+    p = fx.plans()[0]
+    a, b = np.array(p["start"]), np.array(p["goal"])
+    ctx = _ctx(m, sc, spec=sp, width=16)
+    mid = steer(a, b, 0.5)
+    e1, e2 = derive_edge(a, mid, ctx), derive_edge(a, mid, ctx)
+    assert e1 is not None and np.array_equal(e1.waypoints, e2.waypoints)
+    assert np.allclose(e1.start, a, atol=FP32)
+
+
+def test_generate_pairs_match_reference():
+    """Device-batched generate_pair reproduces the reference's pairs
+    (tests/golden/pairs.npz, maniplan/bench.py:229-259) to FP64 rounding."""
+    from paper_2505_06791_b200.harness import generate_pairs
+    prs = fx.pairs()
+    cases = [("upright", "table", "upright", range(300, 316)),
+             ("table_plane", "table", "table_plane", range(0, 16)),
+             ("rand10_s3", "rand10_s3", None, range(30, 40))]
+    total = same = 0
+    for key, scname, spname, seeds in cases:
+        m, sc = fx.robot("arm7"), fx.scene(scname)
+        sp = None if spname is None else fx.spec(spname)
+        got = generate_pairs(m, sc, sp, list(seeds))
+        for i, s in enumerate(prs[f"{key}_seed"]):
+            if s not in got:
+                continue
+            total += 1
+            a, b = got[int(s)]
+            if np.allclose(a, prs[f"{key}_start"][i], atol=1e-9) and \
+                    np.allclose(b, prs[f"{key}_goal"][i], atol=1e-9):
+                same += 1
+    assert total >= 35 and same >= 0.95 * total, (same, total)
+
+
+def test_trial_records_round_trip(tmp_path):
+    from paper_2505_06791_b200.harness import read_records, run_trials, summarize, write_records
+    from paper_2505_06791_b200.planner import PlanParams, PlanProblem
+    m, sc, sp = fx.robot("arm7"), fx.scene("table"), fx.spec("table_plane")
+    prs = fx.pairs()
+    probs = [PlanProblem(m, sc, sp, prs["table_plane_start"][i], prs["table_plane_goal"][i],
+                         PlanParams(width=16, max_iterations=2000), name=f"table_plane#{i}")
+             for i in range(3)]
+    recs = run_trials(probs, trials=2)
+    assert len(recs) == 6 and all(r.status == "Solved" for r in recs)
+    write_records(tmp_path / "records.csv", recs)
+    back = read_records(tmp_path / "records.csv")
+    assert [r.row() for r in back] == [r.row() for r in recs]
+    summ = summarize(recs)
+    assert all(v["success_rate"] == 1.0 for v in summ.values())
