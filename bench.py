@@ -156,7 +156,7 @@ def run_b200(args, world, rank, local):
     from paper_2505_06791_b200 import kernels
     from paper_2505_06791_b200.planner import DeviceOptions, PlanParams, PlanProblem, plan, prepare
     model, scene, spec, starts, goals = workload()
-    opt = DeviceOptions(device=local, teams=args.teams)
+    opt = DeviceOptions(device=local, teams=args.teams, cc_broadphase=args.cc_broadphase)
     Q = args.queries
 
     def problem(step, j):
@@ -304,6 +304,18 @@ def extras(args, local, model, line):
     peak = line["roofline"]["peak"]
     out["cc_checks_per_s"] = checks / s_off
     out["cc_effective_checks_per_s_flag_on"] = poss / (on["kernel_ms"] * 1e-3)
+    # the same motions through the clustered broad phase: reference checks
+    # resolved per second (possible / time) and the checks it evaluated
+    bp = None
+    for _ in range(3):
+        r = kernels.validate_batch(model, sc, wps, True, device=local, broadphase=True)
+        if bp is None or r["kernel_ms"] < bp["kernel_ms"]:
+            bp = r
+    assert (bp["valid"] == on["valid"]).mean() > 0.99
+    out["cc_broadphase"] = {"effective_checks_per_s": poss / (bp["kernel_ms"] * 1e-3),
+                            "checks_evaluated_frac": float(bp["performed"].sum()) / poss,
+                            "kernel_ms": bp["kernel_ms"], "flag": "on",
+                            "kernel": "cp_validate_cull_kernel (999 boxes, 4096 motions x 16)"}
     out["roofline_cc"] = {"bound": "fp32", "kernel": "cp_validate_kernel (999 boxes, 4096 motions x 16)",
                           "achieved": cc_flops / s_off / 1e12, "peak": peak, "unit": "TFLOP/s",
                           "frac": cc_flops / s_off / 1e12 / peak, "traffic": None,
@@ -384,22 +396,27 @@ def other_configs(args, local):
     for name in ("configs[0]", "configs[2]:shelf_x11", "configs[2]:shelf_x111", "configs[3]"):
         label, probs = _cfg_problems(name)
         times, solved, total = [], 0, 0
-        for flag in (("on", "off") if name.startswith("configs[2]") else ("on",)):
+        # configs[2] ablations: early-exit flag on/off x broad phase (auto: on
+        # from 32 primitives) / the reference's lockstep check order
+        variants = ((("on", -1, ""), ("off", -1, " (cc flag off)"), ("on", 0, " (lockstep order)"),
+                     ("off", 0, " (lockstep order, cc flag off)"))
+                    if name.startswith("configs[2]") else (("on", -1, ""),))
+        for flag, bp, suffix in variants:
             tflag = []
+            opt = DeviceOptions(device=local, cc_broadphase=bp)
             for (m, sc, sp, s, g, kw) in probs:
                 for seed in range(3):
                     p = PlanProblem(m, sc, sp, s, g, PlanParams(max_iterations=10**6, time_budget_ms=2000.0,
                                                                 seed_offset=seed * 10_000, flag_mode=flag, **kw))
-                    ctx = prepare(p, DeviceOptions(device=local))
+                    ctx = prepare(p, opt)
                     ctx.flush_l2()
-                    r = plan(p, DeviceOptions(device=local))
+                    r = plan(p, opt)
                     total += 1
                     if r.solved:
                         solved += 1
                         tflag.append(ctx.last_timing()[0])
-            key = name if flag == "on" else name + " (cc flag off)"
-            res[key] = {"workload": label, "median_ms": float(np.median(tflag)) if tflag else None,
-                        "queries": len(probs) * 3, "success_rate": len(tflag) / (len(probs) * 3)}
+            res[name + suffix] = {"workload": label, "median_ms": float(np.median(tflag)) if tflag else None,
+                                  "queries": len(probs) * 3, "success_rate": len(tflag) / (len(probs) * 3)}
         if not args.no_cpu:
             cpu = []
             ok = 0
@@ -537,6 +554,8 @@ def main():
     ap.add_argument("--queries", type=int, default=25, help="queries per step per GPU")
     ap.add_argument("--teams", type=int, default=_env_int("CPRRTC_TEAMS", 0))
     ap.add_argument("--max-iterations", type=int, default=1_000_000)
+    ap.add_argument("--cc-broadphase", type=int, default=-1,
+                    help="planner CC: 1 clustered broad phase, 0 reference lockstep order, -1 auto")
     ap.add_argument("--budget-ms", type=float, default=2000.0)
     ap.add_argument("--cpu-queries", type=int, default=20)
     ap.add_argument("--cpu-budget-ms", type=float, default=2000.0)

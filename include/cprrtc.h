@@ -25,7 +25,7 @@
 extern "C" {
 #endif
 
-#define CPRRTC_ABI_VERSION 1
+#define CPRRTC_ABI_VERSION 2
 
 #if defined(__GNUC__)
 #define CPRRTC_API __attribute__((visibility("default")))
@@ -103,6 +103,11 @@ typedef struct {
     int teams;               /* concurrent extension teams (0: fill the GPU) */
     int tree_capacity;       /* nodes per tree (0: auto) */
     int path_capacity;       /* max path nodes returned per query (0: 1024) */
+    int cc_broadphase;       /* 1: planner CC through the clustered broad phase
+                                (cprrtc_validate_broadphase; same verdicts, the
+                                cc_performed stat then counts evaluated checks);
+                                0: the reference's lockstep check order;
+                                -1: on from 32 obstacle primitives */
 } cprrtc_params;
 
 /* stats[] layout of cprrtc_result (PlanStats, planner.py:130-141) */
@@ -175,6 +180,14 @@ CPRRTC_API int cprrtc_check_config(void *ctx, int B, const double *q, double tau
  * reference counters (performed = lockstep-equivalent count) */
 CPRRTC_API int cprrtc_validate(void *ctx, int B, int W, const double *wps, int flag_on, double margin,
                     int32_t *valid, int32_t *first_bad, int64_t *performed,
+                    int64_t *possible, int64_t *gpu_checks);
+/* the same verdicts (validate_waypoints, pure.py:646-699) through the
+ * clustered broad phase: Morton-sorted chunks of 8 primitives behind
+ * conservative bounding boxes, per-waypoint robot bounding box.  Counters
+ * are this kernel's own: performed = sphere-primitive checks evaluated,
+ * gpu_checks = those + bound tests, first_bad = lowest colliding waypoint. */
+CPRRTC_API int cprrtc_validate_broadphase(void *ctx, int B, int W, const double *wps, int flag_on,
+                    double margin, int32_t *valid, int32_t *first_bad, int64_t *performed,
                     int64_t *possible, int64_t *gpu_checks);
 /* project_segment (pure.py:618-635) for B segments; tau_sm per segment
  * (NULL: auto); trace (B,max_iters,W,n) + trace_prog (B,max_iters) optional */

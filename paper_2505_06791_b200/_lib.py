@@ -30,6 +30,7 @@ EXPORTS = (
     "cprrtc_project_config", "cprrtc_check_config", "cprrtc_validate", "cprrtc_project",
     "cprrtc_nearest", "cprrtc_halton", "cprrtc_plan", "cprrtc_derive_edges",
     "cprrtc_clearance", "cprrtc_damped_step", "cprrtc_flush_l2", "cprrtc_nearest_trees", "cprrtc_step",
+    "cprrtc_validate_broadphase",
 )
 
 
@@ -59,7 +60,8 @@ class Params(C.Structure):
                 ("time_budget_ms", C.c_double), ("connect_tolerance", C.c_double),
                 ("projection_mode", C.c_int), ("flag_on", C.c_int), ("deterministic", C.c_int),
                 ("max_connect_segments", C.c_int), ("cc_margin", C.c_double),
-                ("teams", C.c_int), ("tree_capacity", C.c_int), ("path_capacity", C.c_int)]
+                ("teams", C.c_int), ("tree_capacity", C.c_int), ("path_capacity", C.c_int),
+                ("cc_broadphase", C.c_int)]
 
 
 ST_COUNT = 12

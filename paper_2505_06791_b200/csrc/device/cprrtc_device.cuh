@@ -26,6 +26,8 @@
 #define CP_M ((CP_KIND == 0 ? 1 : 2) + (CP_ORIENT ? 3 : 0))
 #define CP_NP ((CP_N % 2) ? CP_N : (CP_N + 1))   // odd row pitch: no bank conflicts
 #define CP_CHUNK 8
+#define CP_BCH (2 + 2 * CP_CHUNK)   // float4s per box chunk of the clustered scene
+#define CP_SCH (2 + CP_CHUNK)       // float4s per sphere chunk
 #define CP_INTMAX 0x7fffffff
 #define CP_PATH_CAP 4096
 
@@ -630,6 +632,136 @@ __device__ __noinline__ ValOut cp_validate(const Team tm, const float (*seg)[CP_
     return o;
 }
 
+// Broad-phase validation over the clustered scene (sc.cull): the verdict of
+// cp_validate / validate_waypoints (pure.py:646-699) with far fewer checks.
+// Each lane bounds its waypoint's robot spheres by one box; a chunk of 8
+// primitives is skipped by the whole team unless some lane's robot box
+// overlaps the chunk's bound, and then only the robot spheres that reach the
+// bound test the 8 primitives.  Bounds are conservative (the host rounds them
+// outward with 1e-5 m of slack), so every hit cp_validate finds is found.
+// The early-exit flag is a team vote after each chunk.  Counters: performed =
+// sphere-primitive checks evaluated, gpu_checks = those + bound tests;
+// first_bad = lowest colliding waypoint (not the reference's lockstep order).
+__device__ __forceinline__ unsigned cp_team_or(const Team& tm, unsigned v) {
+    return __reduce_or_sync(tm.mask, v);
+}
+
+__device__ __noinline__ ValOut cp_validate_cull(const Team tm, const float (*seg)[CP_NP], int W, int t_first,
+                                                bool flag_on, float margin, const SceneSm sc) {
+    const int t = (int)tm.lane;
+    const bool mine = t >= t_first && t < W;
+    float4 sp[CP_S > 0 ? CP_S : 1];
+    float4 rc, rh;   // robot box of my waypoint (centre / half extent)
+    {
+        float q[CP_N];
+#pragma unroll
+        for (int k = 0; k < CP_N; k++) q[k] = mine ? seg[t][k] : 0.f;
+        float R[CP_N * 9], P[CP_N * 3], AX[CP_N * 3], OR[CP_N * 3], SPH[(CP_S > 0 ? CP_S : 1) * 3];
+        cp_fk<float>(q, R, P, AX, OR, SPH);
+        float lx = cp_inf(), ly = cp_inf(), lz = cp_inf(), hx = -cp_inf(), hy = -cp_inf(), hz = -cp_inf();
+#pragma unroll
+        for (int s = 0; s < CP_S; s++) {
+            const float r = cp_rad_tab[s] + margin;
+            sp[s] = make_float4(SPH[3 * s], SPH[3 * s + 1], SPH[3 * s + 2], r);
+            lx = fminf(lx, SPH[3 * s] - r); hx = fmaxf(hx, SPH[3 * s] + r);
+            ly = fminf(ly, SPH[3 * s + 1] - r); hy = fmaxf(hy, SPH[3 * s + 1] + r);
+            lz = fminf(lz, SPH[3 * s + 2] - r); hz = fmaxf(hz, SPH[3 * s + 2] + r);
+        }
+        rc = make_float4(0.5f * (lx + hx), 0.5f * (ly + hy), 0.5f * (lz + hz), 0.f);
+        // idle lanes get an empty box (never overlaps)
+        rh = mine ? make_float4(0.5f * (hx - lx) + 1e-5f, 0.5f * (hy - ly) + 1e-5f, 0.5f * (hz - lz) + 1e-5f, 0.f)
+                  : make_float4(-1e30f, -1e30f, -1e30f, 0.f);
+    }
+    bool hit = false, stop = false;
+    i64 narrow = 0, bound = 0;
+    const float4* cl = sc.cl;
+#pragma unroll 1
+    for (int k = 0; k < sc.nbc && !stop; k++) {
+        const float4* ch = cl + CP_BCH * k;
+        const float4 bc = cp_lds4(ch), bh = cp_lds4(ch + 1);
+        const bool ov = fabsf(rc.x - bc.x) <= rh.x + bh.x && fabsf(rc.y - bc.y) <= rh.y + bh.y &&
+                        fabsf(rc.z - bc.z) <= rh.z + bh.z;
+        if (!tm.any(ov)) continue;
+        unsigned m[(CP_S + 31) / 32 > 0 ? (CP_S + 31) / 32 : 1] = {};
+        if (ov) {
+#pragma unroll
+            for (int s = 0; s < CP_S; s++)
+                if (cp_hit_box(sp[s].x, sp[s].y, sp[s].z, sp[s].w * sp[s].w, bc, bh)) m[s >> 5] |= 1u << (s & 31);
+            bound += CP_S;
+        }
+#pragma unroll
+        for (int w = 0; w < (CP_S + 31) / 32; w++) {
+            unsigned um = cp_team_or(tm, m[w]);
+#pragma unroll 1
+            while (um) {
+                const int s = 32 * w + __ffs(um) - 1;
+                um &= um - 1;
+                const float4 c = sp[s];
+                const float r2 = c.w * c.w;
+                bool any = false;
+#pragma unroll
+                for (int j = 0; j < CP_CHUNK; j++)
+                    any |= cp_hit_box(c.x, c.y, c.z, r2, cp_lds4(ch + 2 + j), cp_lds4(ch + 2 + CP_CHUNK + j));
+                if ((m[w] >> (s & 31)) & 1u) { hit |= any; narrow += CP_CHUNK; }
+            }
+        }
+        if (flag_on && tm.any(hit)) stop = true;   // the shared collision flag
+    }
+    const float4* cs = cl + CP_BCH * sc.nbc;
+#pragma unroll 1
+    for (int k = 0; k < sc.nec && !stop; k++) {
+        const float4* ch = cs + CP_SCH * k;
+        const float4 bc = cp_lds4(ch), bh = cp_lds4(ch + 1);
+        const bool ov = fabsf(rc.x - bc.x) <= rh.x + bh.x && fabsf(rc.y - bc.y) <= rh.y + bh.y &&
+                        fabsf(rc.z - bc.z) <= rh.z + bh.z;
+        if (!tm.any(ov)) continue;
+        unsigned m[(CP_S + 31) / 32 > 0 ? (CP_S + 31) / 32 : 1] = {};
+        if (ov) {
+#pragma unroll
+            for (int s = 0; s < CP_S; s++)
+                if (cp_hit_box(sp[s].x, sp[s].y, sp[s].z, sp[s].w * sp[s].w, bc, bh)) m[s >> 5] |= 1u << (s & 31);
+            bound += CP_S;
+        }
+#pragma unroll
+        for (int w = 0; w < (CP_S + 31) / 32; w++) {
+            unsigned um = cp_team_or(tm, m[w]);
+#pragma unroll 1
+            while (um) {
+                const int s = 32 * w + __ffs(um) - 1;
+                um &= um - 1;
+                const float4 c = sp[s];
+                bool any = false;
+#pragma unroll
+                for (int j = 0; j < CP_CHUNK; j++) any |= cp_hit_sph(c.x, c.y, c.z, c.w, cp_lds4(ch + 2 + j));
+                if ((m[w] >> (s & 31)) & 1u) { hit |= any; narrow += CP_CHUNK; }
+            }
+        }
+        if (flag_on && tm.any(hit)) stop = true;
+    }
+    if (!stop && CP_P > 0) {
+#pragma unroll 1
+        for (int k = 0; k < CP_P; k++) {
+            const float4 pa = sp[cp_pair_tab[2 * k]], pb = sp[cp_pair_tab[2 * k + 1]];
+            const float rr = pa.w + pb.w;
+            float dx = pa.x - pb.x, dy = pa.y - pb.y, dz = pa.z - pb.z;
+            hit |= mine && fmaf(dx, dx, fmaf(dy, dy, dz * dz)) < rr * rr;
+        }
+        if (mine) narrow += CP_P;
+    }
+    ValOut o;
+    int key = hit ? t : CP_INTMAX, idx = t;
+    tm.argmin_i(key, idx);
+    o.valid = key == CP_INTMAX;
+    o.first_bad = o.valid ? -1 : key;
+    i64 nsum = narrow + bound;
+    // team totals (lane sums; i64 as two halves)
+    unsigned lo = (unsigned)narrow, lo2 = (unsigned)nsum;
+    o.performed = (i64)__reduce_add_sync(tm.mask, lo);
+    o.gpu_checks = (i64)__reduce_add_sync(tm.mask, lo2);
+    o.fk_evals = W - t_first;
+    return o;
+}
+
 // ---------------------------------------------------------------------------
 // nearest neighbour: coalesced float4 SoA scan + team argmin (planner.py:198-201)
 // nodes: coordinate d of node i at nodes[d * cap + i]; never-written slots are
@@ -770,7 +902,8 @@ __device__ __forceinline__ bool cp_should_stop(const Team& tm, QueryState& Q, co
 // validate with stats accumulation; waypoint 0 (an existing tree node) skipped
 __device__ __forceinline__ bool cp_check_motion(const Team& tm, TeamWS& ws, const PlanArgs& A,
                                                 const SceneSm& sc, Stats& st) {
-    ValOut v = cp_validate(tm, ws.seg, A.W, 1, A.flag_on, A.margin, sc);
+    ValOut v = sc.cull ? cp_validate_cull(tm, ws.seg, A.W, 1, A.flag_on, A.margin, sc)
+                       : cp_validate(tm, ws.seg, A.W, 1, A.flag_on, A.margin, sc);
     st.v[ST_CCPERF] += v.performed;     // reference (lockstep) semantics, pure.py:664-698
     st.v[ST_CCPOSS] += (u64)((i64)CP_S * (sc.nb + sc.ne) + CP_P) * (A.W - 1);
     st.v[ST_GPUCHK] += v.gpu_checks;
@@ -949,11 +1082,22 @@ __device__ void cp_plan_query(const Team& tm, TeamWS& ws, const PlanArgs& A, con
 }
 
 __host__ __device__ __forceinline__ int cp_pad8(int x) { return (x + CP_CHUNK - 1) / CP_CHUNK * CP_CHUNK; }
-__device__ __forceinline__ int cp_scene_f4(const SceneSm& g) { return 2 * cp_pad8(g.nb) + cp_pad8(g.ne); }
+__device__ __forceinline__ int cp_scene_f4(const SceneSm& g) {
+    return g.cull ? CP_BCH * g.nbc + CP_SCH * g.nec : 2 * cp_pad8(g.nb) + cp_pad8(g.ne);
+}
 
-// Stage the scene into shared memory, padded to whole CP_CHUNKs with
-// primitives 1e18 m away (never hit), so the check loop has no bounds test.
+// Stage the scene into shared memory.  Reference order: padded to whole
+// CP_CHUNKs with primitives 1e18 m away (never hit), so the check loop has no
+// bounds test.  Clustered: one contiguous copy (the host padded the chunks).
 __device__ __forceinline__ SceneSm cp_stage_scene(const SceneSm& g, float4* sm) {
+    SceneSm s = g;
+    if (g.cull) {
+        const int tot = CP_BCH * g.nbc + CP_SCH * g.nec;
+        for (int i = threadIdx.x; i < tot; i += blockDim.x) sm[i] = g.cl[i];
+        __syncthreads();
+        s.cl = sm;
+        return s;
+    }
     const int nbp = cp_pad8(g.nb), nep = cp_pad8(g.ne);
     float4* bc = sm;
     float4* bh = sm + nbp;
@@ -966,8 +1110,7 @@ __device__ __forceinline__ SceneSm cp_stage_scene(const SceneSm& g, float4* sm) 
     }
     for (int i = threadIdx.x; i < nep; i += blockDim.x) sp[i] = i < g.ne ? g.sph[i] : far;
     __syncthreads();
-    SceneSm s;
-    s.box_c = bc; s.box_h = bh; s.sph = sp; s.nb = g.nb; s.ne = g.ne;
+    s.box_c = bc; s.box_h = bh; s.sph = sp;
     return s;
 }
 
@@ -1311,12 +1454,16 @@ extern "C" __global__ void cp_check_config_kernel(int B, const __grid_constant__
     if ((threadIdx.x & 31) == 0) code[i] = c;
 }
 
-// Batch motion validation with reference semantics (exact counters).
-// One team per motion; wps (B, W, CP_N) FP64 in, scene staged in smem.
-extern "C" __global__ void __launch_bounds__(CP_NTHREADS, 1)
-cp_validate_kernel(int B, int W, int flag_on, float margin, SceneSm scg, const double* wps, int* valid,
-                   int* first_bad, i64* performed, i64* gpu_checks) {
+// Batch motion validation with reference semantics (exact counters), or
+// (CULL) through the clustered broad phase.  One team per motion; wps
+// (B, W, CP_N) FP64 in, scene staged in smem.  Two kernels so that each keeps
+// its own register allocation.
+template <bool CULL>
+__device__ __forceinline__ void cp_validate_batch(int B, int W, int flag_on, float margin, SceneSm scg,
+                                                  const double* wps, int* valid, int* first_bad,
+                                                  i64* performed, i64* gpu_checks) {
     extern __shared__ float4 cp_smem[];
+    scg.cull = CULL ? 1 : 0;   // compile-time layout
     SceneSm sc = cp_stage_scene(scg, cp_smem);
     TeamWS* wsa = reinterpret_cast<TeamWS*>(cp_smem + cp_scene_f4(scg));
     Team tm;
@@ -1328,7 +1475,8 @@ cp_validate_kernel(int B, int W, int flag_on, float margin, SceneSm scg, const d
         if ((int)tm.lane < W)
             for (int k = 0; k < CP_N; k++) ws.seg[tm.lane][k] = (float)wps[((size_t)i * W + tm.lane) * CP_N + k];
         tm.sync();
-        ValOut o = cp_validate(tm, ws.seg, W, 0, flag_on != 0, margin, sc);
+        ValOut o = CULL ? cp_validate_cull(tm, ws.seg, W, 0, flag_on != 0, margin, sc)
+                        : cp_validate(tm, ws.seg, W, 0, flag_on != 0, margin, sc);
         if (tm.lane == 0) {
             valid[i] = o.valid;
             first_bad[i] = o.first_bad;
@@ -1336,6 +1484,16 @@ cp_validate_kernel(int B, int W, int flag_on, float margin, SceneSm scg, const d
             if (gpu_checks) gpu_checks[i] = o.gpu_checks;
         }
     }
+}
+extern "C" __global__ void __launch_bounds__(CP_NTHREADS, 1)
+cp_validate_kernel(int B, int W, int flag_on, float margin, SceneSm scg, const double* wps, int* valid,
+                   int* first_bad, i64* performed, i64* gpu_checks) {
+    cp_validate_batch<false>(B, W, flag_on, margin, scg, wps, valid, first_bad, performed, gpu_checks);
+}
+extern "C" __global__ void __launch_bounds__(CP_NTHREADS, 1)
+cp_validate_cull_kernel(int B, int W, int flag_on, float margin, SceneSm scg, const double* wps, int* valid,
+                        int* first_bad, i64* performed, i64* gpu_checks) {
+    cp_validate_batch<true>(B, W, flag_on, margin, scg, wps, valid, first_bad, performed, gpu_checks);
 }
 
 // Batch segment projection (parallel / literal-gap / sequential), FP32.

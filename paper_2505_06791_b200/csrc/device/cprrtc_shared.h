@@ -27,12 +27,23 @@ struct ProjArgs {
     int mode;             // 0 parallel, 1 literal-gap, 2 sequential ("naive")
 };
 
-// scene: boxes as centre / half extent, spheres as centre + radius (FP32)
+// scene: boxes as centre / half extent, spheres as centre + radius (FP32).
+// Two device layouts of the same primitives:
+//  * reference order (box_c / box_h / sph): the lockstep check order of
+//    pure.py:674-693, exact reference counters;
+//  * clustered (cl, cull = 1): primitives Morton-sorted into chunks of 8, each
+//    chunk led by a conservative bounding box -- box chunk k is float4
+//    [bound c, bound h, 8 box c, 8 box h] at cl + 18k, sphere chunk k is
+//    [bound c, bound h, 8 spheres] at cl + 18 nbc + 10k (broad phase).
 struct SceneSm {
     const float4* box_c;
     const float4* box_h;
     const float4* sph;
     int nb, ne;
+    const float4* cl;
+    int nbc, nec;      // box / sphere chunks of the clustered layout
+    int cull;          // 1: stage and check the clustered layout
+    int pad_;
 };
 
 // stats / work-unit counters (the last four feed the roofline in bench.py)

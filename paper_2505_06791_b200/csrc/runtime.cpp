@@ -15,7 +15,9 @@
 #include <sys/stat.h>
 #include <unistd.h>
 
+#include <algorithm>
 #include <cmath>
+#include <cstdint>
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
@@ -298,6 +300,8 @@ struct Ctx {
     // scene
     int nb = 0, ne = 0;
     DevBuf sc_box_c, sc_box_h, sc_sph, sc_bmin, sc_bmax, sc_sc, sc_sr;
+    DevBuf sc_cl;          // clustered layout (broad phase), see SceneSm
+    int nbc = 0, nec = 0;
     // constraint
     int kind = 0, orient = 0;
     Con<float> conf{};
@@ -348,8 +352,8 @@ const std::vector<const char*> kPlanKernels = {"cp_plan_kernel", "cp_setup_kerne
 const std::vector<const char*> kParityKernels = {"cp_fk_kernel",           "cp_tej_kernel",
                                                   "cp_err_at_kernel",       "cp_project_config_kernel",
                                                   "cp_check_config_kernel", "cp_validate_kernel",
-                                                  "cp_project_kernel",      "cp_nearest_kernel",
-                                                  "cp_halton_kernel"};
+                                                  "cp_validate_cull_kernel", "cp_project_kernel",
+                                                  "cp_nearest_kernel",      "cp_halton_kernel"};
 
 std::string module_name(int G, int kind, int orient, int parity) {
     char name[64];
@@ -388,7 +392,8 @@ int get_module(Ctx* c, int G, int kind, int orient, int parity, Module** out) {
     m->kind = kind;
     m->orient = orient;
     m->ws_bytes = (size_t)(G + 7) * c->NP * sizeof(float);
-    for (const char* k : {"cp_plan_kernel", "cp_validate_kernel", "cp_project_kernel", "cp_dense_kernel"})
+    for (const char* k : {"cp_plan_kernel", "cp_validate_kernel", "cp_validate_cull_kernel", "cp_project_kernel",
+                          "cp_dense_kernel", "cp_step_kernel"})
         if (m->fn.count(k)) drv().funcSetAttribute(m->fn[k], CU_FUNC_ATTRIBUTE_MAX_DYNAMIC_SHARED_SIZE_BYTES, 200 * 1024);
     *out = m.get();
     c->modules[key] = std::move(m);
@@ -434,22 +439,121 @@ template <class T> int download(Ctx* c, T* dst, const DevBuf& b, size_t count) {
     return 0;
 }
 
-SceneSm scene_args(Ctx* c) {
+SceneSm scene_args(Ctx* c, int cull = 0) {
     SceneSm s;
+    std::memset(&s, 0, sizeof s);
     s.box_c = c->sc_box_c.as<float4>();
     s.box_h = c->sc_box_h.as<float4>();
     s.sph = c->sc_sph.as<float4>();
     s.nb = c->nb;
     s.ne = c->ne;
+    s.cl = c->sc_cl.as<float4>();
+    s.nbc = c->nbc;
+    s.nec = c->nec;
+    s.cull = cull ? 1 : 0;
     return s;
 }
 
 int pad8(int x) { return (x + 7) / 8 * 8; }
 
-size_t scene_smem(Ctx* c) { return (size_t)(2 * pad8(c->nb) + pad8(c->ne)) * sizeof(float4); }
+// float4s staged per CTA (cp_scene_f4 in the device code)
+size_t scene_f4(int nb, int ne, int nbc, int nec, int cull) {
+    return cull ? (size_t)(18 * nbc + 10 * nec) : (size_t)(2 * pad8(nb) + pad8(ne));
+}
+size_t scene_smem(Ctx* c, int cull = 0) { return scene_f4(c->nb, c->ne, c->nbc, c->nec, cull) * sizeof(float4); }
+
+// Clustered scene (broad phase): primitives sorted along a 30-bit Morton
+// curve of their centres, cut into chunks of 8, each chunk led by a bounding
+// box rounded outward (FP64 -> FP32 with 1e-5 m + 1e-6 relative slack) so the
+// FP32 chunk test can never reject a primitive the FP32 narrow test would hit.
+static void build_clusters(const cprrtc_scene* s, std::vector<float4>& out, int& nbc, int& nec) {
+    const int nb = s->n_boxes, ne = s->n_spheres;
+    double lo[3] = {INFINITY, INFINITY, INFINITY}, hi[3] = {-INFINITY, -INFINITY, -INFINITY};
+    auto centre = [&](int kind, int i, int a) {
+        return kind == 0 ? 0.5 * (s->box_min[3 * i + a] + s->box_max[3 * i + a]) : s->sph_center[3 * i + a];
+    };
+    for (int kind = 0; kind < 2; kind++)
+        for (int i = 0; i < (kind ? ne : nb); i++)
+            for (int a = 0; a < 3; a++) {
+                lo[a] = std::min(lo[a], centre(kind, i, a));
+                hi[a] = std::max(hi[a], centre(kind, i, a));
+            }
+    auto spread = [](uint32_t v) {   // 10 bits -> every third bit
+        uint64_t x = v & 1023u;
+        x = (x | (x << 16)) & 0x030000FFull;
+        x = (x | (x << 8)) & 0x0300F00Full;
+        x = (x | (x << 4)) & 0x030C30C3ull;
+        x = (x | (x << 2)) & 0x09249249ull;
+        return x;
+    };
+    auto morton = [&](int kind, int i) {
+        uint64_t code = 0;
+        for (int a = 0; a < 3; a++) {
+            double ext = hi[a] - lo[a];
+            double u = ext > 0 ? (centre(kind, i, a) - lo[a]) / ext : 0.0;
+            uint32_t v = (uint32_t)std::min(1023.0, std::max(0.0, u * 1023.0));
+            code |= spread(v) << a;
+        }
+        return code;
+    };
+    auto bound = [](const double* blo, const double* bhi, float4& c, float4& h) {
+        float cc[3], hh[3];
+        for (int a = 0; a < 3; a++) {
+            double cd = 0.5 * (blo[a] + bhi[a]), hd = 0.5 * (bhi[a] - blo[a]);
+            cc[a] = (float)cd;
+            hh[a] = (float)((hd + std::fabs(cd - (double)cc[a])) * (1.0 + 1e-6) + 1e-5);
+        }
+        c = make_float4(cc[0], cc[1], cc[2], 0.f);
+        h = make_float4(hh[0], hh[1], hh[2], 0.f);
+    };
+    const float4 far = make_float4(1e18f, 1e18f, 1e18f, 0.f);
+    const float4 zero = make_float4(0.f, 0.f, 0.f, 0.f);
+    out.clear();
+    for (int kind = 0; kind < 2; kind++) {
+        const int n = kind ? ne : nb;
+        std::vector<std::pair<uint64_t, int>> ord(n);
+        for (int i = 0; i < n; i++) ord[i] = {morton(kind, i), i};
+        std::sort(ord.begin(), ord.end());
+        const int chunks = (n + 7) / 8;
+        for (int k = 0; k < chunks; k++) {
+            double blo[3] = {INFINITY, INFINITY, INFINITY}, bhi[3] = {-INFINITY, -INFINITY, -INFINITY};
+            std::vector<float4> a(8), b(8);
+            for (int j = 0; j < 8; j++) {
+                const int o = 8 * k + j;
+                if (o >= n) { a[j] = far; b[j] = zero; continue; }
+                const int i = ord[o].second;
+                for (int d = 0; d < 3; d++) {
+                    double l = kind ? s->sph_center[3 * i + d] - s->sph_radius[i] : s->box_min[3 * i + d];
+                    double u = kind ? s->sph_center[3 * i + d] + s->sph_radius[i] : s->box_max[3 * i + d];
+                    blo[d] = std::min(blo[d], l);
+                    bhi[d] = std::max(bhi[d], u);
+                }
+                if (kind == 0) {
+                    const double* l = s->box_min + 3 * i;
+                    const double* u = s->box_max + 3 * i;
+                    a[j] = make_float4((float)(0.5 * (l[0] + u[0])), (float)(0.5 * (l[1] + u[1])),
+                                       (float)(0.5 * (l[2] + u[2])), 0.f);
+                    b[j] = make_float4((float)(0.5 * (u[0] - l[0])), (float)(0.5 * (u[1] - l[1])),
+                                       (float)(0.5 * (u[2] - l[2])), 0.f);
+                } else {
+                    a[j] = make_float4((float)s->sph_center[3 * i], (float)s->sph_center[3 * i + 1],
+                                       (float)s->sph_center[3 * i + 2], (float)s->sph_radius[i]);
+                }
+            }
+            float4 c, h;
+            bound(blo, bhi, c, h);
+            out.push_back(c);
+            out.push_back(h);
+            for (int j = 0; j < 8; j++) out.push_back(a[j]);
+            if (kind == 0)
+                for (int j = 0; j < 8; j++) out.push_back(b[j]);
+        }
+        (kind ? nec : nbc) = chunks;
+    }
+}
 
 size_t team_smem(Ctx* c, Module* m, bool with_scene) {
-    size_t sc = with_scene ? scene_smem(c) : 0;
+    size_t sc = with_scene ? std::max(scene_smem(c, 0), scene_smem(c, 1)) : 0;
     return sc + (size_t)(kThreads / m->G) * m->ws_bytes;
 }
 
@@ -582,7 +686,7 @@ int cprrtc_set_scene(void* p, const cprrtc_scene* s) {
     Ctx* c = C(p);
     if (!c || !s) return fail(CPRRTC_EARG, "NULL argument");
     if (s->n_boxes < 0 || s->n_spheres < 0) return fail(CPRRTC_EARG, "negative primitive count");
-    if ((size_t)(2 * s->n_boxes + s->n_spheres) * 16 > 160 * 1024)
+    if (scene_f4(s->n_boxes, s->n_spheres, (s->n_boxes + 7) / 8, (s->n_spheres + 7) / 8, 1) * 16 > 180 * 1024)
         return fail(CPRRTC_ELIMIT, "scene exceeds the shared-memory staging capacity (~5000 boxes)");
     if (int rc = set_device(c)) return rc;
     std::vector<float4> bc(s->n_boxes), bh(s->n_boxes), sp(s->n_spheres);
@@ -604,9 +708,15 @@ int cprrtc_set_scene(void* p, const cprrtc_scene* s) {
     rc = rc ? rc : upload(c, c->sc_bmax, s->box_max, 3 * (size_t)s->n_boxes);
     rc = rc ? rc : upload(c, c->sc_sc, s->sph_center, 3 * (size_t)s->n_spheres);
     rc = rc ? rc : upload(c, c->sc_sr, s->sph_radius, (size_t)s->n_spheres);
+    int nbc = 0, nec = 0;
+    std::vector<float4> cl;
+    build_clusters(s, cl, nbc, nec);
+    rc = rc ? rc : upload(c, c->sc_cl, cl.data(), cl.size());
     if (rc) return rc;
     c->nb = s->n_boxes;
     c->ne = s->n_spheres;
+    c->nbc = nbc;
+    c->nec = nec;
     return sync(c);
 }
 
@@ -800,8 +910,9 @@ int cprrtc_check_config(void* p, int B, const double* q, double tau, int32_t* co
     return sync(c);
 }
 
-int cprrtc_validate(void* p, int B, int W, const double* wps, int flag_on, double margin, int32_t* valid,
-                    int32_t* first_bad, int64_t* performed, int64_t* possible, int64_t* gpu_checks) {
+static int validate_impl(void* p, int B, int W, const double* wps, int flag_on, double margin, int cull,
+                         int32_t* valid, int32_t* first_bad, int64_t* performed, int64_t* possible,
+                         int64_t* gpu_checks) {
     Ctx* c = C(p);
     if (!c || B < 0 || W < 1 || (B && (!wps || !valid || !first_bad || !performed)))
         return fail(CPRRTC_EARG, "bad argument");
@@ -816,7 +927,7 @@ int cprrtc_validate(void* p, int B, int W, const double* wps, int flag_on, doubl
     rc = rc ? rc : c->scratch[3].ensure((size_t)B * 8);
     rc = rc ? rc : c->scratch[4].ensure((size_t)B * 8);
     if (rc) return rc;
-    SceneSm sc = scene_args(c);
+    SceneSm sc = scene_args(c, cull);
     const double* dw = c->scratch[0].as<double>();
     int* dv = c->scratch[1].as<int>();
     int* df = c->scratch[2].as<int>();
@@ -828,7 +939,9 @@ int cprrtc_validate(void* p, int B, int W, const double* wps, int flag_on, doubl
     int grid = (B + tpc - 1) / tpc;
     if (grid > 64 * c->sms) grid = 64 * c->sms;
     CUDA_TRY(cudaEventRecord(c->ev[1], c->stream));
-    if (int rc2 = launch(c, m, "cp_validate_kernel", grid, 1, kThreads, team_smem(c, m, true), args)) return rc2;
+    if (int rc2 = launch(c, m, cull ? "cp_validate_cull_kernel" : "cp_validate_kernel", grid, 1, kThreads,
+                         team_smem(c, m, true), args))
+        return rc2;
     CUDA_TRY(cudaEventRecord(c->ev[2], c->stream));
     download(c, valid, c->scratch[1], (size_t)B);
     download(c, first_bad, c->scratch[2], (size_t)B);
@@ -846,6 +959,17 @@ int cprrtc_validate(void* p, int B, int W, const double* wps, int flag_on, doubl
         for (int i = 0; i < B; i++) possible[i] = per * W;
     }
     return 0;
+}
+
+int cprrtc_validate(void* p, int B, int W, const double* wps, int flag_on, double margin, int32_t* valid,
+                    int32_t* first_bad, int64_t* performed, int64_t* possible, int64_t* gpu_checks) {
+    return validate_impl(p, B, W, wps, flag_on, margin, 0, valid, first_bad, performed, possible, gpu_checks);
+}
+
+int cprrtc_validate_broadphase(void* p, int B, int W, const double* wps, int flag_on, double margin,
+                               int32_t* valid, int32_t* first_bad, int64_t* performed, int64_t* possible,
+                               int64_t* gpu_checks) {
+    return validate_impl(p, B, W, wps, flag_on, margin, 1, valid, first_bad, performed, possible, gpu_checks);
 }
 
 int cprrtc_project(void* p, int B, int W, const double* wps, const double* tau_sm, double tau_task, double alpha,
@@ -1042,7 +1166,8 @@ static PlanArgs make_plan_args(Ctx* c, const cprrtc_params* prm, int B, int cap,
     A.nq = B;
     A.queue_head = c->counters.as<int>();
     A.team_counter = c->counters.as<int>() + 1;
-    A.scene_g = scene_args(c);
+    // broad phase: explicit, or (-1) from 32 obstacle primitives up
+    A.scene_g = scene_args(c, prm->cc_broadphase < 0 ? (c->nb + c->ne >= 32) : prm->cc_broadphase != 0);
     A.con = c->conf;
     A.pa.alpha = (float)prm->alpha;
     A.pa.lam = (float)prm->lam;
@@ -1133,7 +1258,7 @@ int cprrtc_plan(void* p, const cprrtc_params* prm, int B, const double* starts, 
     const int block = (int)(per_cta * 32 / tpw);
     int grid = (int)((want_teams + per_cta - 1) / per_cta);
     if (grid < 1) grid = 1;
-    const size_t smem = scene_smem(c) + (size_t)(block / m->G) * m->ws_bytes;
+    const size_t smem = scene_smem(c, A.scene_g.cull) + (size_t)(block / m->G) * m->ws_bytes;
     A.solo = solo ? 1 : 0;
     if (int rc = upload_conf(c, m)) return rc;
     // the per-call sequence as one CUDA graph, replayed while shapes and
@@ -1280,7 +1405,7 @@ int cprrtc_step(void* p, const cprrtc_params* prm, int op, int N, const double* 
     int* dout = c->scratch[1].as<int>();
     unsigned long long* dst = c->scratch[2].as<unsigned long long>();
     void* args[] = {&A, &op, &zero, &dq, &dout, &dst};
-    if (int rc2 = launch(c, m, "cp_step_kernel", 1, 1, 32, scene_smem(c) + m->ws_bytes, args)) return rc2;
+    if (int rc2 = launch(c, m, "cp_step_kernel", 1, 1, 32, scene_smem(c, A.scene_g.cull) + m->ws_bytes, args)) return rc2;
     int out[3];
     unsigned long long st[CPRRTC_ST_COUNT];
     download(c, out, c->scratch[1], 3);

@@ -274,8 +274,12 @@ def clearance_batch(spheres, others, kind: str = "box", device: int = 0):
     return out
 
 
-def validate_batch(model, scene, wps, flag_on: bool = True, margin: float = 0.0, device: int = 0):
-    """B motions (B, W, n) -> dict(valid, first_bad, performed, possible, gpu_checks)."""
+def validate_batch(model, scene, wps, flag_on: bool = True, margin: float = 0.0, device: int = 0,
+                   broadphase: bool = False):
+    """B motions (B, W, n) -> dict(valid, first_bad, performed, possible, gpu_checks).
+
+    broadphase=False: the reference's lockstep order with its exact counters;
+    True: the clustered broad phase (same verdicts, its own counters)."""
     ctx = context(model, device)
     wps = _f64(wps)
     if wps.ndim == 2:
@@ -288,7 +292,8 @@ def validate_batch(model, scene, wps, flag_on: bool = True, margin: float = 0.0,
              gpu_checks=np.empty(B, np.int64))
     with ctx.lock:
         ctx.set_scene(_packed_scene(scene))
-        _lib.check(ctx.L.cprrtc_validate(
+        fn = ctx.L.cprrtc_validate_broadphase if broadphase else ctx.L.cprrtc_validate
+        _lib.check(fn(
             ctx.h, B, W, _lib.ptr(wps), int(bool(flag_on)), C.c_double(margin),
             _lib.ptr(r["valid"], _ip), _lib.ptr(r["first_bad"], _ip), _lib.ptr(r["performed"], _lp),
             _lib.ptr(r["possible"], _lp), _lib.ptr(r["gpu_checks"], _lp)), "validate")

@@ -125,6 +125,10 @@ class DeviceOptions:
     cc_margin: float = 1e-5      # planner robot-sphere inflation (m)
     tree_capacity: int = 0       # nodes per tree; 0 = derived from the params
     path_capacity: int = 1024
+    # planner collision checks through the clustered broad phase (same
+    # verdicts; cc_performed then counts the checks evaluated): 1 on, 0 the
+    # reference's lockstep order, -1 auto (on from 32 obstacle primitives)
+    cc_broadphase: int = -1
 
 
 @dataclass(frozen=True)
@@ -284,7 +288,7 @@ def _make_params(p: PlanParams, opt: DeviceOptions) -> _lib.Params:
         flag_on=int(p.flag_mode == "on"), deterministic=int(bool(p.deterministic)),
         max_connect_segments=int(p.max_connect_segments), cc_margin=float(opt.cc_margin),
         teams=int(opt.teams), tree_capacity=int(opt.tree_capacity),
-        path_capacity=int(opt.path_capacity))
+        path_capacity=int(opt.path_capacity), cc_broadphase=int(opt.cc_broadphase))
 
 
 def _bind(problem_like, opt: DeviceOptions):
