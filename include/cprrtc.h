@@ -107,7 +107,7 @@ typedef struct {
                                 (cprrtc_validate_broadphase; same verdicts, the
                                 cc_performed stat then counts evaluated checks);
                                 0: the reference's lockstep check order;
-                                -1: on from 32 obstacle primitives */
+                                -1: on whenever the scene has obstacles */
 } cprrtc_params;
 
 /* stats[] layout of cprrtc_result (PlanStats, planner.py:130-141) */

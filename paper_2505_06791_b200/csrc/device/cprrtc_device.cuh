@@ -98,6 +98,20 @@ struct Team {
 // constraint (packed layout of maniplan/constraints.py:123-176)
 // ---------------------------------------------------------------------------
 
+// Division traits.  FP64 (parity / setup paths) keeps the reference's exact
+// operations; FP32 (planner) divides by a diagonal / pivot through one
+// reciprocal (MUFU) and multiplies.
+template <class T> struct CpDiv {
+    static __device__ __forceinline__ T piv(T x) { return x; }           // stored pivot
+    static __device__ __forceinline__ T div(T a, T p) { return a / p; }  // a / pivot
+    static __device__ __forceinline__ T sqrt_piv(T x) { return sqrt(x); }
+};
+template <> struct CpDiv<float> {
+    static __device__ __forceinline__ float piv(float x) { return __frcp_rn(x); }
+    static __device__ __forceinline__ float div(float a, float p) { return a * p; }
+    static __device__ __forceinline__ float sqrt_piv(float x) { return rsqrtf(x); }
+};
+
 // rotation -> quaternion, w >= 0 (maniplan/_kernels/pure.py:130-159)
 template <class T>
 __device__ __forceinline__ void cp_quat(const T* r, T* q) {
@@ -105,19 +119,51 @@ __device__ __forceinline__ void cp_quat(const T* r, T* q) {
     T tr = (r[0] + r[4]) + r[8];
     if (tr > T(0)) {
         s = sqrt(tr + T(1)) * T(2);
-        w = T(0.25) * s; x = (r[7] - r[5]) / s; y = (r[2] - r[6]) / s; z = (r[3] - r[1]) / s;
+        const T is = CpDiv<T>::piv(s);
+        w = T(0.25) * s; x = CpDiv<T>::div(r[7] - r[5], is); y = CpDiv<T>::div(r[2] - r[6], is);
+        z = CpDiv<T>::div(r[3] - r[1], is);
     } else if (r[0] > r[4] && r[0] > r[8]) {
         s = sqrt(((T(1) + r[0]) - r[4]) - r[8]) * T(2);
-        w = (r[7] - r[5]) / s; x = T(0.25) * s; y = (r[1] + r[3]) / s; z = (r[2] + r[6]) / s;
+        const T is = CpDiv<T>::piv(s);
+        w = CpDiv<T>::div(r[7] - r[5], is); x = T(0.25) * s; y = CpDiv<T>::div(r[1] + r[3], is);
+        z = CpDiv<T>::div(r[2] + r[6], is);
     } else if (r[4] > r[8]) {
         s = sqrt(((T(1) + r[4]) - r[0]) - r[8]) * T(2);
-        w = (r[2] - r[6]) / s; x = (r[1] + r[3]) / s; y = T(0.25) * s; z = (r[5] + r[7]) / s;
+        const T is = CpDiv<T>::piv(s);
+        w = CpDiv<T>::div(r[2] - r[6], is); x = CpDiv<T>::div(r[1] + r[3], is); y = T(0.25) * s;
+        z = CpDiv<T>::div(r[5] + r[7], is);
     } else {
         s = sqrt(((T(1) + r[8]) - r[0]) - r[4]) * T(2);
-        w = (r[3] - r[1]) / s; x = (r[2] + r[6]) / s; y = (r[5] + r[7]) / s; z = T(0.25) * s;
+        const T is = CpDiv<T>::piv(s);
+        w = CpDiv<T>::div(r[3] - r[1], is); x = CpDiv<T>::div(r[2] + r[6], is);
+        y = CpDiv<T>::div(r[5] + r[7], is); z = T(0.25) * s;
     }
     if (w < T(0)) { w = -w; x = -x; y = -y; z = -z; }
     q[0] = w; q[1] = x; q[2] = y; q[3] = z;
+}
+
+// rotation-vector scale k = 2 atan2(vn, rw) / vn of a unit quaternion with
+// rw, vn >= 0 (pure.py:338-344).  FP32: atan(x)/x on x in [0, 1] as a
+// degree-8 polynomial in x^2 (max relative error 9e-8, fitted for this file),
+// with the reflection atan(x) = pi/2 - atan(1/x) above 1.
+template <class T> __device__ __forceinline__ T cp_rotscale(T vn, T rw) {
+    return vn < T(1e-12) ? T(2) : T(2) * atan2(vn, rw) / vn;
+}
+template <> __device__ __forceinline__ float cp_rotscale<float>(float vn, float rw) {
+    if (vn < 1e-12f) return 2.f;
+    const bool sw = vn > rw;
+    const float x = sw ? __fdividef(rw, vn) : __fdividef(vn, rw);
+    const float u = x * x;
+    float p = 0.0028531861025840044f;
+    p = fmaf(p, u, -0.016082055866718292f);
+    p = fmaf(p, u, 0.042713798582553864f);
+    p = fmaf(p, u, -0.07506226748228073f);
+    p = fmaf(p, u, 0.1064186692237854f);
+    p = fmaf(p, u, -0.14203891158103943f);
+    p = fmaf(p, u, 0.19992651045322418f);
+    p = fmaf(p, u, -0.33333075046539307f);
+    p = fmaf(p, u, 1.0f);
+    return sw ? __fdividef(2.f * fmaf(-x, p, 1.5707963267948966f), vn) : __fdividef(2.f * p, rw);
 }
 
 // q_fixed^-1 * q_ee as a rotation vector k*v (pure.py:328-344)
@@ -131,12 +177,13 @@ __device__ __forceinline__ T cp_relrot(const Con<T>& c, const T* qe, T* v) {
     if (rw < T(0)) { rw = -rw; rx = -rx; ry = -ry; rz = -rz; }
     T vn = sqrt((rx * rx + ry * ry) + rz * rz);
     v[0] = rx; v[1] = ry; v[2] = rz;
-    return vn < T(1e-12) ? T(2) : T(2) * atan2(vn, rw) / vn;
+    return cp_rotscale<T>(vn, rw);
 }
 
-// task error at a pose (pure.py:312-345); writes CP_M rows
+// task error rows at a pose (pure.py:312-345): position rows, then (locked
+// orientation) the weighted rotation vector k*v of q_fixed^-1 q_ee
 template <class T>
-__device__ __forceinline__ void cp_task_err(const Con<T>& c, const T* p, const T* qe, T* e) {
+__device__ __forceinline__ void cp_task_err_kv(const Con<T>& c, const T* p, T k, const T* v, T* e) {
     int m = 0;
 #if CP_KIND == 0
     e[m++] = ((c.anchor[0] * p[0] + c.anchor[1] * p[1]) + c.anchor[2] * p[2]) - c.offset;
@@ -146,26 +193,47 @@ __device__ __forceinline__ void cp_task_err(const Con<T>& c, const T* p, const T
     e[m++] = (c.b2[0] * dx + c.b2[1] * dy) + c.b2[2] * dz;
 #endif
 #if CP_ORIENT
-    T v[3];
-    T k = cp_relrot(c, qe, v);
     e[m++] = c.weight * (k * v[0]);
     e[m++] = c.weight * (k * v[1]);
     e[m++] = c.weight * (k * v[2]);
 #endif
+    (void)k; (void)v;
+}
+template <class T>
+__device__ __forceinline__ void cp_task_err(const Con<T>& c, const T* p, const T* qe, T* e) {
+    T v[3] = {T(0), T(0), T(0)}, k = T(0);
+#if CP_ORIENT
+    k = cp_relrot(c, qe, v);
+#endif
+    cp_task_err_kv<T>(c, p, k, v, e);
     (void)qe;
+}
+
+// c2(theta) = 1/theta^2 - (1 + cos theta) / (2 theta sin theta) of the inverse
+// left Jacobian (pure.py:352-358).  FP32: its Taylor series
+// 1/12 + t/720 + t^2/30240 + t^3/1209600 + t^4/47900160 (t = theta^2) below
+// t = 0.5 (truncation < 2e-11, and no cancellation, unlike the closed form in
+// FP32), else the closed form with the fast sincos.
+template <class T> __device__ __forceinline__ T cp_so3_c2(T t2) {
+    if (t2 < T(1e-8)) return T(1.0 / 12.0) + t2 / T(720);
+    T th = sqrt(t2), s, co;
+    sincos(th, &s, &co);
+    return T(1) / t2 - (T(1) + co) / ((T(2) * th) * s);
+}
+template <> __device__ __forceinline__ float cp_so3_c2<float>(float t2) {
+    if (t2 < 0.5f)
+        return fmaf(t2, fmaf(t2, fmaf(t2, fmaf(t2, 1.f / 47900160.f, 1.f / 1209600.f), 1.f / 30240.f), 1.f / 720.f),
+                    1.f / 12.f);
+    float th = sqrtf(t2), s, co;
+    cp_sincos(th, &s, &co);
+    return __fdividef(1.f, t2) - __fdividef(1.f + co, (2.f * th) * s);
 }
 
 // inverse left Jacobian of SO(3) (pure.py:348-366)
 template <class T>
 __device__ __forceinline__ void cp_so3_rate(T p0, T p1, T p2, T* a) {
-    T c2, t2 = (p0 * p0 + p1 * p1) + p2 * p2;
-    if (t2 < T(1e-8)) {
-        c2 = T(1.0 / 12.0) + t2 / T(720);
-    } else {
-        T th = sqrt(t2), s, co;
-        sincos(th, &s, &co);
-        c2 = T(1) / t2 - (T(1) + co) / ((T(2) * th) * s);
-    }
+    T t2 = (p0 * p0 + p1 * p1) + p2 * p2;
+    T c2 = cp_so3_c2<T>(t2);
     T h0 = T(0.5) * p0, h1 = T(0.5) * p1, h2 = T(0.5) * p2;
     T c01 = c2 * (p0 * p1), c02 = c2 * (p0 * p2), c12 = c2 * (p1 * p2);
     a[0] = T(1) - c2 * (p1 * p1 + p2 * p2); a[1] = h2 + c01; a[2] = c02 - h1;
@@ -181,16 +249,18 @@ __device__ __forceinline__ void cp_err_jac(const Con<T>& c, const T* q, T* e, T 
     const T* pe = P + 3 * CP_EE;
     T qe[4];
     cp_quat<T>(R + 9 * CP_EE, qe);
-    cp_task_err<T>(c, pe, qe, e);
 #if CP_ORIENT
     T v[3], A[9], Mo[9];
-    T k = cp_relrot(c, qe, v);
+    T k = cp_relrot(c, qe, v);    // once: shared by the error rows and the Jacobian
+    cp_task_err_kv<T>(c, pe, k, v, e);
     cp_so3_rate<T>(k * v[0], k * v[1], k * v[2], A);
 #pragma unroll
     for (int i = 0; i < 3; i++)
 #pragma unroll
         for (int j = 0; j < 3; j++)
             Mo[3 * i + j] = c.weight * ((A[3 * i] * c.rft[j] + A[3 * i + 1] * c.rft[3 + j]) + A[3 * i + 2] * c.rft[6 + j]);
+#else
+    cp_task_err<T>(c, pe, qe, e);
 #endif
 #pragma unroll
     for (int j = 0; j < CP_N; j++) {
@@ -238,9 +308,9 @@ __device__ __forceinline__ bool cp_damped(const T (*J)[CP_N], const T* e, T lam,
             for (int k = 0; k < j; k++) acc -= L[i][k] * L[j][k];
             if (i == j) {
                 if (!(acc > T(0))) return false;
-                L[i][i] = sqrt(acc);
+                L[i][i] = CpDiv<T>::sqrt_piv(acc);   // FP32 holds 1 / L_ii
             } else {
-                L[i][j] = acc / L[j][j];
+                L[i][j] = CpDiv<T>::div(acc, L[j][j]);
             }
         }
 #pragma unroll
@@ -248,14 +318,14 @@ __device__ __forceinline__ bool cp_damped(const T (*J)[CP_N], const T* e, T lam,
         T acc = e[i];
 #pragma unroll
         for (int k = 0; k < i; k++) acc -= L[i][k] * y[k];
-        y[i] = acc / L[i][i];
+        y[i] = CpDiv<T>::div(acc, L[i][i]);
     }
 #pragma unroll
     for (int i = M - 1; i >= 0; i--) {
         T acc = y[i];
 #pragma unroll
         for (int k = i + 1; k < M; k++) acc -= L[k][i] * z[k];
-        z[i] = acc / L[i][i];
+        z[i] = CpDiv<T>::div(acc, L[i][i]);
     }
 #pragma unroll
     for (int k = 0; k < CP_N; k++) {
@@ -337,7 +407,7 @@ __device__ __noinline__ bool cp_project(const Team tm, float (*seg)[CP_NP], int 
                            const ProjArgs pa, int* iters_out, int* prog_out,
                            float* trace = nullptr, int* trace_prog = nullptr,
                            unsigned long long* n_stage1 = nullptr) {
-    unsigned long long s1 = 0;
+    unsigned s1 = 0;
     const int t = (int)tm.lane;
     const bool row = t < W;
     float tau_sm = pa.tau_sm_fixed;
@@ -424,7 +494,7 @@ __device__ __noinline__ bool cp_project(const Team tm, float (*seg)[CP_NP], int 
                 if (!tm.any(!cheap)) { valid = act; full_step = false; }
             }
             if (full_step && act) valid = cp_stage1(pa, xt, xp, tau_sm, xn);
-            if (n_stage1 && full_step) s1 += __popc(tm.ballot(act));
+            if (full_step && act) s1++;   // per lane; summed over the team at the end
             unsigned vm = tm.ballot(act && valid) & full;
             int np = prog;
             if (pa.mode == 1) {   // literal-gap: largest valid index (pure.py:560-563)
@@ -510,7 +580,7 @@ __device__ __noinline__ bool cp_project(const Team tm, float (*seg)[CP_NP], int 
     }
     *iters_out = iters;
     *prog_out = prog;
-    if (n_stage1) *n_stage1 += s1;
+    if (n_stage1) *n_stage1 += __reduce_add_sync(tm.mask, s1);
     return ok;
 }
 

@@ -1166,8 +1166,9 @@ static PlanArgs make_plan_args(Ctx* c, const cprrtc_params* prm, int B, int cap,
     A.nq = B;
     A.queue_head = c->counters.as<int>();
     A.team_counter = c->counters.as<int>() + 1;
-    // broad phase: explicit, or (-1) from 32 obstacle primitives up
-    A.scene_g = scene_args(c, prm->cc_broadphase < 0 ? (c->nb + c->ne >= 32) : prm->cc_broadphase != 0);
+    // broad phase: explicit, or (-1) whenever the scene has obstacles (r1 A/B
+    // on upright Panda, 6 primitives: 0.367 vs 0.395 ms median lockstep)
+    A.scene_g = scene_args(c, prm->cc_broadphase < 0 ? (c->nb + c->ne > 0) : prm->cc_broadphase != 0);
     A.con = c->conf;
     A.pa.alpha = (float)prm->alpha;
     A.pa.lam = (float)prm->lam;

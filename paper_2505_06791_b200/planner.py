@@ -127,7 +127,7 @@ class DeviceOptions:
     path_capacity: int = 1024
     # planner collision checks through the clustered broad phase (same
     # verdicts; cc_performed then counts the checks evaluated): 1 on, 0 the
-    # reference's lockstep order, -1 auto (on from 32 obstacle primitives)
+    # reference's lockstep order, -1 auto (on whenever the scene has obstacles)
     cc_broadphase: int = -1
 
 

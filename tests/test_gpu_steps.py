@@ -13,11 +13,13 @@ FP32 = 2e-6
 
 
 def _ctx(model, scene, spec=None, **over):
-    from paper_2505_06791_b200.planner import PlanContext, PlanParams, PlanProblem
+    # the reference's lockstep check order, so cc_performed keeps the
+    # reference's counter semantics (the broad phase counts its own checks)
+    from paper_2505_06791_b200.planner import DeviceOptions, PlanContext, PlanParams, PlanProblem
     params = PlanParams(**{"width": 8, "deterministic": True, **over})
     prob = PlanProblem(model=model, scene=scene, spec=spec, start=np.zeros(model.n),
                        goal=np.zeros(model.n), params=params)
-    return PlanContext.from_problem(prob)
+    return PlanContext.from_problem(prob, DeviceOptions(cc_broadphase=0))
 
 
 def _scenes():
