@@ -107,7 +107,7 @@ template <class T> struct CpDiv {
     static __device__ __forceinline__ T sqrt_piv(T x) { return sqrt(x); }
 };
 template <> struct CpDiv<float> {
-    static __device__ __forceinline__ float piv(float x) { return __frcp_rn(x); }
+    static __device__ __forceinline__ float piv(float x) { return __fdividef(1.f, x); }
     static __device__ __forceinline__ float div(float a, float p) { return a * p; }
     static __device__ __forceinline__ float sqrt_piv(float x) { return rsqrtf(x); }
 };
@@ -337,6 +337,55 @@ __device__ __forceinline__ bool cp_damped(const T (*J)[CP_N], const T* e, T lam,
     return true;
 }
 
+// FP32 planner variant of cp_damped without early returns: a non-positive
+// (or NaN) pivot marks the system singular -- the caller then takes a zero
+// step (pure.py:529-531) -- and the whole solve stays one basic block, so the
+// scheduler can overlap its MUFU latencies with the surrounding code.
+template <int M>
+__device__ __forceinline__ bool cp_damped_f(const float (*J)[CP_N], const float* e, float lam, float* step) {
+    float L[M][M], y[M], z[M];
+    bool ok = true;
+#pragma unroll
+    for (int i = 0; i < M; i++)
+#pragma unroll
+        for (int j = 0; j <= i; j++) {
+            float acc = 0.f;
+#pragma unroll
+            for (int k = 0; k < CP_N; k++) acc = fmaf(J[i][k], J[j][k], acc);
+            if (i == j) acc += lam * lam;
+#pragma unroll
+            for (int k = 0; k < j; k++) acc -= L[i][k] * L[j][k];
+            if (i == j) {
+                ok &= acc > 0.f;
+                L[i][i] = rsqrtf(fmaxf(acc, 1e-30f));   // 1 / L_ii
+            } else {
+                L[i][j] = acc * L[j][j];
+            }
+        }
+#pragma unroll
+    for (int i = 0; i < M; i++) {
+        float acc = e[i];
+#pragma unroll
+        for (int k = 0; k < i; k++) acc -= L[i][k] * y[k];
+        y[i] = acc * L[i][i];
+    }
+#pragma unroll
+    for (int i = M - 1; i >= 0; i--) {
+        float acc = y[i];
+#pragma unroll
+        for (int k = i + 1; k < M; k++) acc -= L[k][i] * z[k];
+        z[i] = acc * L[i][i];
+    }
+#pragma unroll
+    for (int k = 0; k < CP_N; k++) {
+        float acc = 0.f;
+#pragma unroll
+        for (int i = 0; i < M; i++) acc = fmaf(J[i][k], z[i], acc);
+        step[k] = ok ? acc : 0.f;
+    }
+    return ok;
+}
+
 // The FP32 constraint of the module's current call lives in constant memory
 // (written by the runtime before each launch that projects), so the hot loops
 // address it as constant-bank operands instead of through a pointer.
@@ -356,33 +405,27 @@ __device__ __noinline__ void cp_err_jac_f(const Con<float>& c, const float* q, f
 
 // stage 1 of Alg. 1 for one waypoint (pure.py:511-546).  Validity is judged
 // at the pre-update waypoint with the device margins.
+// Branch-free: a non-finite waypoint is frozen (xn = xt, invalid; pure.py:
+// 524-526) by selects after the (NaN-propagating) evaluation.
 __device__ __forceinline__ bool cp_stage1(const ProjArgs& pa, const float* xt,
                                           const float* xp, float tau_sm, float* xn) {
     bool fin = true;
 #pragma unroll
     for (int k = 0; k < CP_N; k++) fin &= cp_finite(xt[k]);
-    if (!fin) {
-#pragma unroll
-        for (int k = 0; k < CP_N; k++) xn[k] = xt[k];
-        return false;
-    }
     float e[CP_M], J[CP_M][CP_N], g[CP_N];
     cp_err_jac<float>(cp_conf, xt, e, J);
     float en2 = 0.f;
 #pragma unroll
-    for (int i = 0; i < CP_M; i++) en2 += e[i] * e[i];
-    if (!cp_damped<float, CP_M>(J, e, pa.lam, g)) {
-#pragma unroll
-        for (int k = 0; k < CP_N; k++) g[k] = 0.f;
-    }
+    for (int i = 0; i < CP_M; i++) en2 = fmaf(e[i], e[i], en2);
+    cp_damped_f<CP_M>(J, e, pa.lam, g);   // singular -> zero step (pure.py:529-531)
     float d[CP_N], s2 = 0.f;
 #pragma unroll
-    for (int k = 0; k < CP_N; k++) { d[k] = xt[k] - xp[k]; s2 += d[k] * d[k]; }
+    for (int k = 0; k < CP_N; k++) { d[k] = xt[k] - xp[k]; s2 = fmaf(d[k], d[k], s2); }
     float gap = sqrtf(s2);
     float exc = fmaxf(gap - tau_sm, 0.f);
 #pragma unroll
-    for (int k = 0; k < CP_N; k++) xn[k] = xt[k] - pa.alpha * (g[k] + d[k] * exc);
-    return gap < tau_sm * 0.99999f && sqrtf(en2) < pa.tau_task_dev;
+    for (int k = 0; k < CP_N; k++) xn[k] = fin ? xt[k] - pa.alpha * (g[k] + d[k] * exc) : xt[k];
+    return fin && gap < tau_sm * 0.99999f && sqrtf(en2) < pa.tau_task_dev;
 }
 
 __device__ __noinline__ float cp_err_norm(const float* q) {
