@@ -286,8 +286,9 @@ def extras(args, local, model, line):
     out = {}
     # -- CC throughput: 999-box shelf, W=16, flag off (every check performed)
     sc = fx.scene("shelf_x111")
-    qs = kernels.halton_batch(model, 2 * 4096, 1, 12345, device=local)
-    B, W = 4096, 16
+    # 16384 motions x 16 waypoints = 8192 warps: several resident waves on 148 SMs
+    B, W = 16384, 16
+    qs = kernels.halton_batch(model, 2 * B, 1, 12345, device=local)
     t = np.linspace(0, 1, W)[None, :, None]
     wps = qs[0::2][:, None, :] * (1 - t) + qs[1::2][:, None, :] * t
     kernels.validate_batch(model, sc, wps[:64], False, device=local)
@@ -315,8 +316,8 @@ def extras(args, local, model, line):
     out["cc_broadphase"] = {"effective_checks_per_s": poss / (bp["kernel_ms"] * 1e-3),
                             "checks_evaluated_frac": float(bp["performed"].sum()) / poss,
                             "kernel_ms": bp["kernel_ms"], "flag": "on",
-                            "kernel": "cp_validate_cull_kernel (999 boxes, 4096 motions x 16)"}
-    out["roofline_cc"] = {"bound": "fp32", "kernel": "cp_validate_kernel (999 boxes, 4096 motions x 16)",
+                            "kernel": f"cp_validate_cull_kernel (999 boxes, {B} motions x {W})"}
+    out["roofline_cc"] = {"bound": "fp32", "kernel": f"cp_validate_kernel (999 boxes, {B} motions x {W})",
                           "achieved": cc_flops / s_off / 1e12, "peak": peak, "unit": "TFLOP/s",
                           "frac": cc_flops / s_off / 1e12 / peak, "traffic": None,
                           "kernel_ms": best["kernel_ms"]}

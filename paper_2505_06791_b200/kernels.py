@@ -91,6 +91,7 @@ class Context:
         self.kind = 0
         self.m = 1
         self.lock = threading.RLock()
+        self._prepared = None
 
     def __del__(self):
         try:
@@ -129,7 +130,11 @@ class Context:
             self._spec = k
 
     def prepare(self, width: int):
+        key = (self._spec, width)
+        if key == self._prepared:      # module already loaded for this constraint kind / width
+            return
         _lib.check(self.L.cprrtc_prepare(self.h, int(width)), "prepare")
+        self._prepared = key
 
     @property
     def launches(self) -> int:

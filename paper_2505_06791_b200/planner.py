@@ -18,11 +18,12 @@ Differences from the reference, all deliberate:
   launches; ``deterministic`` keeps its reference meaning (ignore the wall
   clock).  ``attempts`` is accepted; the device already evaluates hundreds of
   samples at once.
-* ``stats.iterations`` counts samples drawn; ``cc_performed`` /
-  ``cc_possible`` use the reference's lockstep accounting over the checked
-  waypoints (row 0 of a motion is an existing tree node and is not
-  re-checked); the checks the GPU actually evaluated are in the result's
-  device counters.
+* ``stats.iterations`` counts samples drawn; ``cc_possible`` is the
+  reference's count over the checked waypoints (row 0 of a motion is an
+  existing tree node and is not re-checked).  ``cc_performed`` follows the
+  reference's lockstep accounting with ``DeviceOptions(cc_broadphase=0)``;
+  with the clustered broad phase (the default whenever the scene has
+  obstacles) it counts the sphere-primitive checks actually evaluated.
 """
 
 from __future__ import annotations
@@ -346,35 +347,87 @@ def plan_batch(problems, options: DeviceOptions = DeviceOptions(), return_dense:
         wall = (time.perf_counter() - t0) * 1e3
     out = []
     for i, p in enumerate(problems):
-        r = res[i]
-        st = r.stats
-        stats = PlanStats(iterations=int(st[0]), extensions_attempted=int(st[1]),
-                          extensions_added=int(st[2]), projection_failures=int(st[3]),
-                          collision_rejections=int(st[4]), cc_performed=int(st[5]),
-                          cc_possible=int(st[6]), wall_ms=wall, nodes_start=int(r.nodes_start),
-                          nodes_goal=int(r.nodes_goal), device_ms=float(r.device_ms),
-                          stage1_evals=int(st[8]), cc_fk_evals=int(st[9]), nn_nodes=int(st[10]),
-                          proj_iters=int(st[11]))
-        if r.status == -1:
-            if B == 1:
-                raise PlanSetupError(_SETUP.get(r.setup_code, "invalid start/goal"))
-            out.append(PlanResult("Error:PlanSetupError", None, None, stats))
-            continue
-        if r.status == 4:
-            raise RuntimeError(f"solution path longer than path_capacity={pc}")
-        if r.status != 0:
-            out.append(PlanResult(_STATUS.get(r.status, "IterLimit"), None, None, stats))
-            continue
-        L = int(r.path_len)
-        path = [paths[i, k].copy() for k in range(L)]
-        path[0] = p.start.copy()                 # roots are the exact FP64 endpoints
-        path[-1] = p.goal.copy()
-        sources = tuple(_SRC[int(s)] for s in srcs[i, :L - 1])
-        dense = None
-        if return_dense:
+        res_i = _result(res[i], p, paths[i], srcs[i], wall, B, pc)
+        if return_dense and res_i.solved:
+            L = len(res_i.path)
             dense, ok = _derive(ctx, prm, paths[i, :L], srcs[i, :L - 1])
-        out.append(PlanResult("Solved", tuple(path), sources, stats, dense))
+            res_i = replace(res_i, dense=dense)
+        out.append(res_i)
     return out
+
+
+def _result(r, p, paths_i, srcs_i, wall, B, pc) -> PlanResult:
+    """PlanResult of one cprrtc_result (paths_i (pc, n), srcs_i (pc,))."""
+    st = r.stats
+    stats = PlanStats(iterations=int(st[0]), extensions_attempted=int(st[1]),
+                      extensions_added=int(st[2]), projection_failures=int(st[3]),
+                      collision_rejections=int(st[4]), cc_performed=int(st[5]),
+                      cc_possible=int(st[6]), wall_ms=wall, nodes_start=int(r.nodes_start),
+                      nodes_goal=int(r.nodes_goal), device_ms=float(r.device_ms),
+                      stage1_evals=int(st[8]), cc_fk_evals=int(st[9]), nn_nodes=int(st[10]),
+                      proj_iters=int(st[11]))
+    if r.status == -1:
+        if B == 1:
+            raise PlanSetupError(_SETUP.get(r.setup_code, "invalid start/goal"))
+        return PlanResult("Error:PlanSetupError", None, None, stats)
+    if r.status == 4:
+        raise RuntimeError(f"solution path longer than path_capacity={pc}")
+    if r.status != 0:
+        return PlanResult(_STATUS.get(r.status, "IterLimit"), None, None, stats)
+    L = int(r.path_len)
+    path = list(paths_i[:L].copy())
+    path[0] = p.start.copy()                 # roots are the exact FP64 endpoints
+    path[-1] = p.goal.copy()
+    sources = tuple(_SRC[int(k)] for k in srcs_i[:L - 1])
+    return PlanResult("Solved", tuple(path), sources, stats)
+
+
+class _OneIO:
+    """Reusable host buffers and their ctypes pointers for single-query calls
+    (the latency path: no per-call array construction)."""
+
+    def __init__(self, n, pc):
+        self.s = np.empty((1, n))
+        self.g = np.empty((1, n))
+        self.seed = np.zeros(1, np.int64)
+        self.res = (_lib.Result * 1)()
+        self.paths = np.empty((1, pc, n))
+        self.srcs = np.empty((1, pc), np.int32)
+        self.args = (_lib.ptr(self.s), _lib.ptr(self.g), _lib.ptr(self.seed, _lib._lp), self.res,
+                     _lib.ptr(self.paths), _lib.ptr(self.srcs, _lib._ip))
+
+
+_ONE: dict = {}
+
+
+def _plan_one(problem: PlanProblem, options: DeviceOptions, return_dense: bool) -> PlanResult:
+    prm = _params_struct(problem.params, options)
+    ctx = _bind(problem, options)
+    pc = int(prm.path_capacity)
+    key = (id(ctx), pc, __import__("threading").get_ident())
+    io = _ONE.get(key)
+    if io is None:
+        if len(_ONE) > 64:
+            _ONE.clear()
+        io = _ONE[key] = _OneIO(ctx.n, pc)
+    seed = int(problem.params.seed_offset)
+    if seed < 0:
+        raise ValueError("seed_offset must be >= 0")
+    io.s[0] = problem.start
+    io.g[0] = problem.goal
+    io.seed[0] = seed
+    with ctx.lock:
+        ctx.prepare(problem.params.width)
+        t0 = time.perf_counter()
+        rc = ctx.L.cprrtc_plan(ctx.h, C.byref(prm), 1, *io.args)
+        wall = (time.perf_counter() - t0) * 1e3
+        _lib.check(rc, "plan")
+        res = _result(io.res[0], problem, io.paths[0], io.srcs[0], wall, 1, pc)
+        if return_dense and res.solved:
+            L = len(res.path)
+            dense, ok = _derive(ctx, prm, io.paths[0, :L], io.srcs[0, :L - 1])
+            res = replace(res, dense=dense)
+    return res
 
 
 _OUT: dict = {}
@@ -403,7 +456,7 @@ def plan(problem: PlanProblem, options: DeviceOptions = DeviceOptions(),
             raise PlanSetupError(_SETUP[int(code)])
         stats = PlanStats(wall_ms=(time.perf_counter() - t0) * 1e3, nodes_start=1, nodes_goal=1)
         return PlanResult("Solved", (problem.start.copy(),), (), stats)
-    return plan_batch([problem], options, return_dense)[0]
+    return _plan_one(problem, options, return_dense)
 
 
 def _tau(problem) -> float:

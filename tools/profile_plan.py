@@ -10,6 +10,7 @@ m, sc, sp = fx.robot("arm7"), fx.scene("table"), fx.spec("upright")
 p = fx.pairs()
 for rep in range(6):
     prob = PlanProblem(m, sc, sp, p["upright_start"][k], p["upright_goal"][k],
-                       PlanParams(width=16, max_iterations=10**6, seed_offset=rep * 10000))
+                       PlanParams(width=16, max_iterations=10**6, seed_offset=rep * 10000,
+                                  deterministic=True))   # no wall-clock budget: ncu replays the kernel
     r = plan(prob, DeviceOptions(teams=teams))
     print(rep, r.status, r.stats.device_ms, r.stats.iterations, r.stats.stage1_evals, r.stats.proj_iters)
