@@ -122,7 +122,8 @@ enum {
 
 typedef struct {
     int status;          /* 0 Solved, 1 TimedOut, 2 IterLimit, 3 tree full,
-                            4 path longer than path_capacity, -1 setup error */
+                            4 path longer than path_capacity, 5 stopped because
+                            another racer solved (cprrtc_plan_race), -1 setup error */
     int setup_code;      /* 0 ok; 1/2/3 start limits/manifold/collision;
                             4/5/6 the same for the goal (planner.py:416-427) */
     int path_len;
@@ -215,6 +216,20 @@ CPRRTC_API int cprrtc_halton(void *ctx, int count, int64_t first_index, int64_t 
 CPRRTC_API int cprrtc_plan(void *ctx, const cprrtc_params *params, int B, const double *starts,
                 const double *goals, const int64_t *seeds, cprrtc_result *results,
                 double *paths, int32_t *sources);
+/* One query raced on n_ctx contexts (typically one per GPU; at most
+ * CPRRTC_MAX_RACE): each grows its own tree pair from seeds[k] (distinct
+ * Halton offsets) with the planner of cprrtc_plan; the first racer to solve
+ * stores a first-solution flag into every racer's flag word (peer stores over
+ * NVLink / NVSwitch when the devices have peer access, else one mapped host
+ * word) and the others stop.  results / paths / sources hold n_ctx entries
+ * laid out as cprrtc_plan's with B = n_ctx; *winner = the solved racer with
+ * the shortest device time, or -1.  (The reference has no counterpart: it is
+ * a single-core planner, maniplan/planner.py:430-485.) */
+#define CPRRTC_MAX_RACE 8
+CPRRTC_API int cprrtc_plan_race(void *const *ctxs, int n_ctx, const cprrtc_params *params,
+                                const double *start, const double *goal, const int64_t *seeds,
+                                cprrtc_result *results, double *paths, int32_t *sources,
+                                int32_t *winner);
 /* One reference extend() (op 0, planner.py:317-325 / _attempt_extend :265-306)
  * or connect() (op 1, planner.py:361-409) step on a caller tree: nodes (N, n),
  * parents (N); q (n) is the sample / target.  result[0]: extend -> index of

@@ -1003,6 +1003,11 @@ __device__ __forceinline__ bool cp_should_stop(const Team& tm, QueryState& Q, co
     int s = 0;
     if (tm.lane == 0) {
         s = cp_ldvol(&Q.solved) | cp_ldvol(&Q.stop);
+        if (!s && A.race_flag && cp_ldvol(A.race_flag)) {   // another racer solved the query
+            Q.race_stopped = 1;
+            atomicExch(&Q.stop, 1);
+            s = 1;
+        }
         if (!s && A.budget_ns > 0 && cp_clock_ns() - Q.t0_ns > (u64)A.budget_ns) {
             atomicExch(&Q.timed_out, 1);
             atomicExch(&Q.stop, 1);
@@ -1183,6 +1188,9 @@ __device__ void cp_plan_query(const Team& tm, TeamWS& ws, const PlanArgs& A, con
                 Q.t_end_ns = cp_clock_ns();
                 __threadfence();
                 atomicExch(&Q.stop, 1);
+                // first-solution flag of a race: one store into every racer's word
+                for (int r = 0; r < A.n_race; r++) *(volatile int*)A.race_peers[r] = 1;
+                if (A.n_race) __threadfence_system();
             }
             break;
         }
@@ -1361,7 +1369,7 @@ extern "C" __global__ void __launch_bounds__(256) cp_setup_kernel(const __grid_c
         Q.seed_offset = S.seeds[qi];
         Q.count[0] = 1; Q.count[1] = 1;
         Q.next_sample = 0;
-        Q.solved = 0; Q.stop = c != 0; Q.timed_out = 0; Q.overflow = 0; Q.exhausted = 0;
+        Q.solved = 0; Q.stop = c != 0; Q.timed_out = 0; Q.overflow = 0; Q.exhausted = 0; Q.race_stopped = 0;
         Q.meet[0] = -1; Q.meet[1] = -1;
         for (int i = 0; i < ST_NSTAT; i++) Q.stats[i] = 0ull;
         Q.t0_ns = cp_clock_ns();
@@ -1402,7 +1410,7 @@ extern "C" __global__ void cp_extract_kernel(QueryState* qs, const float* trees,
     O.path_len = 0;
     if (Q.setup_code != 0) { O.status = -1; return; }
     if (!Q.solved) {
-        O.status = Q.timed_out ? 1 : (Q.overflow ? 3 : 2);
+        O.status = Q.timed_out ? 1 : (Q.overflow ? 3 : (Q.race_stopped ? 5 : 2));
         return;
     }
     O.status = 0;

@@ -59,7 +59,7 @@ struct QueryState {
     int solved, stop, timed_out, overflow, exhausted;
     int meet[2];           // meet node in the start / goal tree
     int setup_code;        // endpoint check (planner.py:416-427)
-    int pad;
+    int race_stopped;      // stopped because another racer solved the query
     u64 t0_ns, t_end_ns;
     u64 stats[ST_NSTAT];
 };
@@ -81,7 +81,9 @@ struct PlanArgs {
     int max_iterations, max_connect;
     i64 budget_ns;         // <= 0: no time budget (deterministic)
     int solo;              // 1: one team per warp (the other half-warp idles) -- latency mode
-    int pad_;
+    int n_race;            // racers of a cprrtc_plan_race call (0: no race)
+    int* race_flag;        // this racer's first-solution word (polled)
+    int* race_peers[8];    // every racer's word (peer-mapped); the winner stores 1 to each
 };
 
 struct SetupArgs {
@@ -105,7 +107,8 @@ struct SetupArgs {
 };
 
 struct QueryOut {
-    int status;            // 0 Solved, 1 TimedOut, 2 IterLimit, 3 tree full, 4 path overflow, -1 setup
+    int status;            // 0 Solved, 1 TimedOut, 2 IterLimit, 3 tree full, 4 path overflow,
+                           // 5 stopped by another racer, -1 setup
     int setup_code;
     int path_len;
     int n_nodes[2];

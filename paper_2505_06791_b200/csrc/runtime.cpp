@@ -301,6 +301,7 @@ struct Ctx {
     int nb = 0, ne = 0;
     DevBuf sc_box_c, sc_box_h, sc_sph, sc_bmin, sc_bmax, sc_sc, sc_sr;
     DevBuf sc_cl;          // clustered layout (broad phase), see SceneSm
+    DevBuf race_flag;      // first-solution word of cprrtc_plan_race
     int nbc = 0, nec = 0;
     // constraint
     int kind = 0, orient = 0;
@@ -1188,13 +1189,26 @@ static PlanArgs make_plan_args(Ctx* c, const cprrtc_params* prm, int B, int cap,
     return A;
 }
 
-int cprrtc_plan(void* p, const cprrtc_params* prm, int B, const double* starts, const double* goals,
-                const int64_t* seeds, cprrtc_result* results, double* paths, int32_t* sources) {
-    Ctx* c = C(p);
-    if (!c || !prm || B < 1 || !starts || !goals || !results) return fail(CPRRTC_EARG, "bad argument");
+static int check_params(const cprrtc_params* prm) {
     if (prm->step_size <= 0 || prm->width < 2 || prm->max_iterations < 1 || prm->alpha <= 0 || prm->lam < 0 ||
         prm->proj_max_iters < 1 || prm->projection_mode < 0 || prm->projection_mode > 2)
         return fail(CPRRTC_EARG, "invalid planner parameters");
+    return 0;
+}
+
+// First-solution race of one query across contexts (devices): every racer
+// polls its own flag word; the winner stores 1 into every racer's word (peer
+// stores over NVLink, or one shared mapped host word without peer access).
+struct RaceLink {
+    int* own;
+    int* peers[CPRRTC_MAX_RACE];
+    int n;
+};
+
+// Stage inputs and launch the per-call sequence (H2D, setup, plan, extract)
+// on the context's stream; plan_collect waits and reads the results.
+static int plan_launch(Ctx* c, const cprrtc_params* prm, int B, const double* starts, const double* goals,
+                       const int64_t* seeds, const RaceLink* race) {
     if (int rc = set_device(c)) return rc;
     Module* m;
     if (int rc = cur_module(c, prm->width, 0, &m)) return rc;
@@ -1231,6 +1245,11 @@ int cprrtc_plan(void* p, const cprrtc_params* prm, int B, const double* starts, 
     S.reset_tree = 1;
     // the persistent planner
     PlanArgs A = make_plan_args(c, prm, B, cap, tau);
+    if (race) {
+        A.race_flag = race->own;
+        A.n_race = race->n;
+        for (int k = 0; k < race->n; k++) A.race_peers[k] = race->peers[k];
+    }
     if (!m->plan_occ) {
         int occ = 0;
         drv().occupancy(&occ, m->fn["cp_plan_kernel"], kThreads, team_smem(c, m, true));
@@ -1330,15 +1349,22 @@ int cprrtc_plan(void* p, const cprrtc_params* prm, int B, const double* starts, 
     }
     CUDA_TRY(cudaGraphLaunch(G->exec, c->stream));
     c->launches += 3;   // setup, plan, extract
+    c->last_args = A;
+    c->last_mod = m;
+    c->last_nq = B;
+    return 0;
+}
+
+static int plan_collect(Ctx* c, int B, cprrtc_result* results, double* paths, int32_t* sources) {
+    if (int rc = set_device(c)) return rc;
     if (int rc = sync(c)) return rc;
+    const int n = c->n;
+    const int path_cap = c->path_cap;
     float t_all = 0, t_plan = 0;
     cudaEventElapsedTime(&t_all, c->ev[0], c->ev[3]);
     cudaEventElapsedTime(&t_plan, c->ev[1], c->ev[2]);
     c->last_total_ms = t_all;
     c->last_plan_ms = t_plan;
-    c->last_args = A;
-    c->last_mod = m;
-    c->last_nq = B;
     const QueryOut* out = c->h_out.host<QueryOut>();
     const float* hp = c->h_paths.host<float>();
     const int* hs = c->h_src.host<int>();
@@ -1359,6 +1385,85 @@ int cprrtc_plan(void* p, const cprrtc_params* prm, int B, const double* starts, 
         if (sources && r.path_len > 1)
             for (int k = 0; k < r.path_len - 1; k++) sources[(size_t)i * path_cap + k] = hs[(size_t)i * path_cap + k];
     }
+    return 0;
+}
+
+int cprrtc_plan(void* p, const cprrtc_params* prm, int B, const double* starts, const double* goals,
+                const int64_t* seeds, cprrtc_result* results, double* paths, int32_t* sources) {
+    Ctx* c = C(p);
+    if (!c || !prm || B < 1 || !starts || !goals || !results) return fail(CPRRTC_EARG, "bad argument");
+    if (int rc = check_params(prm)) return rc;
+    if (int rc = plan_launch(c, prm, B, starts, goals, seeds, nullptr)) return rc;
+    return plan_collect(c, B, results, paths, sources);
+}
+
+int cprrtc_plan_race(void* const* ctxs, int n_ctx, const cprrtc_params* prm, const double* start,
+                     const double* goal, const int64_t* seeds, cprrtc_result* results, double* paths,
+                     int32_t* sources, int32_t* winner) {
+    if (!ctxs || n_ctx < 1 || n_ctx > CPRRTC_MAX_RACE || !prm || !start || !goal || !seeds || !results || !winner)
+        return fail(CPRRTC_EARG, "bad argument");
+    if (int rc = check_params(prm)) return rc;
+    std::vector<Ctx*> cs(n_ctx);
+    for (int k = 0; k < n_ctx; k++) {
+        cs[k] = C(ctxs[k]);
+        if (!cs[k]) return fail(CPRRTC_EARG, "NULL context");
+        for (int j = 0; j < k; j++)
+            if (cs[j] == cs[k]) return fail(CPRRTC_EARG, "a context can race only once");
+    }
+    // peer access between every pair of distinct devices (NVLink / NVSwitch)
+    bool peers = true;
+    for (int a = 0; a < n_ctx && peers; a++)
+        for (int b = 0; b < n_ctx; b++) {
+            const int da = cs[a]->device, db = cs[b]->device;
+            if (da == db) continue;
+            int can = 0;
+            cudaDeviceCanAccessPeer(&can, da, db);
+            if (!can) { peers = false; break; }
+            CUDA_TRY(cudaSetDevice(da));
+            cudaError_t e = cudaDeviceEnablePeerAccess(db, 0);
+            if (e != cudaSuccess && e != cudaErrorPeerAccessAlreadyEnabled)
+                return fail(CPRRTC_ECUDA, std::string("peer access: ") + cudaGetErrorString(e));
+            cudaGetLastError();
+        }
+    RaceLink link{};
+    link.n = n_ctx;
+    static int* host_flag = nullptr;   // fallback without peer access: one mapped, portable host word
+    if (peers) {
+        for (int k = 0; k < n_ctx; k++) {
+            if (int rc = set_device(cs[k])) return rc;
+            if (int rc = cs[k]->race_flag.ensure(4)) return rc;
+            CUDA_TRY(cudaMemsetAsync(cs[k]->race_flag.p, 0, 4, cs[k]->stream));
+            link.peers[k] = cs[k]->race_flag.as<int>();
+        }
+    } else {
+        if (!host_flag) {
+            void* h = nullptr;
+            cudaError_t e = cudaHostAlloc(&h, 64, cudaHostAllocMapped | cudaHostAllocPortable);
+            if (e != cudaSuccess) return fail(CPRRTC_ECUDA, std::string("cudaHostAlloc: ") + cudaGetErrorString(e));
+            host_flag = static_cast<int*>(h);   // UVA: the same address on every device
+        }
+        *(volatile int*)host_flag = 0;
+        link.n = 1;
+        link.peers[0] = host_flag;
+    }
+    int rc = 0;
+    for (int k = 0; k < n_ctx && !rc; k++) {
+        link.own = peers ? link.peers[k] : link.peers[0];
+        rc = plan_launch(cs[k], prm, 1, start, goal, seeds + k, &link);
+    }
+    const int pc = prm->path_capacity > 0 ? prm->path_capacity : 1024;
+    const int n = cs[0]->n;
+    for (int k = 0; k < n_ctx; k++) {   // always drain every launched racer
+        int rk = plan_collect(cs[k], 1, results + k, paths ? paths + (size_t)k * pc * n : nullptr,
+                              sources ? sources + (size_t)k * pc : nullptr);
+        if (!rc) rc = rk;
+    }
+    if (rc) return rc;
+    // winner: the solved racer with the shortest device time
+    *winner = -1;
+    for (int k = 0; k < n_ctx; k++)
+        if (results[k].status == 0 && (*winner < 0 || results[k].device_ms < results[*winner].device_ms))
+            *winner = k;
     return 0;
 }
 

@@ -156,19 +156,21 @@ _CTX_LOCK = threading.Lock()
 _BY_ID: dict = {}
 
 
-def context(model_or_packed, device: int = 0) -> Context:
+def context(model_or_packed, device: int = 0, slot: int = 0) -> Context:
+    """The (robot, device, thread) context; ``slot`` > 0 gives further
+    independent contexts on the same device (e.g. several racers on one GPU)."""
     packed = getattr(model_or_packed, "packed", model_or_packed)
     tid = threading.get_ident()
-    hit = _BY_ID.get((id(packed), device, tid))
+    hit = _BY_ID.get((id(packed), device, tid, slot))
     if hit is not None and hit[0] is packed:
         return hit[1]
-    key = (robot_key(packed), device, tid)
+    key = (robot_key(packed), device, tid, slot)
     with _CTX_LOCK:
         ctx = _CTX.get(key)
         if ctx is None:
             ctx = Context(packed, device)
             _CTX[key] = ctx
-        _BY_ID[(id(packed), device, tid)] = (packed, ctx)   # strong ref: ids stay unique
+        _BY_ID[(id(packed), device, tid, slot)] = (packed, ctx)   # strong ref: ids stay unique
     return ctx
 
 

@@ -46,7 +46,7 @@ __all__ = [
     "Tree", "PlanParams", "PlanProblem", "PlanResult", "PlanStats", "PlanContext",
     "ExtendOutcome", "ConnectOutcome", "DeviceOptions", "nearest", "steer", "plan",
     "plan_batch", "extract_path", "derive_edge", "revalidate_path", "dense_path", "extend",
-    "connect", "prepare",
+    "connect", "prepare", "plan_race",
 ]
 
 
@@ -218,7 +218,7 @@ class ConnectOutcome:
 
 
 _MODES = {"parallel": 0, "literal-gap": 1, "naive": 2}
-_STATUS = {0: "Solved", 1: "TimedOut", 2: "IterLimit", 3: "IterLimit"}
+_STATUS = {0: "Solved", 1: "TimedOut", 2: "IterLimit", 3: "IterLimit", 5: "Stopped"}   # 5: another racer solved
 _SETUP = {1: "start violates joint limits", 2: "start is off the constraint manifold",
           3: "start is in collision", 4: "goal violates joint limits",
           5: "goal is off the constraint manifold", 6: "goal is in collision"}
@@ -457,6 +457,57 @@ def plan(problem: PlanProblem, options: DeviceOptions = DeviceOptions(),
         stats = PlanStats(wall_ms=(time.perf_counter() - t0) * 1e3, nodes_start=1, nodes_goal=1)
         return PlanResult("Solved", (problem.start.copy(),), (), stats)
     return _plan_one(problem, options, return_dense)
+
+
+RACE_SEED_STRIDE = 1_000_000_007   # Halton offset between racers (distinct sample streams)
+
+
+def plan_race(problem: PlanProblem, devices=(0, 1), options: DeviceOptions = DeviceOptions()):
+    """One query raced on several GPUs (cprrtc_plan_race): racer k plans on
+    ``devices[k]`` with seed_offset + k * RACE_SEED_STRIDE; the first to solve
+    stores a first-solution flag into every racer's flag word over NVLink
+    (peer stores) and the others stop.  Returns (PlanResult of the winner, or
+    of racer 0 if none solved, winner index or -1, per-racer PlanResults).
+    A device may appear more than once (independent contexts on one GPU)."""
+    devices = tuple(int(d) for d in devices)
+    if not 1 <= len(devices) <= _lib.MAX_RACE:
+        raise ValueError(f"1..{_lib.MAX_RACE} racers")
+    if np.array_equal(problem.start, problem.goal):
+        r = plan(problem, replace(options, device=devices[0]))
+        return r, 0, [r]
+    prm = _params_struct(problem.params, options)
+    seen: dict = {}
+    ctxs = []
+    for d in devices:
+        slot = seen.get(d, 0)
+        seen[d] = slot + 1
+        ctx = kernels.context(problem.model, d, slot)
+        ctx.set_scene(problem.scene.packed())
+        ctx.set_spec(None if problem.spec is None else problem.spec.packed)
+        ctx.prepare(problem.params.width)
+        ctxs.append(ctx)
+    R = len(ctxs)
+    n = ctxs[0].n
+    pc = int(prm.path_capacity)
+    base = int(problem.params.seed_offset)
+    if base < 0:
+        raise ValueError("seed_offset must be >= 0")
+    seeds = np.array([base + k * RACE_SEED_STRIDE for k in range(R)], np.int64)
+    start = np.ascontiguousarray(problem.start, dtype=np.float64)
+    goal = np.ascontiguousarray(problem.goal, dtype=np.float64)
+    res = (_lib.Result * R)()
+    paths = np.empty((R, pc, n))
+    srcs = np.empty((R, pc), np.int32)
+    handles = (C.c_void_p * R)(*[c.h.value for c in ctxs])
+    win = C.c_int32(-1)
+    t0 = time.perf_counter()
+    _lib.check(ctxs[0].L.cprrtc_plan_race(handles, R, C.byref(prm), _lib.ptr(start), _lib.ptr(goal),
+                                          _lib.ptr(seeds, _lib._lp), res, _lib.ptr(paths),
+                                          _lib.ptr(srcs, _lib._ip), C.byref(win)), "plan_race")
+    wall = (time.perf_counter() - t0) * 1e3
+    per = [_result(res[k], problem, paths[k], srcs[k], wall, 1, pc) for k in range(R)]
+    w = int(win.value)
+    return per[w if w >= 0 else 0], w, per
 
 
 def _tau(problem) -> float:

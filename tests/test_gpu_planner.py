@@ -129,3 +129,22 @@ def test_iteration_limit_and_unsolvable():
     res = plan(PlanProblem(m, wall, None, np.array([np.pi / 2, 0.0]), np.array([-np.pi / 2, 0.0]),
                            PlanParams(width=8, max_iterations=10**9, time_budget_ms=50.0)))
     assert res.status == "TimedOut" and 40.0 < res.stats.device_ms < 500.0
+
+
+def test_plan_race_first_solution_flag(oracle):
+    """cprrtc_plan_race on two independent contexts of one GPU (the flag
+    mechanism of the multi-GPU race; distinct devices use peer stores): a
+    winner is reported, its path is sound in FP64, and every racer either
+    solved too or stopped on the flag."""
+    from paper_2505_06791_b200.planner import PlanParams, PlanProblem, plan_race
+    m, sc, sp = fx.robot("arm7"), fx.scene("table"), fx.spec("upright")
+    prs = fx.pairs()
+    feas = np.nonzero(fx.upright_feasible())[0]
+    for k in feas[:4]:
+        prob = PlanProblem(m, sc, sp, prs["upright_start"][k], prs["upright_goal"][k],
+                           PlanParams(width=16, max_iterations=1_000_000, seed_offset=int(k)))
+        best, w, per = plan_race(prob, devices=(0, 0, 0))
+        assert w >= 0 and best.solved and per[w] is best
+        assert all(r.status in ("Solved", "Stopped") for r in per), [r.status for r in per]
+        assert best.stats.device_ms == min(r.stats.device_ms for r in per if r.solved)
+        _check_path(oracle, prob, best)
