@@ -43,6 +43,7 @@ N_PAIRS = 100
 # reference formulas): projection stage 1 with plane+orientation (m=4), FK +
 # world spheres of arm7, one sphere-primitive check, one NN node (3n-1).
 FLOP_STAGE1_M4 = 1750.0
+FLOP_STAGE1_M1 = 1240.0
 FLOP_FK_ARM7 = 1195.0
 FLOP_CHECK = 11.0
 FLOP_NN7 = 20.0
@@ -340,20 +341,30 @@ def extras(args, local, model, line):
                          PlanParams(width=16, max_iterations=300, seed_offset=i * 10_000))
              for i in range(1024)]
     opt = DeviceOptions(device=local)
+    from paper_2505_06791_b200.planner import prepare
+    bctx = prepare(probs[0], opt)
     plan_batch(probs[:8], opt)
-    t0 = time.perf_counter()
-    res = plan_batch(probs, opt)
-    dt = time.perf_counter() - t0
-    best = dt
-    for _ in range(2):
+    best, best_res, best_kms = None, None, None
+    for _ in range(3):
         t0 = time.perf_counter()
         res = plan_batch(probs, opt)
-        best = min(best, time.perf_counter() - t0)
-    dt = best
+        dt = time.perf_counter() - t0
+        if best is None or dt < best:
+            best, best_res, best_kms = dt, res, bctx.last_timing()[1]
+    dt, res = best, best_res
+    # the same kernel at full occupancy (throughput mode): algorithmic FP32
+    # work of the batch (plane constraint: m = 1 stage-1 cost) / kernel time
+    bflops = sum(r.stats.stage1_evals * FLOP_STAGE1_M1 + r.stats.cc_fk_evals * FLOP_FK_ARM7
+                 + r.stats.cc_performed * FLOP_CHECK + r.stats.nn_nodes * FLOP_NN7 for r in res)
+    bach = bflops / (best_kms * 1e-3) / 1e12
     out["batch_1024"] = {"queries_per_s": 1024 / dt, "wall_ms": dt * 1e3,
                          "success_rate": sum(r.solved for r in res) / 1024,
                          "config": "configs[4]: 1024 arm7 table-plane (z=0.60, tau 0.01) queries, W=16, "
-                                   "max_iterations 300 each, one persistent launch"}
+                                   "max_iterations 300 each, one persistent launch",
+                         "roofline": {"bound": "fp32", "kernel": "cp_plan_kernel (batch, every resident team)",
+                                      "achieved": bach, "peak": line["roofline"]["peak"], "unit": "TFLOP/s",
+                                      "frac": bach / line["roofline"]["peak"], "kernel_ms": best_kms,
+                                      "work": "stage1 x 1240 (m=1) + cc_fk x 1195 + checks x 11 + nn_nodes x 20 flop"}}
     return out
 
 

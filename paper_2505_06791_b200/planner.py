@@ -321,10 +321,10 @@ def plan_batch(problems, options: DeviceOptions = DeviceOptions(), return_dense:
         return []
     p0 = problems[0]
     if len(problems) > 1:
-        base = replace(p0.params, seed_offset=0)
+        base = _params_key(p0.params)
         for p in problems[1:]:
             if (p.model is not p0.model or p.scene is not p0.scene or p.spec is not p0.spec
-                    or replace(p.params, seed_offset=0) != base):
+                    or (p.params is not p0.params and _params_key(p.params) != base)):
                 raise ValueError("plan_batch problems must share model, scene, spec and params")
     prm = _params_struct(p0.params, options)
     ctx = _bind(p0, options)
@@ -345,14 +345,68 @@ def plan_batch(problems, options: DeviceOptions = DeviceOptions(), return_dense:
                                      _lib.ptr(seeds, _lib._lp), res, _lib.ptr(paths),
                                      _lib.ptr(srcs, _lib._ip)), "plan")
         wall = (time.perf_counter() - t0) * 1e3
+    if B == 1:
+        out = [_result(res[0], p0, paths[0], srcs[0], wall, B, pc)]
+    else:
+        out = _results_bulk(res, problems, paths, srcs, wall, pc)
+    if return_dense:
+        for i, r in enumerate(out):
+            if r.solved:
+                L = len(r.path)
+                dense, ok = _derive(ctx, prm, paths[i, :L], srcs[i, :L - 1])
+                out[i] = replace(r, dense=dense)
+    return out
+
+
+_PARAM_FIELDS = None
+
+
+def _params_key(p) -> tuple:
+    """PlanParams fields except seed_offset (plan_batch consistency check)."""
+    global _PARAM_FIELDS
+    if _PARAM_FIELDS is None:
+        from dataclasses import fields
+        _PARAM_FIELDS = tuple(f.name for f in fields(PlanParams) if f.name != "seed_offset")
+    return tuple(getattr(p, f) for f in _PARAM_FIELDS)
+
+
+_RESULT_DT = np.dtype({"names": ["status", "setup_code", "path_len", "ns", "ng", "device_ms", "stats"],
+                       "formats": [np.int32, np.int32, np.int32, np.int32, np.int32, np.float64,
+                                   (np.uint64, _lib.ST_COUNT)],
+                       "offsets": [_lib.Result.status.offset, _lib.Result.setup_code.offset,
+                                   _lib.Result.path_len.offset, _lib.Result.nodes_start.offset,
+                                   _lib.Result.nodes_goal.offset, _lib.Result.device_ms.offset,
+                                   _lib.Result.stats.offset],
+                       "itemsize": C.sizeof(_lib.Result)})
+
+
+def _results_bulk(res, problems, paths, srcs, wall, pc):
+    """PlanResults of a batch: one structured numpy view of the result array
+    and bulk conversions instead of per-field ctypes access."""
+    a = np.frombuffer(res, dtype=_RESULT_DT)
+    status = a["status"].tolist()
+    plen = a["path_len"].tolist()
+    ns, ng, dms = a["ns"].tolist(), a["ng"].tolist(), a["device_ms"].tolist()
+    st = a["stats"].tolist()
     out = []
     for i, p in enumerate(problems):
-        res_i = _result(res[i], p, paths[i], srcs[i], wall, B, pc)
-        if return_dense and res_i.solved:
-            L = len(res_i.path)
-            dense, ok = _derive(ctx, prm, paths[i, :L], srcs[i, :L - 1])
-            res_i = replace(res_i, dense=dense)
-        out.append(res_i)
+        s = st[i]
+        stats = PlanStats(s[0], s[1], s[2], s[3], s[4], s[5], s[6], wall, ns[i], ng[i], dms[i],
+                          s[8], s[9], s[10], s[11])
+        code = status[i]
+        if code == 0:
+            L = plen[i]
+            path = list(paths[i, :L].copy())
+            path[0] = p.start.copy()                 # roots are the exact FP64 endpoints
+            path[-1] = p.goal.copy()
+            out.append(PlanResult("Solved", tuple(path), tuple(_SRC[k] for k in srcs[i, :L - 1].tolist()),
+                                  stats))
+        elif code == -1:
+            out.append(PlanResult("Error:PlanSetupError", None, None, stats))
+        elif code == 4:
+            raise RuntimeError(f"solution path longer than path_capacity={pc}")
+        else:
+            out.append(PlanResult(_STATUS.get(code, "IterLimit"), None, None, stats))
     return out
 
 
