@@ -1300,6 +1300,84 @@ __device__ __forceinline__ SceneSm cp_stage_scene(const SceneSm& g, float4* sm) 
 }
 
 #if !CP_PARITY
+// Path extraction (planner.py:488-505) into the result area (mapped host
+// memory), by one team: lane 0 walks the two parent chains (dependent L2
+// loads) into a device index list; then the team gathers the node
+// coordinates and writes path and sources with contiguous lane-consecutive
+// stores (coalesced PCIe writes).  setup_code is written by cp_check_kernel.
+__device__ __noinline__ void cp_extract_query(const Team tm, const PlanArgs& A, int qi) {
+    QueryState& Q = A.qs[qi];
+    QueryOut& O = A.out[qi];
+    const int lane = (int)tm.lane, cap = A.cap, path_cap = A.path_cap;
+    const int ns = min(cp_ldvol(&Q.count[0]), cap), ng = min(cp_ldvol(&Q.count[1]), cap);
+    if (lane < ST_NSTAT) O.stats[lane] = __ldcg(&Q.stats[lane]);
+    if (ST_NSTAT > CP_G && lane + CP_G < ST_NSTAT) O.stats[lane + CP_G] = __ldcg(&Q.stats[lane + CP_G]);
+    const float* ts = cp_tree(A, qi, 0);
+    const float* tg = cp_tree(A, qi, 1);
+    const int* ps = cp_par(A, qi, 0);
+    const int* pg = cp_par(A, qi, 1);
+    int* ch = A.chain + (size_t)qi * path_cap;   // path position -> (tree << 30) | node
+    const int solved = cp_ldvol(&Q.solved);
+    int status = 0, len = 0, ca = 0, skip = 0;
+    if (!solved) {
+        status = cp_ldvol(&Q.timed_out) ? 1 : (cp_ldvol(&Q.overflow) ? 3 : (cp_ldvol(&Q.race_stopped) ? 5 : 2));
+    } else {
+        if (lane == 0) {
+            const int m0 = cp_ldvol(&Q.meet[0]), m1 = cp_ldvol(&Q.meet[1]);
+            for (int i = m0;; i = __ldcg(ps + i)) {   // start chain, meet first
+                if (ca < path_cap) ch[ca] = i;
+                ca++;
+                if (__ldcg(ps + i) == i) break;
+            }
+            bool same = true;
+            for (int d = 0; d < CP_N; d++) same &= __ldcg(ts + (size_t)d * cap + m0) == __ldcg(tg + (size_t)d * cap + m1);
+            skip = same ? 1 : 0;
+            int cb = 0;
+            for (int i = m1;; i = __ldcg(pg + i)) {   // goal chain, meet first
+                if (!(cb == 0 && skip) && ca + cb - skip < path_cap) ch[ca + cb - skip] = (1 << 30) | i;
+                cb++;
+                if (__ldcg(pg + i) == i) break;
+            }
+            len = ca + cb - skip;
+            if (len > path_cap) status = 4;
+            else
+                for (int a = 0, b = ca - 1; a < b; a++, b--) { int t = ch[a]; ch[a] = ch[b]; ch[b] = t; }
+        }
+        status = tm.bcast(status, 0);
+        len = tm.bcast(len, 0);
+        ca = tm.bcast(ca, 0);
+        skip = tm.bcast(skip, 0);
+        __threadfence_block();
+        tm.sync();
+        if (status == 0) {
+            float* path = A.paths + (size_t)qi * path_cap * CP_N;
+            for (int f = lane; f < len * CP_N; f += CP_G) {
+                const int k = f / CP_N, d = f - k * CP_N;
+                const int e = ch[k];
+                path[f] = __ldcg(((e >> 30) ? tg : ts) + (size_t)d * cap + (e & 0x3fffffff));
+            }
+            // edge sources: start edges, then the junction (or the first goal
+            // edge when the meet nodes coincide), then goal edges
+            int* src = A.sources + (size_t)qi * path_cap;
+            for (int k = lane; k < len - 1; k += CP_G) src[k] = k < ca - 1 ? 0 : (k == ca - 1 ? (skip ? 2 : 1) : 2);
+        }
+    }
+    if (lane == 0) {
+        O.status = status;
+        O.path_len = status == 0 ? len : 0;
+        O.n_nodes[0] = ns;
+        O.n_nodes[1] = ng;
+        Q.hwm[0] = ns;
+        Q.hwm[1] = ng;
+        const u64 tend = solved ? Q.t_end_ns : cp_clock_ns();
+        O.device_ms = (double)(tend - Q.t0_ns) * 1e-6;
+    }
+    tm.sync();
+}
+
+#endif
+
+#if !CP_PARITY
 // Dynamic smem: [scene float4s][team workspaces]
 extern "C" __global__ void __launch_bounds__(CP_NTHREADS, 1)
 cp_plan_kernel(const __grid_constant__ PlanArgs A) {
@@ -1331,8 +1409,20 @@ cp_plan_kernel(const __grid_constant__ PlanArgs A) {
         }
         qi = tm.bcast(qi, 0);
         if (qi < 0 || ++visits > 4 * A.nq + 4) break;
-        if (A.qs[qi].setup_code != 0) continue;
+        QueryState& Q = A.qs[qi];
+        if (tm.lane == 0) atomicAdd(&Q.active, 1);
         cp_plan_query(tm, ws, A, sc, qi);
+        // the last team to leave the query extracts its result (a late
+        // joiner may extract again: identical values)
+        int last = 0;
+        if (tm.lane == 0) {
+            __threadfence();
+            last = atomicSub(&Q.active, 1) == 1;
+        }
+        if (tm.bcast(last, 0)) {
+            __threadfence();
+            cp_extract_query(tm, A, qi);
+        }
     }
 }
 
@@ -1401,43 +1491,54 @@ __device__ int cp_check_config_d(const SetupArgs& S, const double* q, int lane) 
 }
 
 #if !CP_PARITY
-extern "C" __global__ void __launch_bounds__(256) cp_setup_kernel(const __grid_constant__ SetupArgs S) {
+// Per-query state and tree roots (planner.py:442-445); one 32-thread block per
+// query.  The NaN refill of the previous run's node slots already happened at
+// the end of that run (cp_reset_kernel, outside the timed region).
+extern "C" __global__ void __launch_bounds__(32) cp_init_kernel(const __grid_constant__ SetupArgs S) {
+    const int qi = blockIdx.x, lane = threadIdx.x;
+    QueryState& Q = S.qs[qi];
+    if (qi == 0 && lane < 16 && S.counters) S.counters[lane] = 0;
+    if (lane < CP_N) {
+        S.trees[((size_t)(2 * qi) * CP_N + lane) * S.cap] = (float)S.starts[(size_t)qi * CP_N + lane];
+        S.trees[((size_t)(2 * qi + 1) * CP_N + lane) * S.cap] = (float)S.goals[(size_t)qi * CP_N + lane];
+    }
+    if (lane == 0) {
+        S.parents[(size_t)(2 * qi) * S.cap] = 0;
+        S.parents[(size_t)(2 * qi + 1) * S.cap] = 0;
+        Q.setup_code = 0;
+        Q.seed_offset = S.seeds[qi];
+        Q.count[0] = 1; Q.count[1] = 1;
+        Q.next_sample = 0;
+        Q.solved = 0; Q.stop = 0; Q.timed_out = 0; Q.overflow = 0; Q.exhausted = 0; Q.race_stopped = 0;
+        Q.active = 0;
+        Q.meet[0] = -1; Q.meet[1] = -1;
+        Q.t0_ns = cp_clock_ns();
+        Q.t_end_ns = 0;
+    }
+    if (lane < ST_NSTAT) Q.stats[lane] = 0ull;
+}
+
+// FP64 endpoint checks (planner.py:416-427 _check_endpoint), run concurrently
+// with the planner (its own graph branch): a bad start / goal stops the query
+// and its code goes straight to the results (the host then reports the
+// reference's PlanSetupError).  One 64-thread block per query: warp 0 checks
+// the start, warp 1 the goal.
+extern "C" __global__ void __launch_bounds__(64) cp_check_kernel(const __grid_constant__ SetupArgs S) {
     const int qi = blockIdx.x;
     const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
     QueryState& Q = S.qs[qi];
     __shared__ int codes[2];
-    if (S.reset_tree) {
-        // NaN-refill the node slots the previous run used (publication marker)
-        const float nan = __int_as_float(0x7fffffff);
-        for (int k = 0; k < 2; k++) {
-            const int h = min(Q.hwm[k], S.cap);
-            float* base = S.trees + (size_t)(2 * qi + k) * CP_N * S.cap;
-            for (int d = 0; d < CP_N; d++)
-                for (int i = threadIdx.x; i < h; i += blockDim.x) base[(size_t)d * S.cap + i] = nan;
-        }
-        __syncthreads();
-    }
-    if (qi == 0 && threadIdx.x < 16 && S.counters) S.counters[threadIdx.x] = 0;
-    if (w < 2) {
-        const double* q = (w == 0 ? S.starts : S.goals) + (size_t)qi * CP_N;
-        int code = cp_check_config_d(S, q, lane);
-        if (lane == 0) codes[w] = code;
-        // trees: roots (planner.py:442-443)
-        if (lane < CP_N) S.trees[((size_t)(2 * qi + w) * CP_N + lane) * S.cap + 0] = (float)q[lane];
-        if (lane == 0) S.parents[(size_t)(2 * qi + w) * S.cap] = 0;
-    }
+    const double* q = (w == 0 ? S.starts : S.goals) + (size_t)qi * CP_N;
+    int code = cp_check_config_d(S, q, lane);
+    if (lane == 0) codes[w] = code;
     __syncthreads();
     if (threadIdx.x == 0) {
         int c = codes[0] ? codes[0] : (codes[1] ? 3 + codes[1] : 0);
-        Q.setup_code = c;
-        Q.seed_offset = S.seeds[qi];
-        Q.count[0] = 1; Q.count[1] = 1;
-        Q.next_sample = 0;
-        Q.solved = 0; Q.stop = c != 0; Q.timed_out = 0; Q.overflow = 0; Q.exhausted = 0; Q.race_stopped = 0;
-        Q.meet[0] = -1; Q.meet[1] = -1;
-        for (int i = 0; i < ST_NSTAT; i++) Q.stats[i] = 0ull;
-        Q.t0_ns = cp_clock_ns();
-        Q.t_end_ns = 0;
+        S.out[qi].setup_code = c;
+        if (c) {
+            Q.setup_code = c;
+            atomicExch(&Q.stop, 1);
+        }
     }
 }
 
@@ -1452,69 +1553,6 @@ extern "C" __global__ void cp_reset_kernel(QueryState* qs, float* trees, int cap
             for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < h; i += gridDim.x * blockDim.x)
                 base[(size_t)d * cap + i] = nan;
     }
-}
-
-// Path extraction (planner.py:488-505) into the result area (mapped host
-// memory).  One warp per query; lane 0 walks the parent chains.
-
-extern "C" __global__ void cp_extract_kernel(QueryState* qs, const float* trees, const int* parents, int cap,
-                                             int nq, QueryOut* out, float* paths, int* sources, int path_cap) {
-    const int qi = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
-    if (qi >= nq || (threadIdx.x & 31) != 0) return;
-    QueryState& Q = qs[qi];
-    QueryOut& O = out[qi];
-    O.setup_code = Q.setup_code;
-    O.n_nodes[0] = min(Q.count[0], cap);
-    O.n_nodes[1] = min(Q.count[1], cap);
-    Q.hwm[0] = O.n_nodes[0];
-    Q.hwm[1] = O.n_nodes[1];
-    for (int i = 0; i < ST_NSTAT; i++) O.stats[i] = Q.stats[i];
-    const u64 tend = Q.solved ? Q.t_end_ns : cp_clock_ns();
-    O.device_ms = (double)(tend - Q.t0_ns) * 1e-6;
-    O.path_len = 0;
-    if (Q.setup_code != 0) { O.status = -1; return; }
-    if (!Q.solved) {
-        O.status = Q.timed_out ? 1 : (Q.overflow ? 3 : (Q.race_stopped ? 5 : 2));
-        return;
-    }
-    O.status = 0;
-    const float* ts = trees + (size_t)(2 * qi) * CP_N * cap;
-    const float* tg = trees + (size_t)(2 * qi + 1) * CP_N * cap;
-    const int* ps = parents + (size_t)(2 * qi) * cap;
-    const int* pg = parents + (size_t)(2 * qi + 1) * cap;
-    float* path = paths + (size_t)qi * path_cap * CP_N;
-    int* src = sources + (size_t)qi * path_cap;
-    int ca = 1, cb = 1;
-    for (int i = Q.meet[0]; ps[i] != i && ca <= path_cap; i = ps[i]) ca++;
-    for (int i = Q.meet[1]; pg[i] != i && cb <= path_cap; i = pg[i]) cb++;
-    bool same = true;
-    for (int d = 0; d < CP_N; d++) same &= ts[(size_t)d * cap + Q.meet[0]] == tg[(size_t)d * cap + Q.meet[1]];
-    const int skip = same ? 1 : 0;
-    const int len = ca + cb - skip;
-    if (len > path_cap) { O.status = 4; return; }
-    int k = ca - 1;
-    for (int i = Q.meet[0];; i = ps[i]) {
-        for (int d = 0; d < CP_N; d++) path[(size_t)k * CP_N + d] = ts[(size_t)d * cap + i];
-        k--;
-        if (ps[i] == i) break;
-    }
-    k = ca;
-    int first = 1;
-    for (int i = Q.meet[1];; i = pg[i]) {
-        if (!(first && skip)) {
-            for (int d = 0; d < CP_N; d++) path[(size_t)k * CP_N + d] = tg[(size_t)d * cap + i];
-            k++;
-        }
-        first = 0;
-        if (pg[i] == i) break;
-    }
-    int s = 0;
-    for (int i = 0; i < ca - 1; i++) src[s++] = 0;
-    if (cb - skip > 0) {
-        src[s++] = skip ? 2 : 1;
-        for (int i = 0; i < cb - skip - 1; i++) src[s++] = 2;
-    }
-    O.path_len = len;
 }
 
 #endif  // !CP_PARITY

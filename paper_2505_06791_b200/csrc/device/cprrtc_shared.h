@@ -60,6 +60,8 @@ struct QueryState {
     int meet[2];           // meet node in the start / goal tree
     int setup_code;        // endpoint check (planner.py:416-427)
     int race_stopped;      // stopped because another racer solved the query
+    int active;            // teams inside the query (the last one out extracts)
+    int pad_;
     u64 t0_ns, t_end_ns;
     u64 stats[ST_NSTAT];
 };
@@ -84,6 +86,13 @@ struct PlanArgs {
     int n_race;            // racers of a cprrtc_plan_race call (0: no race)
     int* race_flag;        // this racer's first-solution word (polled)
     int* race_peers[8];    // every racer's word (peer-mapped); the winner stores 1 to each
+    // results, written by the last team to leave each query (planner.py:488-505)
+    struct QueryOut* out;  // (nq) mapped host memory
+    float* paths;          // (nq, path_cap, CP_N) mapped host memory
+    int* sources;          // (nq, path_cap) mapped host memory
+    int* chain;            // (nq, path_cap) device scratch: path position -> node
+    int path_cap;
+    int pad2_;
 };
 
 struct SetupArgs {
@@ -102,8 +111,7 @@ struct SetupArgs {
     const double* sph_r;
     int nb, ne;
     int* counters;          // planner queue counters, zeroed by block 0 (may be null)
-    int reset_tree;         // 1: NaN-refill the slots the previous run used
-    int pad_;
+    struct QueryOut* out;   // endpoint-check codes go straight to the results
 };
 
 struct QueryOut {

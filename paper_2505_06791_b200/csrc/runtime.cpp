@@ -318,9 +318,12 @@ struct Ctx {
     Module* last_mod = nullptr;
     int last_nq = 0;
     DevBuf dense_buf, dense_ok, dense_nodes;
+    DevBuf chain;          // path extraction: node index per path position
     // scratch for parity/batch entry points
     DevBuf scratch[10];
     cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};
+    cudaStream_t stream2 = nullptr;          // the endpoint-check branch of the plan graph
+    cudaEvent_t fork = nullptr, join = nullptr;
     // cached CUDA graphs of the per-call plan sequence (H2D, setup, plan, extract)
     struct PlanGraph {
         cudaGraphExec_t exec = nullptr;
@@ -348,8 +351,8 @@ std::string prelude(const Ctx* c, int G, int kind, int orient, int parity) {
     return os.str();
 }
 
-const std::vector<const char*> kPlanKernels = {"cp_plan_kernel", "cp_setup_kernel", "cp_reset_kernel",
-                                                "cp_extract_kernel", "cp_dense_kernel", "cp_step_kernel"};
+const std::vector<const char*> kPlanKernels = {"cp_plan_kernel", "cp_init_kernel", "cp_check_kernel",
+                                                "cp_reset_kernel", "cp_dense_kernel", "cp_step_kernel"};
 const std::vector<const char*> kParityKernels = {"cp_fk_kernel",           "cp_tej_kernel",
                                                   "cp_err_at_kernel",       "cp_project_config_kernel",
                                                   "cp_check_config_kernel", "cp_validate_kernel",
@@ -417,8 +420,10 @@ int upload_conf(Ctx* c, Module* m) {
     return 0;
 }
 
-int launch(Ctx* c, Module* m, const char* k, unsigned gx, unsigned gy, unsigned bx, size_t smem, void** args) {
-    CUresult r = drv().launchKernel(m->fn[k], gx, gy, 1, bx, 1, 1, (unsigned)smem, (CUstream)c->stream, args, nullptr);
+int launch(Ctx* c, Module* m, const char* k, unsigned gx, unsigned gy, unsigned bx, size_t smem, void** args,
+           cudaStream_t st = nullptr) {
+    CUresult r = drv().launchKernel(m->fn[k], gx, gy, 1, bx, 1, 1, (unsigned)smem, (CUstream)(st ? st : c->stream),
+                                    args, nullptr);
     if (r != CUDA_SUCCESS) return fail(CPRRTC_ECUDA, std::string("launch ") + k + ": " + cu_err(r));
     c->launches++;
     return 0;
@@ -650,7 +655,10 @@ int cprrtc_ctx_create(int device, const cprrtc_robot* robot, void** out) {
     if (prop.major != 10) return fail(CPRRTC_ENODEV, std::string("sm_100a build needs a Blackwell B200, found ") + prop.name);
     c->sms = prop.multiProcessorCount;
     CUDA_TRY(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
+    CUDA_TRY(cudaStreamCreateWithFlags(&c->stream2, cudaStreamNonBlocking));
     for (auto& e : c->ev) CUDA_TRY(cudaEventCreate(&e));
+    CUDA_TRY(cudaEventCreateWithFlags(&c->fork, cudaEventDisableTiming));
+    CUDA_TRY(cudaEventCreateWithFlags(&c->join, cudaEventDisableTiming));
     c->n = robot->n;
     c->S = robot->n_spheres;
     c->P = robot->n_pairs;
@@ -678,6 +686,9 @@ int cprrtc_ctx_destroy(void* p) {
         if (g.exec) cudaGraphExecDestroy(g.exec);
     for (auto& e : c->ev)
         if (e) cudaEventDestroy(e);
+    if (c->fork) cudaEventDestroy(c->fork);
+    if (c->join) cudaEventDestroy(c->join);
+    if (c->stream2) cudaStreamDestroy(c->stream2);
     cudaStreamDestroy(c->stream);
     delete c;
     return 0;
@@ -1145,8 +1156,10 @@ static int ensure_plan_buffers(Ctx* c, int nq, int cap, int path_cap) {
         rc = rc ? rc : c->h_paths.ensure((size_t)nq * path_cap * n * sizeof(float));
         void* sbefore = c->h_src.h;
         rc = rc ? rc : c->h_src.ensure((size_t)nq * path_cap * sizeof(int));
+        void* cbefore = c->chain.p;
+        rc = rc ? rc : c->chain.ensure((size_t)nq * path_cap * sizeof(int));
         if (before != c->d_starts.p || hbefore != c->h_in.h || obefore != c->h_out.h || pbefore != c->h_paths.h ||
-            sbefore != c->h_src.h) {
+            sbefore != c->h_src.h || cbefore != c->chain.p) {
             for (auto& g : c->graphs)
                 if (g.exec) cudaGraphExecDestroy(g.exec);
             c->graphs.clear();
@@ -1242,9 +1255,14 @@ static int plan_launch(Ctx* c, const cprrtc_params* prm, int B, const double* st
     S.parents = c->parents.as<int>();
     S.cap = cap;
     S.counters = c->counters.as<int>();
-    S.reset_tree = 1;
     // the persistent planner
     PlanArgs A = make_plan_args(c, prm, B, cap, tau);
+    A.out = c->h_out.dev<QueryOut>();
+    A.paths = c->h_paths.dev<float>();
+    A.sources = c->h_src.dev<int>();
+    A.chain = c->chain.as<int>();
+    A.path_cap = path_cap;
+    S.out = A.out;
     if (race) {
         A.race_flag = race->own;
         A.n_race = race->n;
@@ -1300,30 +1318,34 @@ static int plan_launch(Ctx* c, const cprrtc_params* prm, int B, const double* st
         int rc = 0;
         cudaMemcpyAsync(c->d_starts.p, hin, in_bytes, cudaMemcpyHostToDevice, c->stream);
         cudaEventRecordWithFlags(c->ev[0], c->stream, cudaEventRecordExternal);   // device-resident inputs from here on
+        {   // query state + roots
+            void* args[] = {&S};
+            rc = rc ? rc : launch(c, m, "cp_init_kernel", B, 1, 32, 0, args);
+        }
+        // FP64 endpoint checks on a concurrent branch (they only veto a query)
+        cudaEventRecord(c->fork, c->stream);
+        cudaStreamWaitEvent(c->stream2, c->fork, 0);
         {
             void* args[] = {&S};
-            rc = rc ? rc : launch(c, m, "cp_setup_kernel", B, 1, 256, 0, args);
+            rc = rc ? rc : launch(c, m, "cp_check_kernel", B, 1, 64, 0, args, c->stream2);
         }
+        cudaEventRecord(c->join, c->stream2);
         cudaEventRecordWithFlags(c->ev[1], c->stream, cudaEventRecordExternal);
-        {
+        {   // the persistent planner; the last team out of each query extracts its result
             void* args[] = {&A};
             rc = rc ? rc : launch(c, m, "cp_plan_kernel", grid, 1, block, smem, args);
         }
         cudaEventRecordWithFlags(c->ev[2], c->stream, cudaEventRecordExternal);
-        {
+        cudaStreamWaitEvent(c->stream, c->join, 0);
+        cudaEventRecordWithFlags(c->ev[3], c->stream, cudaEventRecordExternal);   // results complete
+        {   // NaN-refill this run's node slots for the next run (after ev[3]: the
+            // host waits on ev[3] only, so this overlaps the host's result handling)
             QueryState* qs = c->qs.as<QueryState>();
-            const float* tr = c->trees.as<float>();
-            const int* pr = c->parents.as<int>();
-            int nq = B;
-            QueryOut* out = c->h_out.dev<QueryOut>();
-            float* hp = c->h_paths.dev<float>();
-            int* hs = c->h_src.dev<int>();
-            int pc = path_cap;
-            int capv = cap;
-            void* args[] = {&qs, &tr, &pr, &capv, &nq, &out, &hp, &hs, &pc};
-            rc = rc ? rc : launch(c, m, "cp_extract_kernel", (B + 3) / 4, 1, 128, 0, args);
+            float* tr = c->trees.as<float>();
+            int capv = cap, nq = B;
+            void* args[] = {&qs, &tr, &capv, &nq};
+            rc = rc ? rc : launch(c, m, "cp_reset_kernel", 8, (unsigned)std::min(2 * B, 65535), 256, 0, args);
         }
-        cudaEventRecordWithFlags(c->ev[3], c->stream, cudaEventRecordExternal);
         cudaGraph_t graph = nullptr;
         cudaError_t e = cudaStreamEndCapture(c->stream, &graph);
         c->launches = launches0;
@@ -1348,7 +1370,7 @@ static int plan_launch(Ctx* c, const cprrtc_params* prm, int B, const double* st
         G = &c->graphs.back();
     }
     CUDA_TRY(cudaGraphLaunch(G->exec, c->stream));
-    c->launches += 3;   // setup, plan, extract
+    c->launches += 4;   // init, check, plan, reset
     c->last_args = A;
     c->last_mod = m;
     c->last_nq = B;
@@ -1357,7 +1379,10 @@ static int plan_launch(Ctx* c, const cprrtc_params* prm, int B, const double* st
 
 static int plan_collect(Ctx* c, int B, cprrtc_result* results, double* paths, int32_t* sources) {
     if (int rc = set_device(c)) return rc;
-    if (int rc = sync(c)) return rc;
+    {   // results are complete at ev[3]; the tree refill behind it may still run
+        cudaError_t e = cudaEventSynchronize(c->ev[3]);
+        if (e != cudaSuccess) return fail(CPRRTC_ECUDA, std::string("kernel failed: ") + cudaGetErrorString(e));
+    }
     const int n = c->n;
     const int path_cap = c->path_cap;
     float t_all = 0, t_plan = 0;
@@ -1370,9 +1395,9 @@ static int plan_collect(Ctx* c, int B, cprrtc_result* results, double* paths, in
     const int* hs = c->h_src.host<int>();
     for (int i = 0; i < B; i++) {
         cprrtc_result& r = results[i];
-        r.status = out[i].status;
         r.setup_code = out[i].setup_code;
-        r.path_len = out[i].path_len;
+        r.status = r.setup_code ? -1 : out[i].status;
+        r.path_len = r.status == 0 ? out[i].path_len : 0;
         r.nodes_start = out[i].n_nodes[0];
         r.nodes_goal = out[i].n_nodes[1];
         r.device_ms = out[i].device_ms;

@@ -12,10 +12,10 @@ feas = np.nonzero(fx.upright_feasible())[0][:20]
 probs = [PlanProblem(m, sc, sp, p["upright_start"][k], p["upright_goal"][k], PlanParams(width=16, max_iterations=10**6, seed_offset=int(k))) for k in feas]
 ctx = prepare(probs[0])
 for pr in probs[:5]: plan(pr)
-walls, devs, cwall = [], [], []
+walls, devs, cwall, kerns = [], [], [], []
 for pr in probs * 3:
     t0 = time.perf_counter(); r = plan(pr); walls.append((time.perf_counter() - t0) * 1e3)
-    devs.append(ctx.last_timing()[0])
+    devs.append(ctx.last_timing()[0]); kerns.append(ctx.last_timing()[1])
 prm = _params_struct(probs[0].params, DeviceOptions())
 res = (_lib.Result * 1)(); paths = np.empty((1, 1024, 7)); src = np.empty((1, 1024), np.int32)
 for pr in probs * 3:
@@ -28,4 +28,5 @@ for _ in range(200): _bind(probs[0], DeviceOptions())
 bind_us = (time.perf_counter() - t0) / 200 * 1e6
 print(f"plan() wall median {np.median(walls):.3f} ms, device {np.median(devs):.3f} ms, "
       f"host overhead {np.median(np.array(walls) - np.array(devs)) * 1e3:.0f} us; "
-      f"C-ABI call overhead {np.median(cwall) * 1e3:.0f} us; _bind {bind_us:.0f} us")
+      f"C-ABI call overhead {np.median(cwall) * 1e3:.0f} us; _bind {bind_us:.0f} us; "
+      f"device time outside the plan kernel {np.median(np.array(devs) - np.array(kerns)) * 1e3:.1f} us")
