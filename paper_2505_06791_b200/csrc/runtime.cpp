@@ -335,6 +335,7 @@ struct Ctx {
     };
     std::vector<PlanGraph> graphs;
     double last_total_ms = 0, last_plan_ms = 0;
+    bool timing_pending = false;   // last_*_ms still to be read from ev[0..3] (last plan call)
     int64_t launches = 0;
 };
 
@@ -783,6 +784,14 @@ int64_t cprrtc_launch_count(void* p) { return p ? C(p)->launches : 0; }
 int cprrtc_last_timing(void* p, double* total_ms, double* plan_ms) {
     Ctx* c = C(p);
     if (!c) return fail(CPRRTC_EARG, "NULL context");
+    if (c->timing_pending) {
+        float t_all = 0, t_plan = 0;
+        cudaEventElapsedTime(&t_all, c->ev[0], c->ev[3]);
+        cudaEventElapsedTime(&t_plan, c->ev[1], c->ev[2]);
+        c->last_total_ms = t_all;
+        c->last_plan_ms = t_plan;
+        c->timing_pending = false;
+    }
     if (total_ms) *total_ms = c->last_total_ms;
     if (plan_ms) *plan_ms = c->last_plan_ms;
     return 0;
@@ -965,6 +974,7 @@ static int validate_impl(void* p, int B, int W, const double* wps, int flag_on, 
         cudaEventElapsedTime(&t, c->ev[1], c->ev[2]);
         c->last_plan_ms = t;
         c->last_total_ms = t;
+        c->timing_pending = false;
     }
     if (possible) {
         const int64_t per = (int64_t)c->S * (c->nb + c->ne) + c->P;
@@ -1103,6 +1113,7 @@ int cprrtc_nearest_trees(void* p, int N, int n_trees, const float* unused, const
     float t = 0;
     cudaEventElapsedTime(&t, c->ev[1], c->ev[2]);
     c->last_plan_ms = c->last_total_ms = t;
+    c->timing_pending = false;
     return 0;
 }
 
@@ -1385,11 +1396,7 @@ static int plan_collect(Ctx* c, int B, cprrtc_result* results, double* paths, in
     }
     const int n = c->n;
     const int path_cap = c->path_cap;
-    float t_all = 0, t_plan = 0;
-    cudaEventElapsedTime(&t_all, c->ev[0], c->ev[3]);
-    cudaEventElapsedTime(&t_plan, c->ev[1], c->ev[2]);
-    c->last_total_ms = t_all;
-    c->last_plan_ms = t_plan;
+    c->timing_pending = true;   // event times are read only when asked for (cprrtc_last_timing)
     const QueryOut* out = c->h_out.host<QueryOut>();
     const float* hp = c->h_paths.host<float>();
     const int* hs = c->h_src.host<int>();

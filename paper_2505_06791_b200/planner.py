@@ -345,10 +345,7 @@ def plan_batch(problems, options: DeviceOptions = DeviceOptions(), return_dense:
                                      _lib.ptr(seeds, _lib._lp), res, _lib.ptr(paths),
                                      _lib.ptr(srcs, _lib._ip)), "plan")
         wall = (time.perf_counter() - t0) * 1e3
-    if B == 1:
-        out = [_result(res[0], p0, paths[0], srcs[0], wall, B, pc)]
-    else:
-        out = _results_bulk(res, problems, paths, srcs, wall, pc)
+    out = _results_bulk(res, problems, paths, srcs, wall, pc)
     if return_dense:
         for i, r in enumerate(out):
             if r.solved:
@@ -402,6 +399,8 @@ def _results_bulk(res, problems, paths, srcs, wall, pc):
             out.append(PlanResult("Solved", tuple(path), tuple(_SRC[k] for k in srcs[i, :L - 1].tolist()),
                                   stats))
         elif code == -1:
+            if len(problems) == 1:
+                raise PlanSetupError(_SETUP.get(int(a["setup_code"][0]), "invalid start/goal"))
             out.append(PlanResult("Error:PlanSetupError", None, None, stats))
         elif code == 4:
             raise RuntimeError(f"solution path longer than path_capacity={pc}")
@@ -476,7 +475,7 @@ def _plan_one(problem: PlanProblem, options: DeviceOptions, return_dense: bool) 
         rc = ctx.L.cprrtc_plan(ctx.h, C.byref(prm), 1, *io.args)
         wall = (time.perf_counter() - t0) * 1e3
         _lib.check(rc, "plan")
-        res = _result(io.res[0], problem, io.paths[0], io.srcs[0], wall, 1, pc)
+        res = _results_bulk(io.res, (problem,), io.paths, io.srcs, wall, pc)[0]
         if return_dense and res.solved:
             L = len(res.path)
             dense, ok = _derive(ctx, prm, io.paths[0, :L], io.srcs[0, :L - 1])
