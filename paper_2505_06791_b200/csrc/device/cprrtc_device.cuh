@@ -518,14 +518,18 @@ __device__ __noinline__ bool cp_project(const Team tm, float (*seg)[CP_NP], int 
         if (ok) { prog = W - 1; iters = total; }
     } else {
         const bool unconstrained = !(pa.tau_task_dev < cp_inf());
+        // each lane keeps its row in registers across iterations and takes the
+        // previous row from lane t-1 by shuffle (no shared-memory round trip);
+        // the rows go back to seg when the loop ends
+        float xc[CP_N];
+#pragma unroll
+        for (int k = 0; k < CP_N; k++) xc[k] = row ? seg[t][k] : 0.f;
         for (int it = 1; it <= pa.max_iters; it++) {
             const bool act = row && t > prog;
-            float xn[CP_N], xt[CP_N], xp[CP_N];
-            bool valid = false, full_step = true;
-            if (act) {
+            float xn[CP_N], xp[CP_N];
 #pragma unroll
-                for (int k = 0; k < CP_N; k++) { xt[k] = seg[t][k]; xp[k] = seg[t - 1][k]; }
-            }
+            for (int k = 0; k < CP_N; k++) xp[k] = __shfl_up_sync(tm.mask, xc[k], 1, CP_G);
+            bool valid = false, full_step = true;
             if (unconstrained) {
                 // tau_task = inf: validity needs no FK (pure.py:545); the
                 // update is computed only if the segment is not accepted as is.
@@ -534,12 +538,12 @@ __device__ __noinline__ bool cp_project(const Team tm, float (*seg)[CP_NP], int 
                     float s2 = 0.f;
                     bool fin = true;
 #pragma unroll
-                    for (int k = 0; k < CP_N; k++) { float d = xt[k] - xp[k]; s2 += d * d; fin &= cp_finite(xt[k]); }
+                    for (int k = 0; k < CP_N; k++) { float d = xc[k] - xp[k]; s2 += d * d; fin &= cp_finite(xc[k]); }
                     cheap = fin && sqrtf(s2) < tau_sm * 0.99999f;
                 }
                 if (!tm.any(!cheap)) { valid = act; full_step = false; }
             }
-            if (full_step && act) valid = cp_stage1(pa, xt, xp, tau_sm, xn);
+            if (full_step && act) valid = cp_stage1(pa, xc, xp, tau_sm, xn);
             if (full_step && act) s1++;   // per lane; summed over the team at the end
             unsigned vm = tm.ballot(act && valid) & full;
             int np = prog;
@@ -556,7 +560,7 @@ __device__ __noinline__ bool cp_project(const Team tm, float (*seg)[CP_NP], int 
                 if (trace) {
                     if (row) {
 #pragma unroll
-                        for (int k = 0; k < CP_N; k++) trace[((size_t)(it - 1) * W + t) * CP_N + k] = seg[t][k];
+                        for (int k = 0; k < CP_N; k++) trace[((size_t)(it - 1) * W + t) * CP_N + k] = xc[k];
                     }
                     if (t == 0) trace_prog[it - 1] = np;
                 }
@@ -565,21 +569,25 @@ __device__ __noinline__ bool cp_project(const Team tm, float (*seg)[CP_NP], int 
                 prog = np;
                 break;
             }
-            tm.sync();
             if (row && t > np) {
 #pragma unroll
-                for (int k = 0; k < CP_N; k++) seg[t][k] = xn[k];
+                for (int k = 0; k < CP_N; k++) xc[k] = xn[k];
             }
-            tm.sync();
             prog = np;
             if (trace) {
                 if (row) {
 #pragma unroll
-                    for (int k = 0; k < CP_N; k++) trace[((size_t)(it - 1) * W + t) * CP_N + k] = seg[t][k];
+                    for (int k = 0; k < CP_N; k++) trace[((size_t)(it - 1) * W + t) * CP_N + k] = xc[k];
                 }
                 if (t == 0) trace_prog[it - 1] = np;
             }
         }
+        tm.sync();
+        if (row) {
+#pragma unroll
+            for (int k = 0; k < CP_N; k++) seg[t][k] = xc[k];
+        }
+        tm.sync();
     }
     if (ok) {
         // clamp to limits; if anything moved, re-check both tolerances
