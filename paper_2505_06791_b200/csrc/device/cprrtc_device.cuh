@@ -706,8 +706,10 @@ __device__ __noinline__ ValOut cp_validate(const Team tm, const float (*seg)[CP_
             float rq[CP_SB];
 #pragma unroll
             for (int u = 0; u < CP_SB; u++) {
+                // a missing last sphere sits far from everything, including the
+                // +1e18 padding primitives of the staged scene
                 const bool in = s + u < CP_S;
-                cq[u] = in ? sp[s + u] : make_float4(1e18f, 1e18f, 1e18f, 0.f);
+                cq[u] = in ? sp[s + u] : make_float4(-3e18f, -3e18f, -3e18f, 0.f);
                 rq[u] = (in ? cp_rad_tab[s + u] : 0.f) + margin;
             }
 #pragma unroll 1

@@ -253,3 +253,21 @@ def test_check_config_codes(K):
     bad[1, 1] += 0.3            # shoulder lift: leaves the plane
     codes = K.check_config_batch(m, sc, sp, bad[:2])
     assert codes[0] == 1 and codes[1] == 2
+
+
+@pytest.mark.parametrize("margin", [0.0, 1e-5])
+def test_validate_flag_off_matches_flag_on_verdicts(K, margin):
+    """Flag off (sphere-pair order) and flag on (lockstep) give the same
+    verdicts and first colliding waypoint, for an odd robot-sphere count
+    (arm8: 9) in scenes whose staged primitive lists are padded, with and
+    without the planner's sphere margin."""
+    for rname, scname in (("arm8", "table"), ("arm8", "shelf_x11"), ("arm7", "posts"), ("arm8_dense", "table")):
+        m, sc = fx.robot(rname), fx.scene(scname)
+        qs = K.halton_batch(m, 1024, 1, 4242)
+        t = np.linspace(0.0, 1.0, 16)[None, :, None]
+        wps = qs[0::2][:, None, :] * (1 - t) + qs[1::2][:, None, :] * t
+        off = K.validate_batch(m, sc, wps, False, margin=margin)
+        on = K.validate_batch(m, sc, wps, True, margin=margin)
+        assert np.array_equal(off["valid"], on["valid"]), (rname, scname)
+        assert np.array_equal(off["first_bad"], on["first_bad"]), (rname, scname)
+        assert 0.05 < off["valid"].mean() < 1.0 or scname == "table"

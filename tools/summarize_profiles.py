@@ -47,6 +47,7 @@ def num(x):
 lines = [f"# ncu summary ({TAG}) -- B200, `ncu --set full --clock-control none`", ""]
 traffic = {}
 for kern, rep in (("cp_plan_kernel", f"prof_plan_{TAG}.ncu-rep"), ("cp_validate_kernel", f"prof_cc_{TAG}.ncu-rep"),
+                  ("cp_validate_cull_kernel", f"prof_cull_{TAG}.ncu-rep"),
                   ("cp_nearest_kernel", f"prof_nn_{TAG}.ncu-rep")):
     path = os.path.join(G, rep)
     if not os.path.exists(path):
