@@ -622,6 +622,7 @@ __device__ __noinline__ bool cp_project(const Team tm, float (*seg)[CP_NP], int 
             if (tm.any(!good)) {
                 ok = false;
                 iters = pa.max_iters;
+                tm.sync();   // every lane's read of seg[t - 1] above precedes the restore
                 if (row) {
 #pragma unroll
                     for (int k = 0; k < CP_N; k++) seg[t][k] = q[k];
