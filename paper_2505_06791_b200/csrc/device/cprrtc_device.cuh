@@ -26,9 +26,6 @@
 #define CP_M ((CP_KIND == 0 ? 1 : 2) + (CP_ORIENT ? 3 : 0))
 #define CP_NP ((CP_N % 2) ? CP_N : (CP_N + 1))   // odd row pitch: no bank conflicts
 #define CP_CHUNK 8
-// robot spheres per staged primitive load in flag-off CC (r1 A/B on 999 boxes,
-// 16384 motions: 1 / 2 / 4 -> 1.66 / 2.00 / 1.74 T checks/s)
-#define CP_SB 2
 #define CP_BCH (2 + 2 * CP_CHUNK)   // float4s per box chunk of the clustered scene
 #define CP_SCH (2 + CP_CHUNK)       // float4s per sphere chunk
 #define CP_INTMAX 0x7fffffff
@@ -671,6 +668,108 @@ __device__ __forceinline__ bool cp_hit_sph(float cx, float cy, float cz, float r
     return fmaf(dx, dx, fmaf(dy, dy, dz * dz)) < rr * rr;
 }
 
+// The environment checks of cp_validate for one flag setting (compile-time,
+// so the flag-off pass carries no votes): updates first_r (smallest round with
+// a hit), rounds_done (checks per waypoint row evaluated) and stop.
+template <bool FLAG>
+__device__ __forceinline__ void cp_env_pass(const Team& tm, const float4* sp, bool mine, float margin,
+                                            const SceneSm& sc, int E, int& first_r, i64& rounds_done,
+                                            bool& stop) {
+    // Robot spheres go in pairs (s, s+1) that share every staged primitive
+    // load.  first_r is the smallest sphere-major round with a hit (the
+    // reference's first detection, pure.py:664-698) whatever the evaluation
+    // order.  With the flag on the team stops exactly when no smaller round
+    // can still hit: a sphere-s hit ends the pass at once; a sphere-(s+1) hit
+    // first lets sphere s finish its primitives alone (its later rounds are
+    // still smaller), then ends the pass.  The votes are the paper's shared
+    // collision flag, taken once per chunk.
+#pragma unroll 1
+    for (int s = 0; s < CP_S && !stop; s += 2) {
+        const bool two = s + 1 < CP_S;
+        const float4 c0 = sp[s];
+        // a missing second sphere sits far from everything, including the
+        // +1e18 padding primitives of the staged scene
+        const float4 c1 = two ? sp[s + 1] : make_float4(-3e18f, -3e18f, -3e18f, 0.f);
+        const float ra = cp_rad_tab[s] + margin, rb = (two ? cp_rad_tab[s + 1] : 0.f) + margin;
+        const float r0 = ra * ra, r1 = rb * rb;
+        const int rb0 = s * E, rb1 = (s + 1) * E;
+        const int per_chunk = two ? 2 * CP_CHUNK : CP_CHUNK;
+        bool only0 = false;
+#pragma unroll 1
+        for (int p0 = 0; p0 < sc.nb && !stop; p0 += CP_CHUNK) {
+            bool a0 = false, a1 = false;
+            if (!only0) {
+#pragma unroll
+                for (int j = 0; j < CP_CHUNK; j++) {
+                    const float4 bc = cp_lds4(sc.box_c + p0 + j), bh = cp_lds4(sc.box_h + p0 + j);
+                    a0 |= cp_hit_box(c0.x, c0.y, c0.z, r0, bc, bh);
+                    a1 |= cp_hit_box(c1.x, c1.y, c1.z, r1, bc, bh);
+                }
+                rounds_done += per_chunk;
+            } else {
+#pragma unroll
+                for (int j = 0; j < CP_CHUNK; j++)
+                    a0 |= cp_hit_box(c0.x, c0.y, c0.z, r0, cp_lds4(sc.box_c + p0 + j), cp_lds4(sc.box_h + p0 + j));
+                rounds_done += CP_CHUNK;
+            }
+            if (mine && a0 && rb0 + p0 < first_r) {   // rare: locate the hit
+                for (int j = 0; j < CP_CHUNK; j++)
+                    if (cp_hit_box(c0.x, c0.y, c0.z, r0, sc.box_c[p0 + j], sc.box_h[p0 + j])) {
+                        first_r = min(first_r, rb0 + p0 + j);
+                        break;
+                    }
+            }
+            if (mine && a1 && rb1 + p0 < first_r) {
+                for (int j = 0; j < CP_CHUNK; j++)
+                    if (cp_hit_box(c1.x, c1.y, c1.z, r1, sc.box_c[p0 + j], sc.box_h[p0 + j])) {
+                        first_r = min(first_r, rb1 + p0 + j);
+                        break;
+                    }
+            }
+            if (FLAG) {
+                if (tm.any(first_r < rb1)) stop = true;
+                else if (tm.any(first_r != CP_INTMAX)) only0 = true;
+            }
+        }
+#pragma unroll 1
+        for (int p0 = 0; p0 < sc.ne && !stop; p0 += CP_CHUNK) {
+            bool a0 = false, a1 = false;
+            if (!only0) {
+#pragma unroll
+                for (int j = 0; j < CP_CHUNK; j++) {
+                    const float4 o = cp_lds4(sc.sph + p0 + j);
+                    a0 |= cp_hit_sph(c0.x, c0.y, c0.z, ra, o);
+                    a1 |= cp_hit_sph(c1.x, c1.y, c1.z, rb, o);
+                }
+                rounds_done += per_chunk;
+            } else {
+#pragma unroll
+                for (int j = 0; j < CP_CHUNK; j++) a0 |= cp_hit_sph(c0.x, c0.y, c0.z, ra, cp_lds4(sc.sph + p0 + j));
+                rounds_done += CP_CHUNK;
+            }
+            if (mine && a0 && rb0 + sc.nb + p0 < first_r) {
+                for (int j = 0; j < CP_CHUNK; j++)
+                    if (cp_hit_sph(c0.x, c0.y, c0.z, ra, sc.sph[p0 + j])) {
+                        first_r = min(first_r, rb0 + sc.nb + p0 + j);
+                        break;
+                    }
+            }
+            if (mine && a1 && rb1 + sc.nb + p0 < first_r) {
+                for (int j = 0; j < CP_CHUNK; j++)
+                    if (cp_hit_sph(c1.x, c1.y, c1.z, rb, sc.sph[p0 + j])) {
+                        first_r = min(first_r, rb1 + sc.nb + p0 + j);
+                        break;
+                    }
+            }
+            if (FLAG) {
+                if (tm.any(first_r < rb1)) stop = true;
+                else if (tm.any(first_r != CP_INTMAX)) only0 = true;
+            }
+        }
+        if (only0) stop = true;   // sphere s is clean: the first sphere-(s+1) hit is the first detection
+    }
+}
+
 // Validate rows [t_first, W) of seg.  Lanes run in lockstep over the
 // reference's check order (robot sphere major, boxes then spheres, then the
 // self pairs), so a team vote after every CP_CHUNK rounds both implements the
@@ -694,107 +793,11 @@ __device__ __noinline__ ValOut cp_validate(const Team tm, const float (*seg)[CP_
         for (int s = 0; s < CP_S; s++) sp[s] = make_float4(SPH[3 * s], SPH[3 * s + 1], SPH[3 * s + 2], 0.f);
     }
     int first_r = CP_INTMAX;
-    i64 rounds_done = 0;
+    i64 rounds_done = 0;   // checks per waypoint row this team evaluated (team-uniform)
     bool stop = false;
-    if (!flag_on) {
-        // Flag off: every check is performed, so the order is free -- robot
-        // spheres go in groups of CP_SB and share each staged primitive load
-        // (one LDS.128 pair per CP_SB checks).  first_r is still the smallest
-        // (sphere-major) round with a hit, i.e. the reference's first detection.
-#pragma unroll 1
-        for (int s = 0; s < CP_S; s += CP_SB) {
-            float4 cq[CP_SB];
-            float rq[CP_SB];
-#pragma unroll
-            for (int u = 0; u < CP_SB; u++) {
-                // a missing last sphere sits far from everything, including the
-                // +1e18 padding primitives of the staged scene
-                const bool in = s + u < CP_S;
-                cq[u] = in ? sp[s + u] : make_float4(-3e18f, -3e18f, -3e18f, 0.f);
-                rq[u] = (in ? cp_rad_tab[s + u] : 0.f) + margin;
-            }
-#pragma unroll 1
-            for (int p0 = 0; p0 < sc.nb; p0 += CP_CHUNK) {
-                bool a[CP_SB];
-#pragma unroll
-                for (int u = 0; u < CP_SB; u++) a[u] = false;
-#pragma unroll
-                for (int j = 0; j < CP_CHUNK; j++) {
-                    const float4 bc = cp_lds4(sc.box_c + p0 + j), bh = cp_lds4(sc.box_h + p0 + j);
-#pragma unroll
-                    for (int u = 0; u < CP_SB; u++) a[u] |= cp_hit_box(cq[u].x, cq[u].y, cq[u].z, rq[u] * rq[u], bc, bh);
-                }
-#pragma unroll
-                for (int u = 0; u < CP_SB; u++)
-                    if (mine && a[u] && (s + u) * E + p0 < first_r) {   // rare: locate the hit
-                        for (int j = 0; j < CP_CHUNK; j++)
-                            if (cp_hit_box(cq[u].x, cq[u].y, cq[u].z, rq[u] * rq[u], sc.box_c[p0 + j], sc.box_h[p0 + j])) {
-                                first_r = min(first_r, (s + u) * E + p0 + j);
-                                break;
-                            }
-                    }
-            }
-#pragma unroll 1
-            for (int p0 = 0; p0 < sc.ne; p0 += CP_CHUNK) {
-                bool a[CP_SB];
-#pragma unroll
-                for (int u = 0; u < CP_SB; u++) a[u] = false;
-#pragma unroll
-                for (int j = 0; j < CP_CHUNK; j++) {
-                    const float4 o = cp_lds4(sc.sph + p0 + j);
-#pragma unroll
-                    for (int u = 0; u < CP_SB; u++) a[u] |= cp_hit_sph(cq[u].x, cq[u].y, cq[u].z, rq[u], o);
-                }
-#pragma unroll
-                for (int u = 0; u < CP_SB; u++)
-                    if (mine && a[u] && (s + u) * E + sc.nb + p0 < first_r) {
-                        for (int j = 0; j < CP_CHUNK; j++)
-                            if (cp_hit_sph(cq[u].x, cq[u].y, cq[u].z, rq[u], sc.sph[p0 + j])) {
-                                first_r = min(first_r, (s + u) * E + sc.nb + p0 + j);
-                                break;
-                            }
-                    }
-            }
-        }
-        rounds_done = (i64)CP_S * E;
-        stop = true;   // skip the lockstep loop below (self pairs still run)
-    }
-#pragma unroll 1
-    for (int s = 0; s < CP_S && !stop; s++) {
-        const float4 c = sp[s];
-        const float r = cp_rad_tab[s] + margin, r2 = r * r;
-        const int rbase = s * E;
-        // boxes, then obstacle spheres (reference order, pure.py:674-693), in
-        // chunks of CP_CHUNK checks: hits of a chunk collect in a bitmask and
-        // the team votes once per chunk (the early-exit flag)
-#pragma unroll 1
-        for (int p0 = 0; p0 < sc.nb; p0 += CP_CHUNK) {
-            bool any = false;
-#pragma unroll
-            for (int j = 0; j < CP_CHUNK; j++) any |= cp_hit_box(c.x, c.y, c.z, r2, cp_lds4(sc.box_c + p0 + j), cp_lds4(sc.box_h + p0 + j));
-            if (mine && any && first_r == CP_INTMAX) {       // rare: locate the first hit of the chunk
-                for (int j = 0; j < CP_CHUNK; j++)
-                    if (cp_hit_box(c.x, c.y, c.z, r2, sc.box_c[p0 + j], sc.box_h[p0 + j])) { first_r = rbase + p0 + j; break; }
-            }
-            rounds_done = rbase + min(p0 + CP_CHUNK, sc.nb);
-            if (flag_on && tm.any(first_r != CP_INTMAX)) { stop = true; break; }
-        }
-        if (stop) break;
-#pragma unroll 1
-        for (int p0 = 0; p0 < sc.ne; p0 += CP_CHUNK) {
-            bool any = false;
-#pragma unroll
-            for (int j = 0; j < CP_CHUNK; j++) any |= cp_hit_sph(c.x, c.y, c.z, r, cp_lds4(sc.sph + p0 + j));
-            if (mine && any && first_r == CP_INTMAX) {
-                for (int j = 0; j < CP_CHUNK; j++)
-                    if (cp_hit_sph(c.x, c.y, c.z, r, sc.sph[p0 + j])) { first_r = rbase + sc.nb + p0 + j; break; }
-            }
-            rounds_done = rbase + sc.nb + min(p0 + CP_CHUNK, sc.ne);
-            if (flag_on && tm.any(first_r != CP_INTMAX)) { stop = true; break; }
-        }
-        if (!stop) rounds_done = rbase + E;
-    }
-    if ((!stop || !flag_on) && CP_P > 0) {
+    if (flag_on) cp_env_pass<true>(tm, sp, mine, margin, sc, E, first_r, rounds_done, stop);
+    else cp_env_pass<false>(tm, sp, mine, margin, sc, E, first_r, rounds_done, stop);
+    if (!stop && CP_P > 0) {
         const int rbase = CP_S * E;
 #pragma unroll 1
         for (int k = 0; k < CP_P; k++) {
@@ -805,7 +808,7 @@ __device__ __noinline__ ValOut cp_validate(const Team tm, const float (*seg)[CP_
             bool hit = fmaf(dx, dx, fmaf(dy, dy, dz * dz)) < rr * rr;
             if (mine && hit && first_r == CP_INTMAX) first_r = rbase + k;
         }
-        rounds_done = rbase + CP_P;
+        rounds_done += CP_P;
     }
     ValOut o;
     int key = first_r, idx = t;
