@@ -403,6 +403,7 @@ def _cfg_problems(name):
 def other_configs(args, local):
     """Median device planning time + success for configs[0], [2], [3] (a few
     queries each, three seeds per query), with the CPU reference beside it."""
+    import fixtures as fx
     from paper_2505_06791_b200.planner import DeviceOptions, PlanParams, PlanProblem, plan, prepare
     res = {}
     for name in ("configs[0]", "configs[2]:shelf_x11", "configs[2]:shelf_x111", "configs[3]"):
@@ -413,10 +414,12 @@ def other_configs(args, local):
         variants = ((("on", -1, ""), ("off", -1, " (cc flag off)"), ("on", 0, " (lockstep order)"),
                      ("off", 0, " (lockstep order, cc flag off)"))
                     if name.startswith("configs[2]") else (("on", -1, ""),))
+        feas = fx.dense8_feasible() if name == "configs[3]" else None
         for flag, bp, suffix in variants:
             tflag = []
+            nfeas = sfeas = 0
             opt = DeviceOptions(device=local, cc_broadphase=bp)
-            for (m, sc, sp, s, g, kw) in probs:
+            for qi, (m, sc, sp, s, g, kw) in enumerate(probs):
                 for seed in range(3):
                     p = PlanProblem(m, sc, sp, s, g, PlanParams(max_iterations=10**6, time_budget_ms=2000.0,
                                                                 seed_offset=seed * 10_000, flag_mode=flag, **kw))
@@ -427,8 +430,16 @@ def other_configs(args, local):
                     if r.solved:
                         solved += 1
                         tflag.append(ctx.last_timing()[0])
+                    if feas is not None and feas[qi]:
+                        nfeas += 1
+                        sfeas += r.solved
             res[name + suffix] = {"workload": label, "median_ms": float(np.median(tflag)) if tflag else None,
                                   "queries": len(probs) * 3, "success_rate": len(tflag) / (len(probs) * 3)}
+            if feas is not None:
+                res[name + suffix]["success_rate_feasible"] = sfeas / max(1, nfeas)
+                res[name + suffix]["feasible_note"] = (
+                    f"{int((~feas).sum())} of the {len(feas)} pairs are unsolved by the reference planner too "
+                    "(3 seeds x 20 s, tests/golden/dense8_feasibility.json)")
         if not args.no_cpu:
             cpu = []
             ok = 0
