@@ -2,7 +2,7 @@
 # ncu captures for profiles/ (run under gpurun; one GPU).  Usage: tools/profile.sh <tag>
 TAG=${1:-r1}
 mkdir -p gpurun_out
-python tools/dump_src.py > /dev/null
+python tools/dump_src.py > /dev/null && cp cprrtc-*.cu gpurun_out/
 timeout 900 python bench.py > gpurun_out/bench_$TAG.json 2> gpurun_out/bench_$TAG.err
 timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches_$TAG.csv \
     python bench.py --steps 1 --warmup 1 --queries 5 --no-extras --no-cpu > gpurun_out/ncu_launches_$TAG.log 2>&1
