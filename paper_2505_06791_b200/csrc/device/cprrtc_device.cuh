@@ -105,11 +105,19 @@ template <class T> struct CpDiv {
     static __device__ __forceinline__ T piv(T x) { return x; }           // stored pivot
     static __device__ __forceinline__ T div(T a, T p) { return a / p; }  // a / pivot
     static __device__ __forceinline__ T sqrt_piv(T x) { return sqrt(x); }
+    // s = 2 sqrt(x) and its pivot
+    static __device__ __forceinline__ T twice_sqrt(T x, T& p) { T s = sqrt(x) * T(2); p = s; return s; }
 };
 template <> struct CpDiv<float> {
     static __device__ __forceinline__ float piv(float x) { return __fdividef(1.f, x); }
     static __device__ __forceinline__ float div(float a, float p) { return a * p; }
     static __device__ __forceinline__ float sqrt_piv(float x) { return rsqrtf(x); }
+    // one MUFU.RSQ gives both 2 sqrt(x) and 1 / (2 sqrt(x))
+    static __device__ __forceinline__ float twice_sqrt(float x, float& p) {
+        const float r = rsqrtf(x);
+        p = 0.5f * r;
+        return 2.f * (x * r);
+    }
 };
 
 // rotation -> quaternion, w >= 0 (maniplan/_kernels/pure.py:130-159)
@@ -118,23 +126,23 @@ __device__ __forceinline__ void cp_quat(const T* r, T* q) {
     T w, x, y, z, s;
     T tr = (r[0] + r[4]) + r[8];
     if (tr > T(0)) {
-        s = sqrt(tr + T(1)) * T(2);
-        const T is = CpDiv<T>::piv(s);
+        T is;
+        s = CpDiv<T>::twice_sqrt(tr + T(1), is);
         w = T(0.25) * s; x = CpDiv<T>::div(r[7] - r[5], is); y = CpDiv<T>::div(r[2] - r[6], is);
         z = CpDiv<T>::div(r[3] - r[1], is);
     } else if (r[0] > r[4] && r[0] > r[8]) {
-        s = sqrt(((T(1) + r[0]) - r[4]) - r[8]) * T(2);
-        const T is = CpDiv<T>::piv(s);
+        T is;
+        s = CpDiv<T>::twice_sqrt(((T(1) + r[0]) - r[4]) - r[8], is);
         w = CpDiv<T>::div(r[7] - r[5], is); x = T(0.25) * s; y = CpDiv<T>::div(r[1] + r[3], is);
         z = CpDiv<T>::div(r[2] + r[6], is);
     } else if (r[4] > r[8]) {
-        s = sqrt(((T(1) + r[4]) - r[0]) - r[8]) * T(2);
-        const T is = CpDiv<T>::piv(s);
+        T is;
+        s = CpDiv<T>::twice_sqrt(((T(1) + r[4]) - r[0]) - r[8], is);
         w = CpDiv<T>::div(r[2] - r[6], is); x = CpDiv<T>::div(r[1] + r[3], is); y = T(0.25) * s;
         z = CpDiv<T>::div(r[5] + r[7], is);
     } else {
-        s = sqrt(((T(1) + r[8]) - r[0]) - r[4]) * T(2);
-        const T is = CpDiv<T>::piv(s);
+        T is;
+        s = CpDiv<T>::twice_sqrt(((T(1) + r[8]) - r[0]) - r[4], is);
         w = CpDiv<T>::div(r[3] - r[1], is); x = CpDiv<T>::div(r[2] + r[6], is);
         y = CpDiv<T>::div(r[5] + r[7], is); z = T(0.25) * s;
     }
@@ -143,16 +151,20 @@ __device__ __forceinline__ void cp_quat(const T* r, T* q) {
 }
 
 // rotation-vector scale k = 2 atan2(vn, rw) / vn of a unit quaternion with
-// rw, vn >= 0 (pure.py:338-344).  FP32: atan(x)/x on x in [0, 1] as a
+// rw, vn >= 0, from s2 = vn^2 (pure.py:338-344).  FP32: atan(x)/x on x in [0, 1] as a
 // degree-8 polynomial in x^2 (max relative error 9e-8, fitted for this file),
 // with the reflection atan(x) = pi/2 - atan(1/x) above 1.
-template <class T> __device__ __forceinline__ T cp_rotscale(T vn, T rw) {
+template <class T> __device__ __forceinline__ T cp_rotscale(T s2, T rw) {
+    const T vn = sqrt(s2);
     return vn < T(1e-12) ? T(2) : T(2) * atan2(vn, rw) / vn;
 }
-template <> __device__ __forceinline__ float cp_rotscale<float>(float vn, float rw) {
-    if (vn < 1e-12f) return 2.f;
+template <> __device__ __forceinline__ float cp_rotscale<float>(float s2, float rw) {
+    // s2 = |v|^2: 1/|v| and 1/w are independent MUFU ops (no sqrt -> divide chain)
+    const float ivn = rsqrtf(s2), irw = __fdividef(1.f, rw);
+    const float vn = s2 * ivn;
+    if (!(s2 >= 1e-24f)) return 2.f;   // |v| < 1e-12 (pure.py:343)
     const bool sw = vn > rw;
-    const float x = sw ? __fdividef(rw, vn) : __fdividef(vn, rw);
+    const float x = sw ? rw * ivn : vn * irw;
     const float u = x * x;
     float p = 0.0028531861025840044f;
     p = fmaf(p, u, -0.016082055866718292f);
@@ -163,7 +175,7 @@ template <> __device__ __forceinline__ float cp_rotscale<float>(float vn, float 
     p = fmaf(p, u, 0.19992651045322418f);
     p = fmaf(p, u, -0.33333075046539307f);
     p = fmaf(p, u, 1.0f);
-    return sw ? __fdividef(2.f * fmaf(-x, p, 1.5707963267948966f), vn) : __fdividef(2.f * p, rw);
+    return sw ? 2.f * fmaf(-x, p, 1.5707963267948966f) * ivn : 2.f * p * irw;
 }
 
 // q_fixed^-1 * q_ee as a rotation vector k*v (pure.py:328-344)
@@ -175,9 +187,8 @@ __device__ __forceinline__ T cp_relrot(const Con<T>& c, const T* qe, T* v) {
     T ry = ((aw * qe[2] - ax * qe[3]) + ay * qe[0]) + az * qe[1];
     T rz = ((aw * qe[3] + ax * qe[2]) - ay * qe[1]) + az * qe[0];
     if (rw < T(0)) { rw = -rw; rx = -rx; ry = -ry; rz = -rz; }
-    T vn = sqrt((rx * rx + ry * ry) + rz * rz);
     v[0] = rx; v[1] = ry; v[2] = rz;
-    return cp_rotscale<T>(vn, rw);
+    return cp_rotscale<T>((rx * rx + ry * ry) + rz * rz, rw);
 }
 
 // task error rows at a pose (pure.py:312-345): position rows, then (locked
@@ -386,6 +397,54 @@ __device__ __forceinline__ bool cp_damped_f(const float (*J)[CP_N], const float*
     return ok;
 }
 
+// FP32 damped step for the plane + orientation task (m = 4) by 2x2 block
+// elimination instead of the Cholesky chain: A = J J^T + lam^2 I =
+// [[P, Q], [Q^T, S]] with 2x2 blocks; P^-1 and the Schur complement
+// S' = S - Q^T P^-1 Q are inverted in closed form, so the solve needs two
+// dependent reciprocals instead of four dependent rsqrt pivots.  A is SPD iff
+// P and S' are, which is exactly when the Cholesky of pure.py:437-480 succeeds;
+// otherwise (or NaN) the step is zero (pure.py:529-531).
+__device__ __forceinline__ bool cp_damped_f4(const float (*J)[CP_N], const float* e, float lam, float* step) {
+    float a[4][4];
+#pragma unroll
+    for (int i = 0; i < 4; i++)
+#pragma unroll
+        for (int j = 0; j <= i; j++) {
+            float acc = 0.f;
+#pragma unroll
+            for (int k = 0; k < CP_N; k++) acc = fmaf(J[i][k], J[j][k], acc);
+            a[i][j] = a[j][i] = acc;
+        }
+    const float l2 = lam * lam;
+    a[0][0] += l2; a[1][1] += l2; a[2][2] += l2; a[3][3] += l2;
+    // P^-1
+    const float dp = fmaf(a[0][0], a[1][1], -a[0][1] * a[0][1]);
+    const float idp = __fdividef(1.f, dp);
+    const float p00 = a[1][1] * idp, p01 = -a[0][1] * idp, p11 = a[0][0] * idp;
+    // X = P^-1 Q  (Q = a[0..1][2..3])
+    const float x00 = fmaf(p00, a[0][2], p01 * a[1][2]), x01 = fmaf(p00, a[0][3], p01 * a[1][3]);
+    const float x10 = fmaf(p01, a[0][2], p11 * a[1][2]), x11 = fmaf(p01, a[0][3], p11 * a[1][3]);
+    // S' = S - Q^T X
+    const float s00 = a[2][2] - fmaf(a[0][2], x00, a[1][2] * x10);
+    const float s01 = a[2][3] - fmaf(a[0][2], x01, a[1][2] * x11);
+    const float s11 = a[3][3] - fmaf(a[0][3], x01, a[1][3] * x11);
+    const float ds = fmaf(s00, s11, -s01 * s01);
+    const float ids = __fdividef(1.f, ds);
+    // w = P^-1 e1; r = e2 - Q^T w; y2 = S'^-1 r; y1 = w - X y2
+    const float w0 = fmaf(p00, e[0], p01 * e[1]), w1 = fmaf(p01, e[0], p11 * e[1]);
+    const float r0 = e[2] - fmaf(a[0][2], w0, a[1][2] * w1);
+    const float r1 = e[3] - fmaf(a[0][3], w0, a[1][3] * w1);
+    const float y2 = fmaf(s11, r0, -s01 * r1) * ids, y3 = fmaf(s00, r1, -s01 * r0) * ids;
+    const float y0 = w0 - fmaf(x00, y2, x01 * y3), y1 = w1 - fmaf(x10, y2, x11 * y3);
+    const bool ok = a[0][0] > 0.f && dp > 0.f && s00 > 0.f && ds > 0.f;
+#pragma unroll
+    for (int k = 0; k < CP_N; k++) {
+        const float g = fmaf(J[0][k], y0, fmaf(J[1][k], y1, fmaf(J[2][k], y2, J[3][k] * y3)));
+        step[k] = ok ? g : 0.f;
+    }
+    return ok;
+}
+
 // The FP32 constraint of the module's current call lives in constant memory
 // (written by the runtime before each launch that projects), so the hot loops
 // address it as constant-bank operands instead of through a pointer.
@@ -417,7 +476,11 @@ __device__ __forceinline__ bool cp_stage1(const ProjArgs& pa, const float* xt,
     float en2 = 0.f;
 #pragma unroll
     for (int i = 0; i < CP_M; i++) en2 = fmaf(e[i], e[i], en2);
+#if CP_M == 4
+    cp_damped_f4(J, e, pa.lam, g);         // singular -> zero step (pure.py:529-531)
+#else
     cp_damped_f<CP_M>(J, e, pa.lam, g);   // singular -> zero step (pure.py:529-531)
+#endif
     float d[CP_N], s2 = 0.f;
 #pragma unroll
     for (int k = 0; k < CP_N; k++) { d[k] = xt[k] - xp[k]; s2 = fmaf(d[k], d[k], s2); }
@@ -446,10 +509,14 @@ __device__ __noinline__ float cp_err_norm(const float* q) {
 // seg rows [0, W) live in shared memory; lane t owns row t.
 // trace (optional, parity only): after every iteration the buffer is copied
 // to trace[it-1] and the prefix to trace_prog[it-1].
+// stop_flag (planner): the query's stop word, polled once per iteration with
+// the load's latency hidden behind stage 1; when it is set the projection is
+// abandoned (returns false with *iters_out = -1) so a team that lost the race
+// leaves within one iteration instead of finishing its projection.
 __device__ __noinline__ bool cp_project(const Team tm, float (*seg)[CP_NP], int W,
                            const ProjArgs pa, int* iters_out, int* prog_out,
                            float* trace = nullptr, int* trace_prog = nullptr,
-                           unsigned long long* n_stage1 = nullptr) {
+                           unsigned long long* n_stage1 = nullptr, const int* stop_flag = nullptr) {
     unsigned s1 = 0;
     const int t = (int)tm.lane;
     const bool row = t < W;
@@ -521,8 +588,11 @@ __device__ __noinline__ bool cp_project(const Team tm, float (*seg)[CP_NP], int 
         float xc[CP_N];
 #pragma unroll
         for (int k = 0; k < CP_N; k++) xc[k] = row ? seg[t][k] : 0.f;
+        bool aborted = false;
         for (int it = 1; it <= pa.max_iters; it++) {
             const bool act = row && t > prog;
+            int sf = 0;
+            if (stop_flag && t == 0) sf = *(const volatile int*)stop_flag;   // consumed after stage 1
             float xn[CP_N], xp[CP_N];
 #pragma unroll
             for (int k = 0; k < CP_N; k++) xp[k] = __shfl_up_sync(tm.mask, xc[k], 1, CP_G);
@@ -540,8 +610,13 @@ __device__ __noinline__ bool cp_project(const Team tm, float (*seg)[CP_NP], int 
                 }
                 if (!tm.any(!cheap)) { valid = act; full_step = false; }
             }
-            if (full_step && act) valid = cp_stage1(pa, xc, xp, tau_sm, xn);
-            if (full_step && act) s1++;   // per lane; summed over the team at the end
+            if (full_step) {
+                // every lane evaluates (branch-free stage 1, no divergent
+                // region); frozen / idle lanes discard the result
+                const bool v = cp_stage1(pa, xc, xp, tau_sm, xn);
+                valid = act && v;
+                if (act) s1++;   // per lane; summed over the team at the end
+            }
             unsigned vm = tm.ballot(act && valid) & full;
             int np = prog;
             if (pa.mode == 1) {   // literal-gap: largest valid index (pure.py:560-563)
@@ -566,6 +641,10 @@ __device__ __noinline__ bool cp_project(const Team tm, float (*seg)[CP_NP], int 
                 prog = np;
                 break;
             }
+            if (stop_flag && tm.bcast(sf, 0)) {   // the query is over: abandon
+                aborted = true;
+                break;
+            }
             if (row && t > np) {
 #pragma unroll
                 for (int k = 0; k < CP_N; k++) xc[k] = xn[k];
@@ -585,6 +664,12 @@ __device__ __noinline__ bool cp_project(const Team tm, float (*seg)[CP_NP], int 
             for (int k = 0; k < CP_N; k++) seg[t][k] = xc[k];
         }
         tm.sync();
+        if (aborted) {
+            *iters_out = -1;
+            *prog_out = prog;
+            if (n_stage1) *n_stage1 += __reduce_add_sync(tm.mask, s1);
+            return false;
+        }
     }
     if (ok) {
         // clamp to limits; if anything moved, re-check both tolerances
@@ -1110,10 +1195,11 @@ __device__ __forceinline__ bool cp_check_motion(const Team& tm, TeamWS& ws, cons
 
 // derive_edge (planner.py:223-245): the motion a->b re-derivable from its endpoints
 __device__ __noinline__ bool cp_derive_edge(const Team& tm, TeamWS& ws, const PlanArgs& A, const SceneSm& sc,
-                               const float* a, const float* b, Stats& st) {
+                               const float* a, const float* b, Stats& st, const int* stop = nullptr) {
     cp_interp(tm, ws.seg, A.W, a, b);
     int it, pr;
-    bool okp = cp_project(tm, ws.seg, A.W, A.pa, &it, &pr, nullptr, nullptr, &st.v[ST_STAGE1]);
+    bool okp = cp_project(tm, ws.seg, A.W, A.pa, &it, &pr, nullptr, nullptr, &st.v[ST_STAGE1], stop);
+    if (it < 0) return false;   // abandoned: the query is over
     st.v[ST_PROJITER] += it;
     if (!okp) {
         st.v[ST_PFAIL]++;
@@ -1166,13 +1252,14 @@ __device__ __noinline__ int cp_connect(const Team& tm, TeamWS& ws, const PlanArg
         cp_steer(tm, ws.qc, ws.qt, A.step, ws.qs);
         cp_interp(tm, ws.seg, A.W, ws.qc, ws.qs);
         int it, pr;
-        bool okp = cp_project(tm, ws.seg, A.W, A.pa, &it, &pr, nullptr, nullptr, &st.v[ST_STAGE1]);
+        bool okp = cp_project(tm, ws.seg, A.W, A.pa, &it, &pr, nullptr, nullptr, &st.v[ST_STAGE1], &Q.stop);
+        if (it < 0) return -1;   // abandoned: the query is over
         st.v[ST_PROJITER] += it;
         if (!okp) { st.v[ST_PFAIL]++; return -1; }
         cp_copy(tm, ws.qe, ws.seg[A.W - 1]);
         if (cp_vec_equal(tm, ws.qe, ws.qs)) {
             if (!cp_check_motion(tm, ws, A, sc, st)) return -1;
-        } else if (!cp_derive_edge(tm, ws, A, sc, ws.qc, ws.qe, st)) {
+        } else if (!cp_derive_edge(tm, ws, A, sc, ws.qc, ws.qe, st, &Q.stop)) {
             return -1;
         }
         float nd = cp_vec_dist(tm, ws.qe, ws.qt);
@@ -1203,7 +1290,8 @@ __device__ __noinline__ int cp_extend_once(const Team& tm, TeamWS& ws, const Pla
     if (cp_vec_equal(tm, ws.qs, ws.qn)) return -1;
     cp_interp(tm, ws.seg, W, ws.qn, ws.qs);
     int pit, ppr;
-    bool okp = cp_project(tm, ws.seg, W, A.pa, &pit, &ppr, nullptr, nullptr, &st.v[ST_STAGE1]);
+    bool okp = cp_project(tm, ws.seg, W, A.pa, &pit, &ppr, nullptr, nullptr, &st.v[ST_STAGE1], &Q.stop);
+    if (pit < 0) return -1;   // abandoned: the query is over
     st.v[ST_PROJITER] += pit;
     if (!okp) { st.v[ST_PFAIL]++; return -2; }
     cp_copy(tm, ws.qe, ws.seg[W - 1]);
@@ -1212,7 +1300,7 @@ __device__ __noinline__ int cp_extend_once(const Team& tm, TeamWS& ws, const Pla
         if (!cp_check_motion(tm, ws, A, sc, st)) return -3;
     } else {
         const unsigned long long pf0 = st.v[ST_PFAIL];
-        if (!cp_derive_edge(tm, ws, A, sc, ws.qn, ws.qe, st)) return st.v[ST_PFAIL] != pf0 ? -2 : -3;
+        if (!cp_derive_edge(tm, ws, A, sc, ws.qn, ws.qe, st, &Q.stop)) return st.v[ST_PFAIL] != pf0 ? -2 : -3;
     }
     const int node = cp_append(tm, A, Q, qi, a, ws.qe, inear);
     return node < 0 ? -4 : node;
@@ -1257,7 +1345,7 @@ __device__ void cp_plan_query(const Team& tm, TeamWS& ws, const PlanArgs& A, con
         if (!ok) {
             cp_copy(tm, ws.qr, js);   // derive_edge overwrites seg / qs only
             cp_copy(tm, ws.qn, jg);
-            ok = cp_derive_edge(tm, ws, A, sc, ws.qr, ws.qn, st);
+            ok = cp_derive_edge(tm, ws, A, sc, ws.qr, ws.qn, st, &Q.stop);
         }
         if (ok) {
             if (tm.lane == 0 && atomicCAS(&Q.solved, 0, 1) == 0) {
