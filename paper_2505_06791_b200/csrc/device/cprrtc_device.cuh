@@ -191,6 +191,56 @@ __device__ __forceinline__ T cp_relrot(const Con<T>& c, const T* qe, T* v) {
     return cp_rotscale<T>((rx * rx + ry * ry) + rz * rz, rw);
 }
 
+// Rotation vector of q_fixed^-1 q_ee straight from the EE rotation matrix
+// (pure.py:328-344 goes through the quaternion).  Generic / FP64: the
+// reference's quaternion route.  FP32 planner: the matrix logarithm of
+// M = R_fixed^T R_ee -- cos(theta) = (tr M - 1)/2, sin(theta) axis = vee(M - M^T)/2,
+// theta = atan2(sin, cos) with the polynomial atan -- which is the same
+// rotation vector without the quaternion's branches and square roots; near
+// theta = pi (cos < -0.7) the skew part is ill-conditioned and the quaternion
+// route is taken instead.
+template <class T>
+__device__ __forceinline__ void cp_orient_rotvec(const Con<T>& c, const T* Ree, T* rv) {
+    T qe[4], v[3];
+    cp_quat<T>(Ree, qe);
+    const T k = cp_relrot(c, qe, v);
+    rv[0] = k * v[0]; rv[1] = k * v[1]; rv[2] = k * v[2];
+}
+template <>
+__device__ __forceinline__ void cp_orient_rotvec<float>(const Con<float>& c, const float* R, float* rv) {
+    const float* f = c.rft;   // R_fixed^T, row-major
+    auto m = [&](int i, int j) { return fmaf(f[3 * i], R[j], fmaf(f[3 * i + 1], R[3 + j], f[3 * i + 2] * R[6 + j])); };
+    const float tr = (m(0, 0) + m(1, 1)) + m(2, 2);
+    const float vx = 0.5f * (m(2, 1) - m(1, 2)), vy = 0.5f * (m(0, 2) - m(2, 0)), vz = 0.5f * (m(1, 0) - m(0, 1));
+    const float cth = 0.5f * (tr - 1.f);
+    if (cth > -0.7f) {
+        const float s2 = fmaf(vx, vx, fmaf(vy, vy, vz * vz));
+        const float ivn = rsqrtf(s2), ic = __fdividef(1.f, cth);
+        const float vn = s2 * ivn;
+        const bool sw = vn > cth;
+        const float x = sw ? cth * ivn : vn * ic;
+        const float u = x * x;
+        float p = 0.0028531861025840044f;
+        p = fmaf(p, u, -0.016082055866718292f);
+        p = fmaf(p, u, 0.042713798582553864f);
+        p = fmaf(p, u, -0.07506226748228073f);
+        p = fmaf(p, u, 0.1064186692237854f);
+        p = fmaf(p, u, -0.14203891158103943f);
+        p = fmaf(p, u, 0.19992651045322418f);
+        p = fmaf(p, u, -0.33333075046539307f);
+        p = fmaf(p, u, 1.0f);
+        // theta / sin(theta); -> 1 as theta -> 0
+        float sc = sw ? fmaf(-x, p, 1.5707963267948966f) * ivn : p * ic;
+        sc = s2 >= 1e-24f ? sc : 1.f;
+        rv[0] = sc * vx; rv[1] = sc * vy; rv[2] = sc * vz;
+    } else {
+        float qe[4], v[3];
+        cp_quat<float>(R, qe);
+        const float k = cp_relrot(c, qe, v);
+        rv[0] = k * v[0]; rv[1] = k * v[1]; rv[2] = k * v[2];
+    }
+}
+
 // task error rows at a pose (pure.py:312-345): position rows, then (locked
 // orientation) the weighted rotation vector k*v of q_fixed^-1 q_ee
 template <class T>
@@ -258,20 +308,18 @@ __device__ __forceinline__ void cp_err_jac(const Con<T>& c, const T* q, T* e, T 
     T R[CP_N * 9], P[CP_N * 3], AX[CP_N * 3], OR[CP_N * 3], SPH[(CP_S > 0 ? CP_S : 1) * 3];
     cp_fk<T>(q, R, P, AX, OR, SPH);
     const T* pe = P + 3 * CP_EE;
-    T qe[4];
-    cp_quat<T>(R + 9 * CP_EE, qe);
 #if CP_ORIENT
-    T v[3], A[9], Mo[9];
-    T k = cp_relrot(c, qe, v);    // once: shared by the error rows and the Jacobian
-    cp_task_err_kv<T>(c, pe, k, v, e);
-    cp_so3_rate<T>(k * v[0], k * v[1], k * v[2], A);
+    T rv[3], A[9], Mo[9];
+    cp_orient_rotvec<T>(c, R + 9 * CP_EE, rv);   // once: shared by the error rows and the Jacobian
+    cp_task_err_kv<T>(c, pe, T(1), rv, e);
+    cp_so3_rate<T>(rv[0], rv[1], rv[2], A);
 #pragma unroll
     for (int i = 0; i < 3; i++)
 #pragma unroll
         for (int j = 0; j < 3; j++)
             Mo[3 * i + j] = c.weight * ((A[3 * i] * c.rft[j] + A[3 * i + 1] * c.rft[3 + j]) + A[3 * i + 2] * c.rft[6 + j]);
 #else
-    cp_task_err<T>(c, pe, qe, e);
+    cp_task_err_kv<T>(c, pe, T(0), pe, e);
 #endif
 #pragma unroll
     for (int j = 0; j < CP_N; j++) {
@@ -494,9 +542,11 @@ __device__ __forceinline__ bool cp_stage1(const ProjArgs& pa, const float* xt,
 __device__ __noinline__ float cp_err_norm(const float* q) {
     float R[CP_N * 9], P[CP_N * 3], AX[CP_N * 3], OR[CP_N * 3], SPH[(CP_S > 0 ? CP_S : 1) * 3];
     cp_fk<float>(q, R, P, AX, OR, SPH);
-    float qe[4], e[CP_M];
-    cp_quat<float>(R + 9 * CP_EE, qe);
-    cp_task_err<float>(cp_conf, P + 3 * CP_EE, qe, e);
+    float rv[3] = {0.f, 0.f, 0.f}, e[CP_M];
+#if CP_ORIENT
+    cp_orient_rotvec<float>(cp_conf, R + 9 * CP_EE, rv);
+#endif
+    cp_task_err_kv<float>(cp_conf, P + 3 * CP_EE, 1.f, rv, e);
     float s = 0.f;
 #pragma unroll
     for (int i = 0; i < CP_M; i++) s += e[i] * e[i];
@@ -1183,10 +1233,15 @@ __device__ __forceinline__ bool cp_should_stop(const Team& tm, QueryState& Q, co
 // validate with stats accumulation; waypoint 0 (an existing tree node) skipped
 __device__ __forceinline__ bool cp_check_motion(const Team& tm, TeamWS& ws, const PlanArgs& A,
                                                 const SceneSm& sc, Stats& st) {
-    ValOut v = sc.cull ? cp_validate_cull(tm, ws.seg, A.W, 1, A.flag_on, A.margin, sc)
-                       : cp_validate(tm, ws.seg, A.W, 1, A.flag_on, A.margin, sc);
+    // every waypoint, row 0 included: the reference validates the whole
+    // derived motion (planner.py:232-236), and a tree node (the endpoint of an
+    // earlier P1 projection) is itself never validated -- only its derived
+    // edge, whose last row the re-projection may have moved.  Lane 0 is idle
+    // during CC otherwise, so the extra row costs no latency.
+    ValOut v = sc.cull ? cp_validate_cull(tm, ws.seg, A.W, 0, A.flag_on, A.margin, sc)
+                       : cp_validate(tm, ws.seg, A.W, 0, A.flag_on, A.margin, sc);
     st.v[ST_CCPERF] += v.performed;     // reference (lockstep) semantics, pure.py:664-698
-    st.v[ST_CCPOSS] += (u64)((i64)CP_S * (sc.nb + sc.ne) + CP_P) * (A.W - 1);
+    st.v[ST_CCPOSS] += (u64)((i64)CP_S * (sc.nb + sc.ne) + CP_P) * A.W;
     st.v[ST_GPUCHK] += v.gpu_checks;
     st.v[ST_FKCC] += v.fk_evals;
     if (!v.valid) st.v[ST_CREJ]++;

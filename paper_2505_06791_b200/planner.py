@@ -19,8 +19,8 @@ Differences from the reference, all deliberate:
   clock).  ``attempts`` is accepted; the device already evaluates hundreds of
   samples at once.
 * ``stats.iterations`` counts samples drawn; ``cc_possible`` is the
-  reference's count over the checked waypoints (row 0 of a motion is an
-  existing tree node and is not re-checked).  ``cc_performed`` follows the
+  reference's count (every waypoint of every checked motion, row 0
+  included, like validate_motion).  ``cc_performed`` follows the
   reference's lockstep accounting with ``DeviceOptions(cc_broadphase=0)``;
   with the clustered broad phase (the default whenever the scene has
   obstacles) it counts the sphere-primitive checks actually evaluated.

@@ -148,3 +148,33 @@ def test_plan_race_first_solution_flag(oracle):
         assert all(r.status in ("Solved", "Stopped") for r in per), [r.status for r in per]
         assert best.stats.device_ms == min(r.stats.device_ms for r in per if r.solved)
         _check_path(oracle, prob, best)
+
+
+def test_every_dense_waypoint_collision_free_many_seeds(oracle):
+    """Regression (r1): tree nodes are endpoints of P1 projections and are
+    never validated themselves -- only their derived edges -- so the planner
+    must check row 0 of every motion like validate_motion does.  A sweep of
+    the window problem used to produce a colliding node in ~2 % of plans."""
+    from paper_2505_06791_b200.planner import (DeviceOptions, PlanParams, PlanProblem, _SRC, _bind, _derive,
+                                               _params_struct, plan)
+    p = next(x for x in fx.plans() if x["id"] == "window_line")
+    m, sc = fx.robot(p["robot"]), fx.scene(p["scene"])
+    sp = fx.spec(p["spec"])
+    kw = dict(p["params"])
+    kw["max_iterations"] = max(kw.get("max_iterations", 1000), 2000)
+    solved = 0
+    for trial in range(150):
+        kw["seed_offset"] = trial * 10_000
+        prob = PlanProblem(m, sc, sp, np.array(p["start"]), np.array(p["goal"]), PlanParams(**kw))
+        res = plan(prob)
+        if not res.solved:
+            continue
+        solved += 1
+        ctx = _bind(prob, DeviceOptions())
+        src = np.array([_SRC.index(s) for s in res.edge_sources], np.int32)
+        dense, ok = _derive(ctx, _params_struct(prob.params, DeviceOptions()), np.stack(res.path), src)
+        assert ok.all()
+        for e in range(dense.shape[0]):   # every row of every edge, the nodes included
+            v, *_ = oracle.validate_waypoints(dense[e], m.packed, sc.packed(), False)
+            assert v, (trial, e)
+    assert solved > 100

@@ -37,6 +37,24 @@ extern "C" __global__ void part_bench(int iters, int part, long long* cyc, float
             cp_fk<float>(q, R, P, AX, OR, SPH);
             const float d = 1e-6f * (P[3 * CP_EE] + R[9 * CP_EE]);
             for (int k = 0; k < CP_N; k++) q[k] += d;
+        } else if (part >= 3) {   // FK + quaternion (3), + rotation vector (4), + SO(3) rate (5)
+            float R[CP_N * 9], P[CP_N * 3], AX[CP_N * 3], OR[CP_N * 3], SPH[(CP_S > 0 ? CP_S : 1) * 3];
+            cp_fk<float>(q, R, P, AX, OR, SPH);
+            float qe[4];
+            cp_quat<float>(R + 9 * CP_EE, qe);
+            float d = qe[0] + qe[1];
+            if (part >= 4) {
+                float v[3];
+                const float k = cp_relrot(cp_conf, qe, v);
+                d = k * v[0];
+                if (part >= 5) {
+                    float A9[9];
+                    cp_so3_rate<float>(k * v[0], k * v[1], k * v[2], A9);
+                    d = A9[0] + A9[4] + A9[8];
+                }
+            }
+            d *= 1e-6f;
+            for (int k = 0; k < CP_N; k++) q[k] += d;
         } else if (part == 1) {   // FK + quaternion + task error + Jacobian
             float e[CP_M], J[CP_M][CP_N];
             cp_err_jac<float>(cp_conf, q, e, J);
@@ -105,11 +123,12 @@ int main() {
     stage1_bench<<<1, 16>>>(it, cyc, out);
     cudaMemcpy(&h, cyc, 8, cudaMemcpyDeviceToHost);
     printf("stage1: %.0f cycles per evaluation (1 warp, 16 lanes)\n", (double)h / it);
-    for (int part = 0; part < 3; part++) {
+    for (int part = 0; part < 6; part++) {
         part_bench<<<1, 16>>>(it, part, cyc, out);
         part_bench<<<1, 16>>>(it, part, cyc, out);
         cudaMemcpy(&h, cyc, 8, cudaMemcpyDeviceToHost);
-        printf("part %s: %.0f cycles\n", part == 0 ? "fk" : (part == 1 ? "fk+err+jac" : "damped"), (double)h / it);
+        const char* nm[6] = {"fk", "fk+err+jac", "damped", "fk+quat", "fk+quat+rotvec", "fk+quat+rotvec+so3"};
+        printf("part %s: %.0f cycles\n", nm[part], (double)h / it);
     }
     int* its; int hi;
     cudaMalloc(&its, 4);
