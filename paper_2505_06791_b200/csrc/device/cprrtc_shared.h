@@ -50,20 +50,28 @@ struct SceneSm {
 enum { ST_ITER = 0, ST_ATT, ST_ADDED, ST_PFAIL, ST_CREJ, ST_CCPERF, ST_CCPOSS, ST_GPUCHK,
        ST_STAGE1, ST_FKCC, ST_NNODES, ST_PROJITER, ST_NSTAT };
 
-// per-query planner state in HBM
-struct QueryState {
-    i64 seed_offset;
-    int count[2];          // tree node counters (atomic append)
-    int hwm[2];            // nodes used by the previous run (NaN refill)
-    int next_sample;       // Halton index counter (= reference iteration)
+// per-query planner state in HBM, one 128-byte L2 line per access pattern:
+// the flags every team polls, the counters every team hits with atomics, and
+// the stats added once per team -- so polling never queues behind atomics
+struct alignas(128) QueryState {
+    // line 0: polled flags and read-mostly state
     int solved, stop, timed_out, overflow, exhausted;
-    int meet[2];           // meet node in the start / goal tree
-    int setup_code;        // endpoint check (planner.py:416-427)
     int race_stopped;      // stopped because another racer solved the query
-    int active;            // teams inside the query (the last one out extracts)
-    int pad_;
+    int setup_code;        // endpoint check (planner.py:416-427)
+    int meet[2];           // meet node in the start / goal tree
+    int hwm[2];            // nodes used by the previous run (NaN refill)
+    int pad0_;
+    i64 seed_offset;
     u64 t0_ns, t_end_ns;
+    int pad1_[14];
+    // line 1: atomics
+    int count[2];          // tree node counters (atomic append)
+    int next_sample;       // Halton index counter (= reference iteration)
+    int active;            // teams inside the query (the last one out extracts)
+    int pad2_[28];
+    // line 2: stats (one atomicAdd per team and counter)
     u64 stats[ST_NSTAT];
+    u64 pad3_[16 - ST_NSTAT];
 };
 
 struct PlanArgs {

@@ -17,6 +17,7 @@
 
 #include <algorithm>
 #include <cmath>
+#include <cstddef>
 #include <cstdint>
 #include <cstdio>
 #include <cstdlib>
@@ -32,6 +33,9 @@
 
 #include "../../include/cprrtc.h"
 #include "device/cprrtc_shared.h"
+
+static_assert(sizeof(QueryState) == 384 && offsetof(QueryState, count) == 128 && offsetof(QueryState, stats) == 256,
+              "QueryState: polled flags, atomics and stats on separate 128-byte lines");
 
 namespace cprrtc {
 std::string codegen_robot(const cprrtc_robot& r, std::string* err);

@@ -81,6 +81,20 @@ extern "C" __global__ void part_bench(int iters, int part, long long* cyc, float
     out[threadIdx.x] = q[0];
 }
 
+// Halton sample (FP64, bit-exact with the reference) latency, lane k = joint k
+extern "C" __global__ void halton_bench(int iters, long long seed, long long* cyc, double* out) {
+    const int lane = threadIdx.x;
+    double acc = 0.0;
+    long long t0 = clock64();
+    for (int i = 0; i < iters; i++) {
+        if (lane < CP_N) acc += cp_halton((i64)(500 + i) + seed + (acc > 1e300 ? 1 : 0), lane);
+        __syncwarp();
+    }
+    long long t1 = clock64();
+    if (threadIdx.x == 0) cyc[0] = t1 - t0;
+    out[threadIdx.x] = acc;
+}
+
 // one Alg. 1 projection of a 16-waypoint segment from an on-manifold start
 // toward a point 0.5 rad away (the planner's P1), repeated
 extern "C" __global__ void proj_bench(int reps, long long* cyc, int* iters_out) {
@@ -129,6 +143,15 @@ int main() {
         cudaMemcpy(&h, cyc, 8, cudaMemcpyDeviceToHost);
         const char* nm[6] = {"fk", "fk+err+jac", "damped", "fk+quat", "fk+quat+rotvec", "fk+quat+rotvec+so3"};
         printf("part %s: %.0f cycles\n", nm[part], (double)h / it);
+    }
+    {
+        double* dout; cudaMalloc(&dout, 256);
+        for (long long seed : {0LL, 10000LL, 1000000LL}) {
+            halton_bench<<<1, 16>>>(200, seed, cyc, dout);
+            halton_bench<<<1, 16>>>(200, seed, cyc, dout);
+            cudaMemcpy(&h, cyc, 8, cudaMemcpyDeviceToHost);
+            printf("halton (seed_offset %lld): %.0f cycles per sample\n", seed, (double)h / 200);
+        }
     }
     int* its; int hi;
     cudaMalloc(&its, 4);
