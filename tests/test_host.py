@@ -104,3 +104,15 @@ def test_robot_yaml_round_trip_and_errors():
         load_robot("name: x\nlinks: 3\njoints: [{axis: [0,0,1], limits: [-1, 1]}]\n")
     with pytest.raises(ValueError):
         m.check_q(np.zeros(3))
+
+
+def test_plan_race_argument_checks():
+    """plan_race validates its racer list before touching a device."""
+    import pytest
+    from paper_2505_06791_b200.planner import PlanParams, PlanProblem, plan_race
+    m = fx.robot("planar2")
+    prob = PlanProblem(m, fx.scene("empty"), None, np.zeros(2), np.array([1.0, 0.5]), PlanParams())
+    with pytest.raises(ValueError):
+        plan_race(prob, devices=())
+    with pytest.raises(ValueError):
+        plan_race(prob, devices=tuple(range(9)))
