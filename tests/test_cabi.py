@@ -66,7 +66,7 @@ def test_device_source_is_one_translation_unit():
     from paper_2505_06791_b200 import _lib
     src = _lib.device_source(fx.robot("planar2").packed, 16, 0, 0, 0)
     for k in ("cp_plan_kernel", "cp_init_kernel", "cp_check_kernel", "cp_extract_query", "cp_dense_kernel",
-              "#define CP_G 16", "struct QueryState"):
+              "#define CP_G 16", "struct alignas(128) QueryState"):
         assert k in src
     assert "cp_validate_kernel" in src and "#if CP_PARITY" in src
 
