@@ -274,6 +274,7 @@ def run_b200(args, world, rank, local):
     if rank == 0 and not args.no_extras:
         line.update(extras(args, local, model, line))
         line["other_configs"] = other_configs(args, local)
+        line["ablation_projection"] = ablation_projection(args, local)
     if rank == 0 and world == 1 and not args.no_cpu:
         line["cpu_baseline"] = cpu_baseline(args)
     return line
@@ -398,6 +399,36 @@ def _cfg_problems(name):
                         prs["dense8_line_goal"][i], dict(width=16)))
         return "8-DoF arm8 with 36 collision spheres / 96 self pairs, table, line constraint, W=16", out
     raise KeyError(name)
+
+
+def ablation_projection(args, local):
+    """The paper's projection ablation (parallel vs the
+    sequential "naive" projector) on the headline workload: 30 feasible
+    upright pairs x 2 seeds per mode, device median time and success."""
+    import fixtures as fx
+    from paper_2505_06791_b200.planner import DeviceOptions, PlanParams, PlanProblem, plan, prepare
+    model, scene, spec, starts, goals = workload()
+    feas = np.nonzero(fx.upright_feasible())[0][:30]
+    opt = DeviceOptions(device=local)
+    out = {}
+    for mode in ("parallel", "naive", "literal-gap"):
+        times, ok, n = [], 0, 0
+        for k in feas:
+            for seed in range(2):
+                p = PlanProblem(model, scene, spec, starts[k], goals[k],
+                                PlanParams(width=16, max_iterations=10**6, time_budget_ms=2000.0,
+                                           seed_offset=int(k) * 10_000 + seed, projection_mode=mode))
+                ctx = prepare(p, opt)
+                ctx.flush_l2()
+                r = plan(p, opt)
+                n += 1
+                if r.solved:
+                    ok += 1
+                    times.append(ctx.last_timing()[0])
+        out[mode] = {"median_ms": float(np.median(times)) if times else None, "success_rate": ok / n,
+                     "queries": n}
+    out["workload"] = "configs[1] upright Panda, 30 feasible pairs x 2 seeds, W=16"
+    return out
 
 
 def other_configs(args, local):
