@@ -1157,8 +1157,25 @@ __device__ __forceinline__ double cp_radical_inverse(i64 index, int base) {
     }
     return f;
 }
+// The same operations without the per-digit FP64 division and 64-bit integer
+// division: the scale sequence is the generated table cp_hscale (the
+// reference's own values, bit for bit) and i / b is a 64-bit multiply-high by
+// cp_hmagic (exact for i < 2^32).  k = joint index (base = k-th prime).
+__device__ __forceinline__ double cp_radical_inverse_k(i64 index, int k) {
+    if (index < 0 || index >= (1ll << 32)) return cp_radical_inverse(index, cp_prime(k));
+    const u64 M = cp_hmagic[k], b = (u64)cp_prime(k);
+    const double* sc = cp_hscale[k];
+    u64 i = (u64)index;
+    double f = 0.0;
+    for (int d = 0; i > 0; d++) {
+        const u64 q = __umul64hi(i << 24, M);
+        f = __dadd_rn(f, __dmul_rn((double)(i - q * b), sc[d]));
+        i = q;
+    }
+    return f;
+}
 __device__ __forceinline__ double cp_halton(i64 index, int k) {
-    double u = cp_radical_inverse(index, cp_prime(k));
+    double u = cp_radical_inverse_k(index, k);
     return __dadd_rn(cp_lo(k), __dmul_rn(__dsub_rn(cp_hi(k), cp_lo(k)), u));
 }
 
@@ -1952,7 +1969,7 @@ extern "C" __global__ void cp_halton_kernel(int count, i64 first, i64 seed_offse
     int i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= count) return;
     for (int k = 0; k < CP_N; k++) {
-        double u = cp_radical_inverse(first + i + seed_offset, cp_prime(k));
+        double u = cp_radical_inverse_k(first + i + seed_offset, k);
         out[(size_t)i * CP_N + k] = __dadd_rn(lo[k], __dmul_rn(__dsub_rn(hi[k], lo[k]), u));
     }
 }

@@ -102,6 +102,18 @@ def test_halton_bit_exact(K):
             assert np.array_equal(got, k[f"halton_{name}_{seed}"])
 
 
+def test_halton_fast_path_matches_oracle(K, oracle):
+    """The table / multiply-high radical inverse (indices < 2^32) and the
+    generic one beyond agree bit for bit with the pinned oracle."""
+    m = fx.robot("arm8")
+    lo, hi = m.packed.lo, m.packed.hi
+    for seed in (123_456_789, 2**32 - 40, 2**32 + 7, 10**11 + 3):
+        got = K.halton_batch(m, 64, 1, seed)
+        for i in range(64):
+            want = oracle.halton(m.n, 1 + i, seed, lo, hi)
+            assert np.array_equal(got[i], want), (seed, i)
+
+
 def test_nearest(K):
     k = fx.kats()
     m = fx.robot("arm7")
