@@ -26,6 +26,7 @@
 #define CP_M ((CP_KIND == 0 ? 1 : 2) + (CP_ORIENT ? 3 : 0))
 #define CP_NP ((CP_N % 2) ? CP_N : (CP_N + 1))   // odd row pitch: no bank conflicts
 #define CP_CHUNK 8
+#define CP_VOTE 4                    // lockstep CC: early-exit vote every CP_VOTE chunks
 #define CP_BCH (2 + 2 * CP_CHUNK)   // float4s per box chunk of the clustered scene
 #define CP_SCH (2 + CP_CHUNK)       // float4s per sphere chunk
 #define CP_INTMAX 0x7fffffff
@@ -878,9 +879,13 @@ __device__ __forceinline__ void cp_env_pass(const Team& tm, const float4* sp, bo
                         break;
                     }
             }
-            if (FLAG) {
-                if (tm.any(first_r < rb1)) stop = true;
-                else if (tm.any(first_r != CP_INTMAX)) only0 = true;
+            // the flag vote every CP_VOTE chunks and at the end of the boxes:
+            // later votes only add checks past the first detection (first_r is
+            // exact regardless), and fewer votes keep the chunk loop tight
+            if (FLAG && (((p0 / CP_CHUNK) % CP_VOTE) == CP_VOTE - 1 || p0 + CP_CHUNK >= sc.nb)) {
+                const int mr = (int)__reduce_min_sync(tm.mask, (unsigned)first_r);   // one team vote
+                if (mr < rb1) stop = true;
+                else if (mr != CP_INTMAX) only0 = true;
             }
         }
 #pragma unroll 1
@@ -913,9 +918,10 @@ __device__ __forceinline__ void cp_env_pass(const Team& tm, const float4* sp, bo
                         break;
                     }
             }
-            if (FLAG) {
-                if (tm.any(first_r < rb1)) stop = true;
-                else if (tm.any(first_r != CP_INTMAX)) only0 = true;
+            if (FLAG && (((p0 / CP_CHUNK) % CP_VOTE) == CP_VOTE - 1 || p0 + CP_CHUNK >= sc.ne)) {
+                const int mr = (int)__reduce_min_sync(tm.mask, (unsigned)first_r);   // one team vote
+                if (mr < rb1) stop = true;
+                else if (mr != CP_INTMAX) only0 = true;
             }
         }
         if (only0) stop = true;   // sphere s is clean: the first sphere-(s+1) hit is the first detection
