@@ -178,3 +178,23 @@ def test_every_dense_waypoint_collision_free_many_seeds(oracle):
             v, *_ = oracle.validate_waypoints(dense[e], m.packed, sc.packed(), False)
             assert v, (trial, e)
     assert solved > 100
+
+
+def test_upright_suite_matches_reference_success(oracle):
+    """BASELINE configs[1] as a suite: the 100 upright-Panda pairs in one
+    batch.  Every pair the reference planner solves (3 seeds x 20 s,
+    tests/golden/upright_feasibility.json) is solved, and every returned path
+    is sound in FP64 (dense motions on the manifold and collision-free)."""
+    from paper_2505_06791_b200.planner import PlanParams, PlanProblem, plan_batch
+    m, sc, sp = fx.robot("arm7"), fx.scene("table"), fx.spec("upright")
+    prs = fx.pairs()
+    feas = fx.upright_feasible()
+    probs = [PlanProblem(m, sc, sp, prs["upright_start"][k], prs["upright_goal"][k],
+                         PlanParams(width=16, max_iterations=10**7, time_budget_ms=3000.0,
+                                    seed_offset=int(k) * 10_000))
+             for k in range(len(feas))]
+    res = plan_batch(probs)
+    solved = np.array([r.solved for r in res])
+    assert solved[feas].all(), np.nonzero(feas & ~solved)[0]
+    for k in np.nonzero(solved)[0][::4]:
+        _check_path(oracle, probs[k], res[k])
