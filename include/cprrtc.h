@@ -216,7 +216,15 @@ CPRRTC_API int cprrtc_halton(void *ctx, int count, int64_t first_index, int64_t 
 CPRRTC_API int cprrtc_plan(void *ctx, const cprrtc_params *params, int B, const double *starts,
                 const double *goals, const int64_t *seeds, cprrtc_result *results,
                 double *paths, int32_t *sources);
-/* One query raced on n_ctx contexts (typically one per GPU; at most
+/* cprrtc_plan's batch sharded over n_ctx contexts (typically one per GPU):
+ * context k plans the contiguous slice [k*B/n_ctx, (k+1)*B/n_ctx); every shard
+ * is launched before any is awaited, and the results land in the caller's
+ * arrays exactly as cprrtc_plan would lay them out.  Independent queries, no
+ * collective (BASELINE configs[4]). */
+CPRRTC_API int cprrtc_plan_multi(void *const *ctxs, int n_ctx, const cprrtc_params *params, int B,
+                                 const double *starts, const double *goals, const int64_t *seeds,
+                                 cprrtc_result *results, double *paths, int32_t *sources);
+/* One query raced on n_ctx contexts/* One query raced on n_ctx contexts (typically one per GPU; at most
  * CPRRTC_MAX_RACE): each grows its own tree pair from seeds[k] (distinct
  * Halton offsets) with the planner of cprrtc_plan; the first racer to solve
  * stores a first-solution flag into every racer's flag word (peer stores over

@@ -1433,6 +1433,44 @@ int cprrtc_plan(void* p, const cprrtc_params* prm, int B, const double* starts, 
     return plan_collect(c, B, results, paths, sources);
 }
 
+int cprrtc_plan_multi(void* const* ctxs, int n_ctx, const cprrtc_params* prm, int B, const double* starts,
+                      const double* goals, const int64_t* seeds, cprrtc_result* results, double* paths,
+                      int32_t* sources) {
+    if (!ctxs || n_ctx < 1 || !prm || B < 1 || !starts || !goals || !results)
+        return fail(CPRRTC_EARG, "bad argument");
+    if (int rc = check_params(prm)) return rc;
+    std::vector<Ctx*> cs(n_ctx);
+    for (int k = 0; k < n_ctx; k++) {
+        cs[k] = C(ctxs[k]);
+        if (!cs[k]) return fail(CPRRTC_EARG, "NULL context");
+        for (int j = 0; j < k; j++)
+            if (cs[j] == cs[k]) return fail(CPRRTC_EARG, "a context can appear only once");
+        if (cs[k]->n != cs[0]->n) return fail(CPRRTC_EARG, "contexts must share the robot");
+    }
+    const int n = cs[0]->n;
+    const int pc = prm->path_capacity > 0 ? prm->path_capacity : 1024;
+    // contiguous shards, launched on every device before any is awaited
+    std::vector<int> lo(n_ctx + 1);
+    for (int k = 0; k <= n_ctx; k++) lo[k] = (int)((long long)B * k / n_ctx);
+    int rc = 0;
+    int launched = 0;
+    for (int k = 0; k < n_ctx && !rc; k++) {
+        const int b = lo[k + 1] - lo[k];
+        if (b == 0) continue;
+        rc = plan_launch(cs[k], prm, b, starts + (size_t)lo[k] * n, goals + (size_t)lo[k] * n,
+                         seeds ? seeds + lo[k] : nullptr, nullptr);
+        launched = k + 1;
+    }
+    for (int k = 0; k < launched; k++) {   // always drain what was launched
+        const int b = lo[k + 1] - lo[k];
+        if (b == 0) continue;
+        int rk = plan_collect(cs[k], b, results + lo[k], paths ? paths + (size_t)lo[k] * pc * n : nullptr,
+                              sources ? sources + (size_t)lo[k] * pc : nullptr);
+        if (!rc) rc = rk;
+    }
+    return rc;
+}
+
 int cprrtc_plan_race(void* const* ctxs, int n_ctx, const cprrtc_params* prm, const double* start,
                      const double* goal, const int64_t* seeds, cprrtc_result* results, double* paths,
                      int32_t* sources, int32_t* winner) {

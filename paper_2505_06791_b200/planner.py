@@ -308,13 +308,18 @@ def prepare(problem: PlanProblem, options: DeviceOptions = DeviceOptions()):
     return ctx
 
 
-def plan_batch(problems, options: DeviceOptions = DeviceOptions(), return_dense: bool = False):
+def plan_batch(problems, options: DeviceOptions = DeviceOptions(), return_dense: bool = False,
+               devices=None):
     """Plan many independent queries in one persistent launch.
 
     All problems must share model, scene, spec and params (apart from
     start, goal and params.seed_offset).  Returns a list of PlanResult; a bad
     start/goal raises PlanSetupError for that problem only if it is the sole
     problem, else the result carries status 'Error:PlanSetupError'.
+    ``devices`` (e.g. ``range(8)``) shards the batch into contiguous slices,
+    one persistent launch per device, all launched before any is awaited
+    (cprrtc_plan_multi; no collective).  A device may repeat (independent
+    contexts on one GPU).
     """
     problems = list(problems)
     if not problems:
@@ -338,13 +343,32 @@ def plan_batch(problems, options: DeviceOptions = DeviceOptions(), return_dense:
     res = (_lib.Result * B)()
     pc = int(prm.path_capacity)
     paths, srcs = _out_buffers(B, pc, n)
-    with ctx.lock:
-        ctx.prepare(p0.params.width)
+    devs = tuple(int(d) for d in devices) if devices is not None else ()
+    if len(devs) > 1:
+        seen: dict = {}
+        ctxs = []
+        for d in devs:
+            slot = seen.get(d, 0)
+            seen[d] = slot + 1
+            c = kernels.context(p0.model, d, slot)
+            c.set_scene(p0.scene.packed())
+            c.set_spec(None if p0.spec is None else p0.spec.packed)
+            c.prepare(p0.params.width)
+            ctxs.append(c)
+        handles = (C.c_void_p * len(ctxs))(*[c.h.value for c in ctxs])
         t0 = time.perf_counter()
-        _lib.check(ctx.L.cprrtc_plan(ctx.h, C.byref(prm), B, _lib.ptr(starts), _lib.ptr(goals),
-                                     _lib.ptr(seeds, _lib._lp), res, _lib.ptr(paths),
-                                     _lib.ptr(srcs, _lib._ip)), "plan")
+        _lib.check(ctx.L.cprrtc_plan_multi(handles, len(ctxs), C.byref(prm), B, _lib.ptr(starts),
+                                           _lib.ptr(goals), _lib.ptr(seeds, _lib._lp), res, _lib.ptr(paths),
+                                           _lib.ptr(srcs, _lib._ip)), "plan_multi")
         wall = (time.perf_counter() - t0) * 1e3
+    else:
+        with ctx.lock:
+            ctx.prepare(p0.params.width)
+            t0 = time.perf_counter()
+            _lib.check(ctx.L.cprrtc_plan(ctx.h, C.byref(prm), B, _lib.ptr(starts), _lib.ptr(goals),
+                                         _lib.ptr(seeds, _lib._lp), res, _lib.ptr(paths),
+                                         _lib.ptr(srcs, _lib._ip)), "plan")
+            wall = (time.perf_counter() - t0) * 1e3
     out = _results_bulk(res, problems, paths, srcs, wall, pc)
     if return_dense:
         for i, r in enumerate(out):

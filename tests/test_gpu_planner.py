@@ -96,6 +96,24 @@ def test_plan_batch(oracle):
             _check_path(oracle, prob, r)
 
 
+def test_plan_batch_sharded_over_contexts(oracle):
+    """plan_batch(devices=...) -> cprrtc_plan_multi: contiguous shards, one
+    persistent launch per context (here three contexts of one GPU), results
+    in input order and sound."""
+    from paper_2505_06791_b200.planner import PlanParams, PlanProblem, plan_batch
+    m, sc, sp = fx.robot("arm7"), fx.scene("table"), fx.spec("table_plane")
+    prs = fx.pairs()
+    probs = [PlanProblem(m, sc, sp, prs["table_plane_start"][i], prs["table_plane_goal"][i],
+                         PlanParams(width=16, max_iterations=2000, seed_offset=i * 10_000))
+             for i in range(50)]
+    res = plan_batch(probs, devices=(0, 0, 0))
+    assert len(res) == 50 and sum(r.solved for r in res) >= 48
+    for prob, r in list(zip(probs, res))[::7]:
+        if r.solved:
+            assert np.array_equal(r.path[0], prob.start) and np.array_equal(r.path[-1], prob.goal)
+            _check_path(oracle, prob, r)
+
+
 def test_setup_errors():
     from paper_2505_06791_b200.errors import PlanSetupError
     from paper_2505_06791_b200.planner import PlanParams, PlanProblem, plan
