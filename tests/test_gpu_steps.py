@@ -153,3 +153,78 @@ def test_trial_records_round_trip(tmp_path):
     assert [r.row() for r in back] == [r.row() for r in recs]
     summ = summarize(recs)
     assert all(v["success_rate"] == 1.0 for v in summ.values())
+
+
+def _ref_project(oracle, m, sp, seg):
+    """projection.py parallel_project + _finish (clip to limits, FP64 recheck)."""
+    gaps = np.linalg.norm(np.diff(seg, axis=0), axis=1)
+    tau_sm = max(1.5 * float(gaps.max()), 1e-6) if len(gaps) else 1e-6
+    ok, xi, it, prog, _ = oracle.project_segment(seg, m.packed, sp.packed, sp.tau_task, tau_sm,
+                                                 0.1, 1e-3, 128, 0)
+    if not ok:
+        return None
+    lo, hi = m.packed.lo, m.packed.hi
+    xc = np.clip(xi, lo, hi)
+    if not np.array_equal(xc, xi):
+        for t, q in enumerate(xc):
+            e = oracle.task_error_at(sp.packed, oracle.ee_pose(m.packed, q))
+            if not np.linalg.norm(e) < sp.tau_task:
+                return None
+            if t and not np.linalg.norm(q - xc[t - 1]) < tau_sm:
+                return None
+    return xc
+
+
+def _ref_extend(oracle, m, sc, sp, q_near, q_rand, W=16, step=0.5):
+    """maniplan planner.py:265-306 (_attempt_extend) composed from the pinned
+    oracle's primitives, FP64: returns (reason or None, q_end)."""
+    from paper_2505_06791_b200.planner import steer
+    q_steer = steer(q_near, q_rand, step)
+    if np.array_equal(q_steer, q_near):
+        return "degenerate", None
+    interp = lambda a, b: np.array([a + (k / (W - 1)) * (b - a) for k in range(W)])  # noqa: E731
+    seg = interp(q_near, q_steer)
+    seg[0], seg[-1] = q_near, q_steer
+    xi = _ref_project(oracle, m, sp, seg)
+    if xi is None:
+        return "projection", None
+    q_end = xi[-1].copy()
+    if not np.array_equal(q_end, q_steer):
+        seg2 = interp(q_near, q_end)
+        seg2[0], seg2[-1] = q_near, q_end
+        xi = _ref_project(oracle, m, sp, seg2)
+        if xi is None:
+            return "projection", q_end
+    ok, *_ = oracle.validate_waypoints(xi, m.packed, sc.packed(), True)
+    return (None if ok else "collision"), q_end
+
+
+@pytest.mark.parametrize("spec_name,scene_name", [("table_plane", "table"), ("upright", "table"),
+                                                  ("plane55", "shelf"), ("plane55", "shelf_x11")])
+def test_extend_outcomes_match_reference(oracle, spec_name, scene_name):
+    """The device extend (one team, FP32) against the reference's
+    _attempt_extend recomposed from the FP64 oracle, from an on-manifold node
+    toward Halton samples: the same outcome for the large majority, and the
+    same new node within FP32 / projection-iteration tolerance."""
+    from paper_2505_06791_b200 import kernels
+    from paper_2505_06791_b200.planner import Tree, extend
+    m, sc, sp = fx.robot("arm7"), fx.scene(scene_name), fx.spec(spec_name)
+    prs = fx.pairs()
+    if spec_name == "plane55":
+        root = np.array(next(x for x in fx.plans() if x["id"] == "shelf_plane55_800")["start"])
+    else:
+        root = prs[("upright" if spec_name == "upright" else "table_plane") + "_start"][3]
+    samples = kernels.halton_batch(m, 60, 1, 777)
+    agree = close = both = 0
+    for q in samples:
+        ctx = _ctx(m, sc, sp, width=16)
+        tree = Tree(root, "start")
+        out = extend(tree, q, ctx)
+        reason, q_end = _ref_extend(oracle, m, sc, sp, root, q)
+        dev = None if out.added else out.reason
+        agree += dev == reason
+        if out.added and reason is None:
+            both += 1
+            close += np.abs(tree.node(1) - q_end).max() < 2e-3
+    assert agree >= 0.9 * len(samples), agree
+    assert both >= 5 and close >= 0.9 * both, (both, close)
