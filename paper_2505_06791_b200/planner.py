@@ -147,7 +147,7 @@ class PlanProblem:
         object.__setattr__(self, "goal", self.model.check_q(self.goal))
 
 
-@dataclass
+@dataclass(slots=True)
 class PlanStats:
     iterations: int = 0
     extensions_attempted: int = 0
@@ -401,6 +401,15 @@ _RESULT_DT = np.dtype({"names": ["status", "setup_code", "path_len", "ns", "ng",
                        "itemsize": C.sizeof(_lib.Result)})
 
 
+def _solved(path, sources, stats) -> "PlanResult":
+    """PlanResult("Solved", path, sources, stats) without the frozen
+    dataclass's per-field __setattr__ round trips (the batch decoding loop
+    builds one per query)."""
+    r = object.__new__(PlanResult)
+    r.__dict__.update(status="Solved", path=path, edge_sources=sources, stats=stats, dense=None)
+    return r
+
+
 def _results_bulk(res, problems, paths, srcs, wall, pc):
     """PlanResults of a batch: one structured numpy view of the result array
     and bulk conversions instead of per-field ctypes access."""
@@ -409,6 +418,10 @@ def _results_bulk(res, problems, paths, srcs, wall, pc):
     plen = a["path_len"].tolist()
     ns, ng, dms = a["ns"].tolist(), a["ng"].tolist(), a["device_ms"].tolist()
     st = a["stats"].tolist()
+    # one copy of every returned row (the per-query paths are views of it)
+    lmax = max(plen) if plen else 0
+    rows = np.array(paths[:, :lmax]) if lmax else paths[:, :0]
+    src_of = _SRC.__getitem__
     out = []
     for i, p in enumerate(problems):
         s = st[i]
@@ -417,11 +430,10 @@ def _results_bulk(res, problems, paths, srcs, wall, pc):
         code = status[i]
         if code == 0:
             L = plen[i]
-            path = list(paths[i, :L].copy())
+            path = list(rows[i, :L])
             path[0] = p.start.copy()                 # roots are the exact FP64 endpoints
             path[-1] = p.goal.copy()
-            out.append(PlanResult("Solved", tuple(path), tuple(_SRC[k] for k in srcs[i, :L - 1].tolist()),
-                                  stats))
+            out.append(_solved(tuple(path), tuple(map(src_of, srcs[i, :L - 1].tolist())), stats))
         elif code == -1:
             if len(problems) == 1:
                 raise PlanSetupError(_SETUP.get(int(a["setup_code"][0]), "invalid start/goal"))
