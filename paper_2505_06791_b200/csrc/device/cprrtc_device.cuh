@@ -1024,8 +1024,22 @@ __device__ __noinline__ ValOut cp_validate_cull(const Team tm, const float (*seg
     bool hit = false, stop = false;
     i64 narrow = 0, bound = 0;
     const float4* cl = sc.cl;
+    // superchunk bounds (8 chunks each) after the chunks: a group the team's
+    // robot boxes miss skips all 64 of its primitives with one test and vote
+    const int nbg = (sc.nbc + 7) >> 3, neg = (sc.nec + 7) >> 3;
+    const float4* gb = cl + CP_BCH * sc.nbc + CP_SCH * sc.nec;
+    const float4* gs = gb + 2 * nbg;
 #pragma unroll 1
-    for (int k = 0; k < sc.nbc && !stop; k++) {
+    for (int g = 0; g < nbg && !stop; g++) {
+    {
+        const float4 gc = cp_lds4(gb + 2 * g), gh = cp_lds4(gb + 2 * g + 1);
+        const bool gov = fabsf(rc.x - gc.x) <= rh.x + gh.x && fabsf(rc.y - gc.y) <= rh.y + gh.y &&
+                         fabsf(rc.z - gc.z) <= rh.z + gh.z;
+        if (!tm.any(gov)) continue;
+    }
+    const int kend = min(8 * g + 8, sc.nbc);
+#pragma unroll 1
+    for (int k = 8 * g; k < kend && !stop; k++) {
         const float4* ch = cl + CP_BCH * k;
         const float4 bc = cp_lds4(ch), bh = cp_lds4(ch + 1);
         const bool ov = fabsf(rc.x - bc.x) <= rh.x + bh.x && fabsf(rc.y - bc.y) <= rh.y + bh.y &&
@@ -1056,9 +1070,19 @@ __device__ __noinline__ ValOut cp_validate_cull(const Team tm, const float (*seg
         }
         if (flag_on && tm.any(hit)) stop = true;   // the shared collision flag
     }
+    }
     const float4* cs = cl + CP_BCH * sc.nbc;
 #pragma unroll 1
-    for (int k = 0; k < sc.nec && !stop; k++) {
+    for (int g = 0; g < neg && !stop; g++) {
+    {
+        const float4 gc = cp_lds4(gs + 2 * g), gh = cp_lds4(gs + 2 * g + 1);
+        const bool gov = fabsf(rc.x - gc.x) <= rh.x + gh.x && fabsf(rc.y - gc.y) <= rh.y + gh.y &&
+                         fabsf(rc.z - gc.z) <= rh.z + gh.z;
+        if (!tm.any(gov)) continue;
+    }
+    const int kend = min(8 * g + 8, sc.nec);
+#pragma unroll 1
+    for (int k = 8 * g; k < kend && !stop; k++) {
         const float4* ch = cs + CP_SCH * k;
         const float4 bc = cp_lds4(ch), bh = cp_lds4(ch + 1);
         const bool ov = fabsf(rc.x - bc.x) <= rh.x + bh.x && fabsf(rc.y - bc.y) <= rh.y + bh.y &&
@@ -1086,6 +1110,7 @@ __device__ __noinline__ ValOut cp_validate_cull(const Team tm, const float (*seg
             }
         }
         if (flag_on && tm.any(hit)) stop = true;
+    }
     }
     if (!stop && CP_P > 0) {
 #pragma unroll 1
@@ -1465,7 +1490,8 @@ __device__ void cp_plan_query(const Team& tm, TeamWS& ws, const PlanArgs& A, con
 
 __host__ __device__ __forceinline__ int cp_pad8(int x) { return (x + CP_CHUNK - 1) / CP_CHUNK * CP_CHUNK; }
 __device__ __forceinline__ int cp_scene_f4(const SceneSm& g) {
-    return g.cull ? CP_BCH * g.nbc + CP_SCH * g.nec : 2 * cp_pad8(g.nb) + cp_pad8(g.ne);
+    return g.cull ? CP_BCH * g.nbc + CP_SCH * g.nec + 2 * ((g.nbc + 7) / 8 + (g.nec + 7) / 8)
+                  : 2 * cp_pad8(g.nb) + cp_pad8(g.ne);
 }
 
 // Stage the scene into shared memory.  Reference order: padded to whole
@@ -1474,7 +1500,7 @@ __device__ __forceinline__ int cp_scene_f4(const SceneSm& g) {
 __device__ __forceinline__ SceneSm cp_stage_scene(const SceneSm& g, float4* sm) {
     SceneSm s = g;
     if (g.cull) {
-        const int tot = CP_BCH * g.nbc + CP_SCH * g.nec;
+        const int tot = cp_scene_f4(g);
         for (int i = threadIdx.x; i < tot; i += blockDim.x) sm[i] = g.cl[i];
         __syncthreads();
         s.cl = sm;

@@ -469,7 +469,7 @@ int pad8(int x) { return (x + 7) / 8 * 8; }
 
 // float4s staged per CTA (cp_scene_f4 in the device code)
 size_t scene_f4(int nb, int ne, int nbc, int nec, int cull) {
-    return cull ? (size_t)(18 * nbc + 10 * nec) : (size_t)(2 * pad8(nb) + pad8(ne));
+    return cull ? (size_t)(18 * nbc + 10 * nec + 2 * ((nbc + 7) / 8 + (nec + 7) / 8)) : (size_t)(2 * pad8(nb) + pad8(ne));
 }
 size_t scene_smem(Ctx* c, int cull = 0) { return scene_f4(c->nb, c->ne, c->nbc, c->nec, cull) * sizeof(float4); }
 
@@ -520,13 +520,19 @@ static void build_clusters(const cprrtc_scene* s, std::vector<float4>& out, int&
     const float4 far = make_float4(1e18f, 1e18f, 1e18f, 0.f);
     const float4 zero = make_float4(0.f, 0.f, 0.f, 0.f);
     out.clear();
+    // superchunk bounds (groups of 8 chunks = 64 primitives), appended after
+    // the chunks: [box groups (c, h)] [sphere groups (c, h)]
+    std::vector<float4> groups[2];
     for (int kind = 0; kind < 2; kind++) {
         const int n = kind ? ne : nb;
         std::vector<std::pair<uint64_t, int>> ord(n);
         for (int i = 0; i < n; i++) ord[i] = {morton(kind, i), i};
         std::sort(ord.begin(), ord.end());
         const int chunks = (n + 7) / 8;
+        double glo[3], ghi[3];
         for (int k = 0; k < chunks; k++) {
+            if (k % 8 == 0)
+                for (int d = 0; d < 3; d++) { glo[d] = INFINITY; ghi[d] = -INFINITY; }
             double blo[3] = {INFINITY, INFINITY, INFINITY}, bhi[3] = {-INFINITY, -INFINITY, -INFINITY};
             std::vector<float4> a(8), b(8);
             for (int j = 0; j < 8; j++) {
@@ -558,9 +564,18 @@ static void build_clusters(const cprrtc_scene* s, std::vector<float4>& out, int&
             for (int j = 0; j < 8; j++) out.push_back(a[j]);
             if (kind == 0)
                 for (int j = 0; j < 8; j++) out.push_back(b[j]);
+            for (int d = 0; d < 3; d++) { glo[d] = std::min(glo[d], blo[d]); ghi[d] = std::max(ghi[d], bhi[d]); }
+            if (k % 8 == 7 || k == chunks - 1) {
+                float4 gc, gh;
+                bound(glo, ghi, gc, gh);
+                groups[kind].push_back(gc);
+                groups[kind].push_back(gh);
+            }
         }
         (kind ? nec : nbc) = chunks;
     }
+    out.insert(out.end(), groups[0].begin(), groups[0].end());
+    out.insert(out.end(), groups[1].begin(), groups[1].end());
 }
 
 size_t team_smem(Ctx* c, Module* m, bool with_scene) {
