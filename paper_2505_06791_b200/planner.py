@@ -410,6 +410,25 @@ def _solved(path, sources, stats) -> "PlanResult":
     return r
 
 
+def _result_one(r, p, paths_i, srcs_i, wall, pc) -> "PlanResult":
+    """The single-query latency path's decoding (one ctypes result)."""
+    s = r.stats[:]
+    stats = PlanStats(s[0], s[1], s[2], s[3], s[4], s[5], s[6], wall, r.nodes_start, r.nodes_goal,
+                      r.device_ms, s[8], s[9], s[10], s[11])
+    code = r.status
+    if code == 0:
+        L = r.path_len
+        path = list(paths_i[:L].copy())
+        path[0] = p.start.copy()                 # roots are the exact FP64 endpoints
+        path[-1] = p.goal.copy()
+        return _solved(tuple(path), tuple(map(_SRC.__getitem__, srcs_i[:L - 1].tolist())), stats)
+    if code == -1:
+        raise PlanSetupError(_SETUP.get(r.setup_code, "invalid start/goal"))
+    if code == 4:
+        raise RuntimeError(f"solution path longer than path_capacity={pc}")
+    return PlanResult(_STATUS.get(code, "IterLimit"), None, None, stats)
+
+
 def _results_bulk(res, problems, paths, srcs, wall, pc):
     """PlanResults of a batch: one structured numpy view of the result array
     and bulk conversions instead of per-field ctypes access."""
@@ -511,7 +530,7 @@ def _plan_one(problem: PlanProblem, options: DeviceOptions, return_dense: bool) 
         rc = ctx.L.cprrtc_plan(ctx.h, C.byref(prm), 1, *io.args)
         wall = (time.perf_counter() - t0) * 1e3
         _lib.check(rc, "plan")
-        res = _results_bulk(io.res, (problem,), io.paths, io.srcs, wall, pc)[0]
+        res = _result_one(io.res[0], problem, io.paths[0], io.srcs[0], wall, pc)
         if return_dense and res.solved:
             L = len(res.path)
             dense, ok = _derive(ctx, prm, io.paths[0, :L], io.srcs[0, :L - 1])
