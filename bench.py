@@ -268,7 +268,7 @@ def run_b200(args, world, rank, local):
                      "peak": fp32_peak, "unit": "TFLOP/s", "frac": achieved / fp32_peak,
                      "peak_source": f"nominal FP32 FMA ({sms} SM x 128 lanes x 2 x {max_mhz} MHz); "
                                     "MEASURED_PEAKS.json has no FP32 entry",
-                     "traffic": None,
+                     "traffic": _ncu_traffic("cp_plan_kernel"),
                      "work": "stage1 x 1750 + cc_fk x 1195 + checks x 11 + nn_nodes x 20 flop"},
     }
     if rank == 0 and not args.no_extras:
@@ -321,7 +321,7 @@ def extras(args, local, model, line):
                             "kernel": f"cp_validate_cull_kernel (999 boxes, {B} motions x {W})"}
     out["roofline_cc"] = {"bound": "fp32", "kernel": f"cp_validate_kernel (999 boxes, {B} motions x {W})",
                           "achieved": cc_flops / s_off / 1e12, "peak": peak, "unit": "TFLOP/s",
-                          "frac": cc_flops / s_off / 1e12 / peak, "traffic": None,
+                          "frac": cc_flops / s_off / 1e12 / peak, "traffic": _ncu_traffic("cp_validate_kernel"),
                           "kernel_ms": best["kernel_ms"]}
     # -- NN scan streaming: 4736 distinct trees of 16384 nodes (2.2 GB > L2)
     T, N = 2368, 16384
@@ -334,7 +334,8 @@ def extras(args, local, model, line):
     hbm = _measured_hbm()
     out["roofline_nn"] = {"bound": "hbm", "kernel": f"cp_nearest_kernel ({T} trees x {N} nodes, SoA float4)",
                           "achieved": gbs, "peak": hbm[0], "unit": "GB/s", "frac": gbs / hbm[0],
-                          "peak_source": hbm[1], "traffic": None, "kernel_ms": ms}
+                          "peak_source": hbm[1], "traffic": _ncu_traffic("cp_nearest_kernel"),
+                          "algorithmic_bytes": T * N * BYTES_NN7, "kernel_ms": ms}
     # -- batched queries (configs[4]): 1024 table-plane queries in one launch
     m, sc2, sp = fx.robot("arm7"), fx.scene("table"), fx.spec("table_plane")
     prs = fx.pairs()
@@ -490,6 +491,23 @@ def _cpu_generic(model, scene, spec, s, g, kw, budget):
     r = orc.plan(model.packed, scene.packed(), None if spec is None else spec.packed, s, g,
                  max_iterations=10**6, time_budget_ms=budget, **kw)
     return r["status"] == "Solved", (time.perf_counter() - t0) * 1e3
+
+
+def _ncu_traffic(kernel):
+    """DRAM bytes per launch of `kernel` from the newest committed ncu --set full
+    summary (profiles/*_traffic.json, tools/summarize_profiles.py), or None."""
+    import glob
+    files = sorted(glob.glob(os.path.join(ROOT, "profiles", "r*_traffic.json")), key=os.path.getmtime)
+    for f in reversed(files):
+        try:
+            with open(f) as fh:
+                d = json.load(fh)
+            if kernel in d:
+                return {"dram_bytes_per_launch": d[kernel]["dram_bytes_per_launch"],
+                        "source": os.path.relpath(f, ROOT)}
+        except Exception:
+            continue
+    return None
 
 
 def _measured_hbm():

@@ -61,11 +61,12 @@ for kern, rep in (("cp_plan_kernel", f"prof_plan_{TAG}.ncu-rep"), ("cp_validate_
                      if k.startswith("smsp__pcsamp_warps_issue_stalled") and not k.endswith("not_issued")),
                     key=lambda kv: -kv[1])[:6]
     lines += ["", "top stall reasons (pc samples): " + ", ".join(f"{k.split('stalled_')[1]} {int(v)}" for k, v in stalls), ""]
-    rd = num(r.get("dram__bytes_read.sum", ("0", ""))[0]) or 0
-    wr = num(r.get("dram__bytes_write.sum", ("0", ""))[0]) or 0
-    ur = r.get("dram__bytes_read.sum", ("", ""))[1]
-    scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}.get(ur, 1)
-    traffic[kern] = {"dram_bytes_per_launch": (rd + wr) * scale,
+    units = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
+
+    def nbytes(key):
+        v, u = r.get(key, ("0", "byte"))
+        return (num(v) or 0) * units.get(u, 1)
+    traffic[kern] = {"dram_bytes_per_launch": nbytes("dram__bytes_read.sum") + nbytes("dram__bytes_write.sum"),
                      "duration": r.get("gpu__time_duration.sum")}
 lc = os.path.join(G, f"launches_{TAG}.csv")
 if os.path.exists(lc):
