@@ -497,7 +497,7 @@ def _ncu_traffic(kernel):
     """DRAM bytes per launch of `kernel` from the newest committed ncu --set full
     summary (profiles/*_traffic.json, tools/summarize_profiles.py), or None."""
     import glob
-    files = sorted(glob.glob(os.path.join(ROOT, "profiles", "r*_traffic.json")), key=os.path.getmtime)
+    files = sorted(glob.glob(os.path.join(ROOT, "profiles", "r*_traffic.json")))   # r1 < r1b < ... < r2
     for f in reversed(files):
         try:
             with open(f) as fh:
