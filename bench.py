@@ -494,8 +494,9 @@ def _cpu_generic(model, scene, spec, s, g, kw, budget):
 
 
 def _ncu_traffic(kernel):
-    """DRAM bytes per launch of `kernel` from the newest committed ncu --set full
-    summary (profiles/*_traffic.json, tools/summarize_profiles.py), or None."""
+    """DRAM bytes (read + write) per launch of `kernel` from the newest
+    committed ncu --set full summary (profiles/r*_traffic.json, written by
+    tools/summarize_profiles.py from the capture of the same kernel), or None."""
     import glob
     files = sorted(glob.glob(os.path.join(ROOT, "profiles", "r*_traffic.json")))   # r1 < r1b < ... < r2
     for f in reversed(files):
@@ -503,8 +504,7 @@ def _ncu_traffic(kernel):
             with open(f) as fh:
                 d = json.load(fh)
             if kernel in d:
-                return {"dram_bytes_per_launch": d[kernel]["dram_bytes_per_launch"],
-                        "source": os.path.relpath(f, ROOT)}
+                return float(d[kernel]["dram_bytes_per_launch"])
         except Exception:
             continue
     return None
