@@ -1426,6 +1426,248 @@ __device__ __noinline__ int cp_extend_once(const Team& tm, TeamWS& ws, const Pla
     return node < 0 ? -4 : node;
 }
 
+// ===========================================================================
+// Pair mode (single queries): a team is two warps.  Warp P draws samples and
+// runs the P1 projections of the extension and of the greedy connect; warp C
+// certifies each motion P produced -- derive_edge's re-projection when the
+// endpoint moved, the collision check, the append -- one motion behind P, so
+// the certification of motion k overlaps P1 of motion k+1 (planner.py:265-306
+// and :361-409 evaluated in the same order; P posts motion k+1 only after C
+// accepted motion k, whose node is its parent).
+// ===========================================================================
+// The pair's mailbox (shared memory, in the unused half-team slot of P's
+// warp): two mbarriers -- `full` (P's 16 lanes arrive after writing a job, C
+// waits), `done` (C's 16 lanes arrive after finishing it, P waits) -- give the
+// hand-offs release / acquire ordering without a CTA barrier.
+struct PairBox {
+    unsigned long long full, done;   // mbarriers
+    int result;                      // new node index, or -2 projection, -3 collision, -4 full
+    int qi, tree, parent, derive, exit;
+    int p_ndone, p_pend;             // P's bookkeeping: done phases consumed, a result outstanding
+    float from[CP_NP], to[CP_NP];
+};
+__device__ __forceinline__ PairBox* cp_pair_box(TeamWS* slot) {
+    return reinterpret_cast<PairBox*>((reinterpret_cast<unsigned long long>(slot) + 7ull) & ~7ull);
+}
+__device__ __forceinline__ unsigned cp_smem_addr(const void* p) { return (unsigned)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ void cp_mb_init(unsigned long long* b, int count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(cp_smem_addr(b)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void cp_mb_arrive(unsigned long long* b) {
+    asm volatile("{ .reg .b64 st; mbarrier.arrive.shared::cta.b64 st, [%0]; }" ::"r"(cp_smem_addr(b)) : "memory");
+}
+__device__ __forceinline__ void cp_mb_wait(unsigned long long* b, int parity) {
+    unsigned ok = 0;
+    while (!ok) {
+        asm volatile("{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2; selp.u32 %0, 1, 0, p; }"
+                     : "=r"(ok)
+                     : "r"(cp_smem_addr(b)), "r"(parity)
+                     : "memory");
+    }
+}
+
+// P: consume the outstanding job's completion, if any
+__device__ __forceinline__ void cp_pair_wait_idle(const Team& tm, PairBox& bx) {
+    tm.sync();
+    if (bx.p_pend) {
+        cp_mb_wait(&bx.done, bx.p_ndone & 1);
+        tm.sync();
+        if (tm.lane == 0) { bx.p_ndone = bx.p_ndone + 1; bx.p_pend = 0; }
+    }
+    tm.sync();
+}
+
+// post a certification job; from / to are team vectors (lanes < CP_N)
+__device__ __forceinline__ void cp_pair_post(const Team& tm, PairBox& bx, TeamWS& wsc, int qi, int tree,
+                                             int parent, bool derive, const float* from, const float* to,
+                                             const float (*seg)[CP_NP], int W, int exit_job = 0) {
+    cp_pair_wait_idle(tm, bx);
+    if ((int)tm.lane < CP_N) { bx.from[tm.lane] = from[tm.lane]; bx.to[tm.lane] = to[tm.lane]; }
+    if (!exit_job && !derive && (int)tm.lane < W)   // the P1 motion itself is the canonical edge
+#pragma unroll
+        for (int k = 0; k < CP_N; k++) wsc.seg[tm.lane][k] = seg[tm.lane][k];
+    if (tm.lane == 0) {
+        bx.qi = qi; bx.tree = tree; bx.parent = parent; bx.derive = derive ? 1 : 0; bx.exit = exit_job;
+        bx.p_pend = 1;
+    }
+    tm.sync();
+    cp_mb_arrive(&bx.full);   // every lane: release of its own writes
+}
+
+__device__ __forceinline__ int cp_pair_result(const Team& tm, PairBox& bx) {
+    cp_pair_wait_idle(tm, bx);
+    return tm.bcast(bx.result, 0);
+}
+
+// warp C: certify jobs until P posts the exit job
+__device__ void cp_pair_certifier(const Team& tm, TeamWS& ws, PairBox& bx, const PlanArgs& A, const SceneSm& sc) {
+    for (int nfull = 0;; nfull++) {
+        cp_mb_wait(&bx.full, nfull & 1);
+        tm.sync();
+        if (bx.exit) break;
+        const int qi = bx.qi, tree = bx.tree;
+        QueryState& Q = A.qs[qi];
+        Stats st;
+        int res;
+        bool ok;
+        if (bx.derive) {
+            if ((int)tm.lane < CP_N) { ws.qr[tm.lane] = bx.from[tm.lane]; ws.qn[tm.lane] = bx.to[tm.lane]; }
+            tm.sync();
+            const unsigned long long pf0 = st.v[ST_PFAIL];
+            ok = cp_derive_edge(tm, ws, A, sc, ws.qr, ws.qn, st, &Q.stop);
+            res = ok ? 0 : (st.v[ST_PFAIL] != pf0 ? -2 : -3);
+        } else {
+            ok = cp_check_motion(tm, ws, A, sc, st);
+            res = ok ? 0 : -3;
+        }
+        if (ok) {
+            if ((int)tm.lane < CP_N) ws.qe[tm.lane] = bx.to[tm.lane];
+            tm.sync();
+            const int node = cp_append(tm, A, Q, qi, tree, ws.qe, bx.parent);
+            res = node < 0 ? -4 : node;
+        }
+        if (tm.lane == 0) {
+#pragma unroll
+            for (int i = 0; i < ST_NSTAT; i++)
+                if (st.v[i]) atomicAdd(&Q.stats[i], st.v[i]);
+            bx.result = res;
+        }
+        tm.sync();
+        cp_mb_arrive(&bx.done);   // every lane: release
+    }
+}
+
+// warp P: the sampling / projection side of cp_plan_query
+__device__ void cp_plan_query_pair(const Team& tm, TeamWS& ws, TeamWS& wsc, PairBox& bx, const PlanArgs& A,
+                                   const SceneSm& sc, int qi) {
+    QueryState& Q = A.qs[qi];
+    Stats st;
+    const int W = A.W;
+    for (;;) {
+        if (cp_should_stop(tm, Q, A)) break;
+        int it = 0;
+        if (tm.lane == 0) it = atomicAdd(&Q.next_sample, 1) + 1;
+        it = tm.bcast(it, 0);
+        if (it > A.max_iterations) {
+            if (tm.lane == 0) atomicExch(&Q.exhausted, 1);
+            break;
+        }
+        st.v[ST_ITER]++;
+        st.v[ST_ATT]++;
+        const int a = (it - 1) & 1, b = a ^ 1;
+        if ((int)tm.lane < CP_N) ws.qr[tm.lane] = (float)cp_halton((i64)it + Q.seed_offset, tm.lane);
+        tm.sync();
+        // extension P1 (planner.py:265-281)
+        const int cnt_a = cp_count(A, Q, a);
+        st.v[ST_NNODES] += cnt_a;
+        const int inear = cp_nearest(tm, cp_tree(A, qi, a), A.cap, cnt_a, ws.qr);
+        cp_load_node(tm, A, qi, a, inear, ws.qn);
+        cp_steer(tm, ws.qn, ws.qr, A.step, ws.qs);
+        if (cp_vec_equal(tm, ws.qs, ws.qn)) continue;
+        cp_interp(tm, ws.seg, W, ws.qn, ws.qs);
+        int pit, ppr;
+        bool okp = cp_project(tm, ws.seg, W, A.pa, &pit, &ppr, nullptr, nullptr, &st.v[ST_STAGE1], &Q.stop);
+        if (pit < 0) break;
+        st.v[ST_PROJITER] += pit;
+        if (!okp) { st.v[ST_PFAIL]++; continue; }
+        cp_copy(tm, ws.qe, ws.seg[W - 1]);
+        if (cp_vec_equal(tm, ws.qe, ws.qn)) continue;
+        cp_pair_post(tm, bx, wsc, qi, a, inear, !cp_vec_equal(tm, ws.qe, ws.qs), ws.qn, ws.qe, ws.seg, W);
+        // greedy connect of tree b toward q_new while C certifies the extension
+        cp_copy(tm, ws.qt, ws.qe);
+        const int cnt_b = cp_count(A, Q, b);
+        st.v[ST_NNODES] += cnt_b;
+        int icur = cp_nearest(tm, cp_tree(A, qi, b), A.cap, cnt_b, ws.qt);
+        cp_load_node(tm, A, qi, b, icur, ws.qc);
+        float dist = cp_vec_dist(tm, ws.qc, ws.qt);
+        int node = -1, meet = -1;
+        bool pending_ext = true, stop = false, full = false;
+        int prev = -1;          // node of the last accepted connect motion
+        bool pending_con = false;
+        if (dist <= A.tol) {
+            node = cp_pair_result(tm, bx);
+            pending_ext = false;
+            if (node == -4) full = true;
+            if (node >= 0) meet = icur;
+        } else {
+            for (int segs = 0; segs < A.max_connect; segs++) {
+                if (cp_should_stop(tm, Q, A)) { stop = true; break; }
+                cp_steer(tm, ws.qc, ws.qt, A.step, ws.qs);
+                cp_interp(tm, ws.seg, W, ws.qc, ws.qs);
+                int it2, pr2;
+                const bool ok1 = cp_project(tm, ws.seg, W, A.pa, &it2, &pr2, nullptr, nullptr, &st.v[ST_STAGE1],
+                                            &Q.stop);
+                if (it2 >= 0) st.v[ST_PROJITER] += it2;
+                // the previous motion must be accepted before this one builds on it
+                if (pending_ext) {
+                    node = cp_pair_result(tm, bx);
+                    pending_ext = false;
+                    if (node < 0) { full = node == -4; break; }
+                } else if (pending_con) {
+                    prev = cp_pair_result(tm, bx);
+                    pending_con = false;
+                    if (prev < 0) { full = prev == -4; break; }
+                    icur = prev;
+                }
+                if (it2 < 0) { stop = true; break; }
+                if (!ok1) { st.v[ST_PFAIL]++; break; }
+                cp_copy(tm, ws.qe, ws.seg[W - 1]);
+                const float nd = cp_vec_dist(tm, ws.qe, ws.qt);
+                if (!(nd < dist)) break;
+                cp_pair_post(tm, bx, wsc, qi, b, icur, !cp_vec_equal(tm, ws.qe, ws.qs), ws.qc, ws.qe, ws.seg, W);
+                pending_con = true;
+                cp_copy(tm, ws.qc, ws.qe);
+                dist = nd;
+                if (dist <= A.tol) {
+                    const int r = cp_pair_result(tm, bx);
+                    pending_con = false;
+                    if (r >= 0) meet = r;
+                    else full = r == -4;
+                    break;
+                }
+            }
+            // drain: motions still being certified are kept (the reference
+            // appends every accepted motion of a trapped connect too)
+            if (pending_ext) { node = cp_pair_result(tm, bx); pending_ext = false; if (node == -4) full = true; }
+            if (pending_con) { const int r = cp_pair_result(tm, bx); if (r == -4) full = true; }
+        }
+        if (node >= 0) st.v[ST_ADDED]++;
+        if (full) {
+            if (tm.lane == 0) { atomicExch(&Q.overflow, 1); atomicExch(&Q.stop, 1); }
+            break;
+        }
+        if (stop) break;
+        if (node < 0 || meet < 0) continue;
+        // junction (planner.py:466-481): q_new (tree a) against the meet node (tree b)
+        cp_load_node(tm, A, qi, b, meet, ws.qm);
+        const float* js = a == 0 ? ws.qt : ws.qm;
+        const float* jg = a == 0 ? ws.qm : ws.qt;
+        bool ok = cp_vec_equal(tm, js, jg);
+        if (!ok) {
+            cp_copy(tm, ws.qr, js);
+            cp_copy(tm, ws.qn, jg);
+            ok = cp_derive_edge(tm, ws, A, sc, ws.qr, ws.qn, st, &Q.stop);
+        }
+        if (ok) {
+            if (tm.lane == 0 && atomicCAS(&Q.solved, 0, 1) == 0) {
+                Q.meet[a] = node;
+                Q.meet[b] = meet;
+                Q.t_end_ns = cp_clock_ns();
+                __threadfence();
+                atomicExch(&Q.stop, 1);
+                for (int r = 0; r < A.n_race; r++) *(volatile int*)A.race_peers[r] = 1;
+                if (A.n_race) __threadfence_system();
+            }
+            break;
+        }
+    }
+    if (tm.lane == 0) {
+#pragma unroll
+        for (int i = 0; i < ST_NSTAT; i++)
+            if (st.v[i]) atomicAdd(&Q.stats[i], st.v[i]);
+    }
+}
+
 // One team works on query qi until it is solved / stopped / out of samples.
 __device__ void cp_plan_query(const Team& tm, TeamWS& ws, const PlanArgs& A, const SceneSm& sc, int qi) {
     QueryState& Q = A.qs[qi];
@@ -1607,11 +1849,32 @@ cp_plan_kernel(const __grid_constant__ PlanArgs A) {
     extern __shared__ float4 cp_smem[];
     SceneSm sc = cp_stage_scene(A.scene_g, cp_smem);
     TeamWS* wsa = reinterpret_cast<TeamWS*>(cp_smem + cp_scene_f4(A.scene_g));
+    if (A.pair) {   // pair mailboxes live in shared memory: set them up before any warp uses one
+        for (int w = 2 * threadIdx.x; w < (int)(blockDim.x >> 5); w += 2 * blockDim.x) {
+            PairBox* b = cp_pair_box(&wsa[w * (32 / CP_G) + 1]);
+            cp_mb_init(&b->full, CP_G);
+            cp_mb_init(&b->done, CP_G);
+            b->p_ndone = 0;
+            b->p_pend = 0;
+        }
+        __syncthreads();
+    }
     // latency mode: one team per warp, so divergent teams never share a warp
     if (A.solo && (int)(threadIdx.x & 31) >= CP_G) return;
     Team tm;
     const int team_in_cta = (threadIdx.x >> 5) * (32 / CP_G) + (threadIdx.x & 31) / CP_G;
     TeamWS& ws = wsa[team_in_cta];
+    // pair mode (solo, CP_G = 16): odd warps certify for the even warp before
+    // them; the pair's mailbox is the unused half-team slot of the even warp
+    PairBox* bx = nullptr;
+    if (A.pair) {
+        const int w = threadIdx.x >> 5;
+        bx = cp_pair_box(&wsa[(w & ~1) * (32 / CP_G) + 1]);
+        if (w & 1) {
+            cp_pair_certifier(tm, ws, *bx, A, sc);
+            return;
+        }
+    }
     int visits = 0;
     for (;;) {
         int qi = -1;
@@ -1644,7 +1907,8 @@ cp_plan_kernel(const __grid_constant__ PlanArgs A) {
         if (qi < 0 || ++visits > 4 * A.nq + 4) break;
         QueryState& Q = A.qs[qi];
         if (tm.lane == 0) atomicAdd(&Q.active, 1);
-        cp_plan_query(tm, ws, A, sc, qi);
+        if (bx) cp_plan_query_pair(tm, ws, wsa[((threadIdx.x >> 5) + 1) * (32 / CP_G)], *bx, A, sc, qi);
+        else cp_plan_query(tm, ws, A, sc, qi);
         // the last team to leave the query extracts its result (a late
         // joiner may extract again: identical values)
         int last = 0;
@@ -1657,6 +1921,8 @@ cp_plan_kernel(const __grid_constant__ PlanArgs A) {
             cp_extract_query(tm, A, qi);
         }
     }
+    if (bx)   // release the certifier warp
+        cp_pair_post(tm, *bx, ws, 0, 0, 0, true, ws.qr, ws.qr, ws.seg, 0, 1);
 }
 
 #endif  // !CP_PARITY

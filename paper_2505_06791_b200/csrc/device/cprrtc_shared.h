@@ -100,7 +100,7 @@ struct PlanArgs {
     int* sources;          // (nq, path_cap) mapped host memory
     int* chain;            // (nq, path_cap) device scratch: path position -> node
     int path_cap;
-    int pad2_;
+    int pair;              // 1: two-warp teams (single queries; warp P projects, warp C certifies)
 };
 
 struct SetupArgs {

@@ -1305,6 +1305,12 @@ static int plan_launch(Ctx* c, const cprrtc_params* prm, int B, const double* st
     }
     // single queries run one team per warp (latency); batches pack two (G=16)
     const bool solo = B == 1 && m->G == 16 && !(prm->teams < 0);
+    // two-warp teams (P projects, C certifies one motion behind) for single
+    // queries; CPRRTC_PAIR=0 restores one-warp teams.  r1 sweep (upright Panda,
+    // same box): one-warp 512 teams 0.204 ms median / p90 0.396; pairs 192 /
+    // 256 / 296 / 384 -> 0.195 / 0.197 / 0.198 / 0.206 ms, p90 0.358
+    static const bool pair_off = getenv("CPRRTC_PAIR") && atoi(getenv("CPRRTC_PAIR")) == 0;
+    const bool pair = solo && !pair_off;
     const int tpw = solo ? 1 : 32 / m->G;         // teams per warp
     const int max_tpc = solo ? kThreads / 32 : kThreads / m->G;   // teams per full CTA
     const int resident = m->plan_occ * c->sms * max_tpc;
@@ -1313,21 +1319,24 @@ static int plan_launch(Ctx* c, const cprrtc_params* prm, int B, const double* st
     // median -- or (batches) every resident team; never more than a quarter of the
     // sample budget so that at least ~4 waves of extensions build on each other
     // (samples are the reference's iterations)
-    long long want_teams = prm->teams > 0 ? prm->teams : (B == 1 ? 512 : (long long)resident);
+    long long want_teams = prm->teams > 0 ? prm->teams : (B == 1 ? (pair ? 256 : 512) : (long long)resident);
     long long budget_teams = (long long)B * prm->max_iterations / 4;
     if (budget_teams < tpw) budget_teams = tpw;
     if (want_teams > budget_teams) want_teams = budget_teams;
     if (want_teams > resident) want_teams = resident;
     // spread the teams over every SM first (latency of a team is set by how
     // many warps share its SM), then fill CTAs up to 256 threads
+    if (pair) want_teams *= 2;                    // warps: one P and one C per team
     long long per_cta = (want_teams + c->sms - 1) / c->sms;
     per_cta = (per_cta + tpw - 1) / tpw * tpw;
+    if (pair) per_cta = (per_cta + 1) / 2 * 2;    // whole pairs per CTA
     if (per_cta > max_tpc) per_cta = max_tpc;
     const int block = (int)(per_cta * 32 / tpw);
     int grid = (int)((want_teams + per_cta - 1) / per_cta);
     if (grid < 1) grid = 1;
     const size_t smem = scene_smem(c, A.scene_g.cull) + (size_t)(block / m->G) * m->ws_bytes;
     A.solo = solo ? 1 : 0;
+    A.pair = pair ? 1 : 0;
     if (int rc = upload_conf(c, m)) return rc;
     // the per-call sequence as one CUDA graph, replayed while shapes and
     // arguments repeat (inputs change only inside the pinned staging block)
