@@ -1307,8 +1307,8 @@ static int plan_launch(Ctx* c, const cprrtc_params* prm, int B, const double* st
     const bool solo = B == 1 && m->G == 16 && !(prm->teams < 0);
     // two-warp teams (P projects, C certifies one motion behind) for single
     // queries; CPRRTC_PAIR=0 restores one-warp teams.  r1 sweep (upright Panda,
-    // same box): one-warp 512 teams 0.204 ms median / p90 0.396; pairs 192 /
-    // 256 / 296 / 384 -> 0.195 / 0.197 / 0.198 / 0.206 ms, p90 0.358
+    // one box): one-warp 512 teams 0.202 ms median / p90 0.383; pairs 192 /
+    // 256 / 320 / 384 -> 0.178 / 0.177 / 0.185 / 0.186 ms, p90 0.334-0.343
     static const bool pair_off = getenv("CPRRTC_PAIR") && atoi(getenv("CPRRTC_PAIR")) == 0;
     const bool pair = solo && !pair_off;
     const int tpw = solo ? 1 : 32 / m->G;         // teams per warp
