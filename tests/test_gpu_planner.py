@@ -216,3 +216,34 @@ def test_upright_suite_matches_reference_success(oracle):
     assert solved[feas].all(), np.nonzero(feas & ~solved)[0]
     for k in np.nonzero(solved)[0][::4]:
         _check_path(oracle, probs[k], res[k])
+
+
+def test_one_warp_teams_fallback():
+    """CPRRTC_PAIR=0 (one-warp teams, the batch code path) still plans single
+    queries soundly; run in a subprocess because the switch is read once."""
+    import subprocess
+    import sys
+    code = r"""
+import sys, numpy as np
+sys.path[:0] = ['.', 'tests']
+import fixtures as fx
+from oracle import oracle
+from test_gpu_planner import _check_path
+from paper_2505_06791_b200.planner import PlanParams, PlanProblem, plan
+m, sc, sp = fx.robot('arm7'), fx.scene('table'), fx.spec('upright')
+prs = fx.pairs()
+feas = np.nonzero(fx.upright_feasible())[0][:6]
+for k in feas:
+    prob = PlanProblem(m, sc, sp, prs['upright_start'][k], prs['upright_goal'][k],
+                       PlanParams(width=16, max_iterations=10**6, seed_offset=int(k)))
+    r = plan(prob)
+    assert r.solved, r.status
+    _check_path(oracle, prob, r)
+print('ok')
+"""
+    import os
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = dict(os.environ, CPRRTC_PAIR="0")
+    out = subprocess.run([sys.executable, "-c", code], cwd=root, env=env, capture_output=True, text=True,
+                         timeout=600)
+    assert out.returncode == 0 and "ok" in out.stdout, out.stderr[-2000:]
