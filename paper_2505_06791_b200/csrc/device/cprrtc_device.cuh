@@ -659,8 +659,10 @@ __device__ __noinline__ bool cp_project(const Team tm, float (*seg)[CP_NP], int 
         bool aborted = false;
         for (int it = 1; it <= pa.max_iters; it++) {
             const bool act = row && t > prog;
+            // lane 0 loads the stop word (consumed after stage 1); r1 A/B: all
+            // 16 lanes loading it (volatile: one request each) cost 5 %
             int sf = 0;
-            if (stop_flag && t == 0) sf = *(const volatile int*)stop_flag;   // consumed after stage 1
+            if (stop_flag && t == 0) sf = *(const volatile int*)stop_flag;
             float xn[CP_N], xp[CP_N];
 #pragma unroll
             for (int k = 0; k < CP_N; k++) xp[k] = __shfl_up_sync(tm.mask, xc[k], 1, CP_G);

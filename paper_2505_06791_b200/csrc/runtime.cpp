@@ -352,6 +352,18 @@ std::string prelude(const Ctx* c, int G, int kind, int orient, int parity) {
     std::ostringstream os;
     os << "#define CP_G " << G << "\n#define CP_KIND " << kind << "\n#define CP_ORIENT " << orient
        << "\n#define CP_NTHREADS " << kThreads << "\n#define CP_PARITY " << parity << "\n";
+    // developer knob for same-box A/B runs: CPRRTC_DEFINES="NAME=VAL,NAME2" adds
+    // #defines to every module (and so to the cubin cache key)
+    if (const char* d = getenv("CPRRTC_DEFINES")) {
+        std::string all(d), item;
+        std::stringstream ss(all);
+        while (std::getline(ss, item, ',')) {
+            if (item.empty()) continue;
+            const size_t eq = item.find('=');
+            os << "#define " << (eq == std::string::npos ? item : item.substr(0, eq) + " " + item.substr(eq + 1))
+               << "\n";
+        }
+    }
     os << kSharedSrc << "\n" << c->robot_src << "\n";
     return os.str();
 }

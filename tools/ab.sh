@@ -1,0 +1,12 @@
+#!/usr/bin/env bash
+# same-box A/B of device-code variants: tools/ab.sh "DEFS_A" "DEFS_B" [rounds]
+# (DEFS = CPRRTC_DEFINES value, "" for the default build); prints median / p10 / p90 / e2e
+A="$1"; B="$2"; R=${3:-2}
+for r in $(seq $R); do
+  for v in A B; do
+    if [ $v = A ]; then D="$A"; else D="$B"; fi
+    CPRRTC_DEFINES="$D" timeout 300 python bench.py --steps 4 --warmup 2 --no-extras --no-cpu > gpurun_out/ab_tmp.json 2>/dev/null
+    python -c "
+import json; d=json.load(open('gpurun_out/ab_tmp.json')); print('$v [$D]', round(d['value'],4), round(d['p10_ms'],4), round(d['p90_ms'],4), round(d['e2e']['value'],4))" >> gpurun_out/ab.log
+  done
+done
