@@ -1428,6 +1428,8 @@ __device__ __noinline__ int cp_extend_once(const Team& tm, TeamWS& ws, const Pla
     return node < 0 ? -4 : node;
 }
 
+__device__ __noinline__ void cp_extract_path(const Team tm, const PlanArgs& A, int qi);   // below
+
 // ===========================================================================
 // Pair mode (single queries): a team is two warps.  Warp P draws samples and
 // runs the P1 projections of the extension and of the greedy connect; warp C
@@ -1654,6 +1656,7 @@ __device__ void cp_plan_query_pair(const Team& tm, TeamWS& ws, TeamWS& wsc, Pair
             ok = cp_derive_edge(tm, ws, A, sc, ws.qr, ws.qn, st, &Q.stop);
         }
         if (ok) {
+            int won = 0;
             if (tm.lane == 0 && atomicCAS(&Q.solved, 0, 1) == 0) {
                 Q.meet[a] = node;
                 Q.meet[b] = meet;
@@ -1662,7 +1665,9 @@ __device__ void cp_plan_query_pair(const Team& tm, TeamWS& ws, TeamWS& wsc, Pair
                 atomicExch(&Q.stop, 1);
                 for (int r = 0; r < A.n_race; r++) *(volatile int*)A.race_peers[r] = 1;
                 if (A.n_race) __threadfence_system();
+                won = 1;
             }
+            if (tm.bcast(won, 0)) cp_extract_path(tm, A, qi);   // while the other teams leave
             break;
         }
     }
@@ -1715,6 +1720,7 @@ __device__ void cp_plan_query(const Team& tm, TeamWS& ws, const PlanArgs& A, con
             ok = cp_derive_edge(tm, ws, A, sc, ws.qr, ws.qn, st, &Q.stop);
         }
         if (ok) {
+            int won = 0;
             if (tm.lane == 0 && atomicCAS(&Q.solved, 0, 1) == 0) {
                 Q.meet[a] = node;
                 Q.meet[b] = meet;
@@ -1724,7 +1730,9 @@ __device__ void cp_plan_query(const Team& tm, TeamWS& ws, const PlanArgs& A, con
                 // first-solution flag of a race: one store into every racer's word
                 for (int r = 0; r < A.n_race; r++) *(volatile int*)A.race_peers[r] = 1;
                 if (A.n_race) __threadfence_system();
+                won = 1;
             }
+            if (tm.bcast(won, 0)) cp_extract_path(tm, A, qi);   // while the other teams leave
             break;
         }
     }
@@ -1775,66 +1783,83 @@ __device__ __forceinline__ SceneSm cp_stage_scene(const SceneSm& g, float4* sm) 
 // loads) into a device index list; then the team gathers the node
 // coordinates and writes path and sources with contiguous lane-consecutive
 // stores (coalesced PCIe writes).  setup_code is written by cp_check_kernel.
-__device__ __noinline__ void cp_extract_query(const Team tm, const PlanArgs& A, int qi) {
+// The solved query's path (planner.py:488-505), by the team that solved it,
+// right away -- it overlaps the other teams' exit.  Lane 0 walks the two
+// parent chains (dependent L2 loads) into a device index list; then the team
+// gathers the node coordinates and writes path and sources with contiguous
+// lane-consecutive stores (coalesced PCIe writes).
+__device__ __noinline__ void cp_extract_path(const Team tm, const PlanArgs& A, int qi) {
     QueryState& Q = A.qs[qi];
     QueryOut& O = A.out[qi];
     const int lane = (int)tm.lane, cap = A.cap, path_cap = A.path_cap;
-    const int ns = min(cp_ldvol(&Q.count[0]), cap), ng = min(cp_ldvol(&Q.count[1]), cap);
-    if (lane < ST_NSTAT) O.stats[lane] = __ldcg(&Q.stats[lane]);
-    if (ST_NSTAT > CP_G && lane + CP_G < ST_NSTAT) O.stats[lane + CP_G] = __ldcg(&Q.stats[lane + CP_G]);
     const float* ts = cp_tree(A, qi, 0);
     const float* tg = cp_tree(A, qi, 1);
     const int* ps = cp_par(A, qi, 0);
     const int* pg = cp_par(A, qi, 1);
     int* ch = A.chain + (size_t)qi * path_cap;   // path position -> (tree << 30) | node
-    const int solved = cp_ldvol(&Q.solved);
     int status = 0, len = 0, ca = 0, skip = 0;
-    if (!solved) {
-        status = cp_ldvol(&Q.timed_out) ? 1 : (cp_ldvol(&Q.overflow) ? 3 : (cp_ldvol(&Q.race_stopped) ? 5 : 2));
-    } else {
-        if (lane == 0) {
-            const int m0 = cp_ldvol(&Q.meet[0]), m1 = cp_ldvol(&Q.meet[1]);
-            for (int i = m0;; i = __ldcg(ps + i)) {   // start chain, meet first
-                if (ca < path_cap) ch[ca] = i;
-                ca++;
-                if (__ldcg(ps + i) == i) break;
-            }
-            bool same = true;
-            for (int d = 0; d < CP_N; d++) same &= __ldcg(ts + (size_t)d * cap + m0) == __ldcg(tg + (size_t)d * cap + m1);
-            skip = same ? 1 : 0;
-            int cb = 0;
-            for (int i = m1;; i = __ldcg(pg + i)) {   // goal chain, meet first
-                if (!(cb == 0 && skip) && ca + cb - skip < path_cap) ch[ca + cb - skip] = (1 << 30) | i;
-                cb++;
-                if (__ldcg(pg + i) == i) break;
-            }
-            len = ca + cb - skip;
-            if (len > path_cap) status = 4;
-            else
-                for (int a = 0, b = ca - 1; a < b; a++, b--) { int t = ch[a]; ch[a] = ch[b]; ch[b] = t; }
+    if (lane == 0) {
+        const int m0 = cp_ldvol(&Q.meet[0]), m1 = cp_ldvol(&Q.meet[1]);
+        for (int i = m0;; i = __ldcg(ps + i)) {   // start chain, meet first
+            if (ca < path_cap) ch[ca] = i;
+            ca++;
+            if (__ldcg(ps + i) == i) break;
         }
-        status = tm.bcast(status, 0);
-        len = tm.bcast(len, 0);
-        ca = tm.bcast(ca, 0);
-        skip = tm.bcast(skip, 0);
-        __threadfence_block();
-        tm.sync();
-        if (status == 0) {
-            float* path = A.paths + (size_t)qi * path_cap * CP_N;
-            for (int f = lane; f < len * CP_N; f += CP_G) {
-                const int k = f / CP_N, d = f - k * CP_N;
-                const int e = ch[k];
-                path[f] = __ldcg(((e >> 30) ? tg : ts) + (size_t)d * cap + (e & 0x3fffffff));
-            }
-            // edge sources: start edges, then the junction (or the first goal
-            // edge when the meet nodes coincide), then goal edges
-            int* src = A.sources + (size_t)qi * path_cap;
-            for (int k = lane; k < len - 1; k += CP_G) src[k] = k < ca - 1 ? 0 : (k == ca - 1 ? (skip ? 2 : 1) : 2);
+        bool same = true;
+        for (int d = 0; d < CP_N; d++) same &= __ldcg(ts + (size_t)d * cap + m0) == __ldcg(tg + (size_t)d * cap + m1);
+        skip = same ? 1 : 0;
+        int cb = 0;
+        for (int i = m1;; i = __ldcg(pg + i)) {   // goal chain, meet first
+            if (!(cb == 0 && skip) && ca + cb - skip < path_cap) ch[ca + cb - skip] = (1 << 30) | i;
+            cb++;
+            if (__ldcg(pg + i) == i) break;
         }
+        len = ca + cb - skip;
+        if (len > path_cap) status = 4;
+        else
+            for (int a = 0, b = ca - 1; a < b; a++, b--) { int t = ch[a]; ch[a] = ch[b]; ch[b] = t; }
+    }
+    status = tm.bcast(status, 0);
+    len = tm.bcast(len, 0);
+    ca = tm.bcast(ca, 0);
+    skip = tm.bcast(skip, 0);
+    __threadfence_block();
+    tm.sync();
+    if (status == 0) {
+        float* path = A.paths + (size_t)qi * path_cap * CP_N;
+        for (int f = lane; f < len * CP_N; f += CP_G) {
+            const int k = f / CP_N, d = f - k * CP_N;
+            const int e = ch[k];
+            path[f] = __ldcg(((e >> 30) ? tg : ts) + (size_t)d * cap + (e & 0x3fffffff));
+        }
+        // edge sources: start edges, then the junction (or the first goal
+        // edge when the meet nodes coincide), then goal edges
+        int* src = A.sources + (size_t)qi * path_cap;
+        for (int k = lane; k < len - 1; k += CP_G) src[k] = k < ca - 1 ? 0 : (k == ca - 1 ? (skip ? 2 : 1) : 2);
     }
     if (lane == 0) {
         O.status = status;
         O.path_len = status == 0 ? len : 0;
+    }
+    tm.sync();
+}
+
+// The rest of the result, by the last team to leave the query (when the node
+// counts and the stats are final): counters, node counts, device time and,
+// for an unsolved query, its status.  setup_code is written by cp_check_kernel.
+__device__ __noinline__ void cp_extract_query(const Team tm, const PlanArgs& A, int qi) {
+    QueryState& Q = A.qs[qi];
+    QueryOut& O = A.out[qi];
+    const int lane = (int)tm.lane, cap = A.cap;
+    const int ns = min(cp_ldvol(&Q.count[0]), cap), ng = min(cp_ldvol(&Q.count[1]), cap);
+    if (lane < ST_NSTAT) O.stats[lane] = __ldcg(&Q.stats[lane]);
+    if (ST_NSTAT > CP_G && lane + CP_G < ST_NSTAT) O.stats[lane + CP_G] = __ldcg(&Q.stats[lane + CP_G]);
+    const int solved = cp_ldvol(&Q.solved);
+    if (lane == 0) {
+        if (!solved) {
+            O.status = cp_ldvol(&Q.timed_out) ? 1 : (cp_ldvol(&Q.overflow) ? 3 : (cp_ldvol(&Q.race_stopped) ? 5 : 2));
+            O.path_len = 0;
+        }
         O.n_nodes[0] = ns;
         O.n_nodes[1] = ng;
         Q.hwm[0] = ns;
