@@ -1321,6 +1321,8 @@ static int plan_launch(Ctx* c, const cprrtc_params* prm, int B, const double* st
     // queries; CPRRTC_PAIR=0 restores one-warp teams.  r1 sweep (upright Panda,
     // one box): one-warp 512 teams 0.202 ms median / p90 0.383; pairs 192 /
     // 256 / 320 / 384 -> 0.178 / 0.177 / 0.185 / 0.186 ms, p90 0.334-0.343
+    // (r1 A/B on the 999-box shelf: pairs also win for unconstrained queries,
+    // arm8 0.28 -> 0.23 ms, arm7 equal)
     static const bool pair_off = getenv("CPRRTC_PAIR") && atoi(getenv("CPRRTC_PAIR")) == 0;
     const bool pair = solo && !pair_off;
     const int tpw = solo ? 1 : 32 / m->G;         // teams per warp
