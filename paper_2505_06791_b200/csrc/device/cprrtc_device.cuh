@@ -1798,31 +1798,38 @@ __device__ __noinline__ void cp_extract_path(const Team tm, const PlanArgs& A, i
     const int* pg = cp_par(A, qi, 1);
     int* ch = A.chain + (size_t)qi * path_cap;   // path position -> (tree << 30) | node
     int status = 0, len = 0, ca = 0, skip = 0;
+    // the two parent chains are walked concurrently: lane 0 the start tree
+    // into ch[0..), lane 1 the goal tree into ch[path_cap - 1] downwards
+    const int m0 = cp_ldvol(&Q.meet[0]), m1 = cp_ldvol(&Q.meet[1]);
+    int cnt = 0;
     if (lane == 0) {
-        const int m0 = cp_ldvol(&Q.meet[0]), m1 = cp_ldvol(&Q.meet[1]);
         for (int i = m0;; i = __ldcg(ps + i)) {   // start chain, meet first
-            if (ca < path_cap) ch[ca] = i;
-            ca++;
+            if (cnt < path_cap) ch[cnt] = i;
+            cnt++;
             if (__ldcg(ps + i) == i) break;
         }
-        bool same = true;
-        for (int d = 0; d < CP_N; d++) same &= __ldcg(ts + (size_t)d * cap + m0) == __ldcg(tg + (size_t)d * cap + m1);
-        skip = same ? 1 : 0;
-        int cb = 0;
-        for (int i = m1;; i = __ldcg(pg + i)) {   // goal chain, meet first
-            if (!(cb == 0 && skip) && ca + cb - skip < path_cap) ch[ca + cb - skip] = (1 << 30) | i;
-            cb++;
+    } else if (lane == 1) {
+        for (int i = m1;; i = __ldcg(pg + i)) {   // goal chain, meet first, stored from the end
+            if (cnt < path_cap) ch[path_cap - 1 - cnt] = (1 << 30) | i;
+            cnt++;
             if (__ldcg(pg + i) == i) break;
         }
-        len = ca + cb - skip;
-        if (len > path_cap) status = 4;
-        else
-            for (int a = 0, b = ca - 1; a < b; a++, b--) { int t = ch[a]; ch[a] = ch[b]; ch[b] = t; }
     }
-    status = tm.bcast(status, 0);
-    len = tm.bcast(len, 0);
-    ca = tm.bcast(ca, 0);
-    skip = tm.bcast(skip, 0);
+    ca = tm.bcast(cnt, 0);
+    const int cb = tm.bcast(cnt, 1);
+    bool same = true;
+    for (int d = 0; d < CP_N; d++) same &= __ldcg(ts + (size_t)d * cap + m0) == __ldcg(tg + (size_t)d * cap + m1);
+    skip = same ? 1 : 0;
+    len = ca + cb - skip;
+    __threadfence_block();
+    tm.sync();
+    if (len > path_cap || ca + cb > path_cap) {
+        status = 4;
+    } else if (lane == 0) {
+        // start chain root..meet, then the goal chain meet..root (the meet node once if equal)
+        for (int a = 0, b = ca - 1; a < b; a++, b--) { int t = ch[a]; ch[a] = ch[b]; ch[b] = t; }
+        for (int k = skip; k < cb; k++) ch[ca + k - skip] = ch[path_cap - 1 - k];
+    }
     __threadfence_block();
     tm.sync();
     if (status == 0) {
