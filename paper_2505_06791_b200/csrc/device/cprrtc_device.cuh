@@ -11,10 +11,12 @@
 // Execution model: a team of CP_G lanes of one warp
 // owns one tree extension at a time -- lane t holds waypoint t of the motion
 // (the paper's "one thread per waypoint").  Alg. 1's barriers
-// become __syncwarp on the team mask, stage 2's prefix scan a ballot, and the
-// paper's shared-memory collision flag a team vote taken every
-// CP_CHUNK primitive checks.  Obstacles are staged once per CTA in shared
-// memory; trees are SoA float arrays in HBM with atomic append.
+// become a shuffle of row t-1 and a ballot, stage 2's prefix scan the ballot,
+// and the paper's shared-memory collision flag a team vote per
+// chunk of primitives.  Single queries pair two warps per team (warp P
+// projects, warp C certifies one motion behind, mbarrier hand-offs).
+// Obstacles are staged once per CTA in shared memory; trees are SoA float
+// arrays in HBM with atomic append.
 //
 // Every function cites the reference function it replaces
 // (maniplan/..., /root/reference/pkg/src/).
@@ -1964,8 +1966,8 @@ cp_plan_kernel(const __grid_constant__ PlanArgs A) {
 
 #endif  // !CP_PARITY
 
-// Per-query setup, FP64 (planner.py:416-427 _check_endpoint, :442-445 trees).
-// One CTA (64 threads) per query: warp 0 checks the start, warp 1 the goal.
+// FP64 endpoint test of one configuration (planner.py:416-427
+// _check_endpoint): limits, manifold, collision; one warp.
 
 __device__ int cp_check_config_d(const SetupArgs& S, const double* q, int lane) {
     // 1 limits, 2 manifold, 3 collision, 0 ok  (evaluated by all 32 lanes)
