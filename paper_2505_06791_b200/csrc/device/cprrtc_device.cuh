@@ -573,20 +573,130 @@ __device__ __noinline__ float cp_err_norm(const float* q) {
     return sqrtf(s);
 }
 
+// The iterations of Alg. 1 (pure.py:549-568) for the team's rows xc (lane t =
+// waypoint t).  UNC: tau_task = inf, validity needs no FK (pure.py:545) and the
+// update is computed only if the segment is not accepted as is.  The prefix
+// update is branch-free for both modes (contiguous prefix, pure.py:564-568;
+// literal-gap, pure.py:560-563); the stop word rides in bit 0 of the validity
+// ballot (lane 0 holds the fixed start, never active), so the poll costs no
+// extra warp collective.
+//
+// The poll is an asynchronous 16-byte copy of the stop word's L2 sector into
+// one of two shared-memory slots of the team (cp.async.cg, one commit group
+// per iteration: no register scoreboard); after stage 1 the loop reads the
+// copy issued one iteration earlier, behind cp.async.wait_group 1 -- which
+// never waits in practice (an iteration, ~1200 cycles, covers the L2 round
+// trip), wherever ptxas places it.  A stop is seen one iteration late.  r1
+// (B200): a plain load cost ~300 cycles per iteration of ~1500 (ptxas turned
+// its value into a predicate right after issue, stalling on the round trip),
+// and a same-iteration cp.async.wait_all was hoisted the same way.
+template <bool UNC, bool TRACE>
+__device__ __forceinline__ void cp_alg1_loop(const Team tm, int W, const ProjArgs& pa, float tau_sm,
+                                             float* xc, int& prog, int& iters, bool& ok, bool& aborted,
+                                             unsigned& s1, const int* stop_flag, int* pslot,
+                                             float* trace, int* trace_prog) {
+    const int t = (int)tm.lane;
+    const bool row = t < W;
+    const unsigned full = (W >= 32) ? 0xffffffffu : ((1u << W) - 1u);
+    // lane 0 polls (r1 A/B: all 16 lanes loading the word cost 5 %); the
+    // issue is predicated and the wait + read run on every lane, so the loop
+    // body stays one basic block (a branch around either cost ~100 cycles)
+    const bool poll = stop_flag && pslot && t == 0;
+    const unsigned long long sbase = (unsigned long long)stop_flag & ~15ull;
+    const unsigned slot = pslot ? (unsigned)__cvta_generic_to_shared(pslot) : 0u;   // 2 x 16 B slots
+    const unsigned soff = (unsigned)((unsigned long long)stop_flag - sbase);
+    // prologue poll into slot 0 (read by iteration 1)
+    asm volatile("{ .reg .pred p; setp.ne.u32 p, %2, 0; @p cp.async.cg.shared.global [%0], [%1], 16; "
+                 "cp.async.commit_group; }" ::"r"(slot), "l"(sbase), "r"((unsigned)poll));
+    const float tsm = tau_sm * 0.99999f;
+    for (int it = 1; it <= pa.max_iters; it++) {
+        const bool act = row && t > prog;
+        const unsigned put = slot + 16u * (it & 1), get = slot + 16u * ((it + 1) & 1) + soff;
+        asm volatile("{ .reg .pred p; setp.ne.u32 p, %2, 0; @p cp.async.cg.shared.global [%0], [%1], 16; "
+                     "cp.async.commit_group; }" ::"r"(put), "l"(sbase), "r"((unsigned)poll));
+        float xn[CP_N], xp[CP_N];
+#pragma unroll
+        for (int k = 0; k < CP_N; k++) xp[k] = __shfl_up_sync(tm.mask, xc[k], 1, CP_G);
+        bool valid = false, full_step = true;
+        if (UNC) {
+#pragma unroll
+            for (int k = 0; k < CP_N; k++) xn[k] = xc[k];
+            bool cheap = true;
+            if (act) {
+                float s2 = 0.f;
+                bool fin = true;
+#pragma unroll
+                for (int k = 0; k < CP_N; k++) { float d = xc[k] - xp[k]; s2 += d * d; fin &= cp_finite(xc[k]); }
+                cheap = fin && sqrtf(s2) < tsm;
+            }
+            if (!tm.any(!cheap)) { valid = act; full_step = false; }
+        }
+        if (!UNC || full_step) {
+            // every lane evaluates (branch-free stage 1); frozen / idle lanes
+            // discard the result
+            const bool v = cp_stage1(pa, xc, xp, tau_sm, xn);
+            valid = act && v;
+            s1 += act ? 1u : 0u;   // per lane; summed over the team at the end
+        }
+        int sf;   // lane 0 only; no "memory" clobber (it would pin stage 1's constant-bank reads)
+        asm volatile("{ .reg .pred p; setp.ne.u32 p, %2, 0; cp.async.wait_group 1; mov.u32 %0, 0; "
+                     "@p ld.shared.b32 %0, [%1]; }" : "=r"(sf) : "r"(get), "r"((unsigned)poll));
+        const unsigned vm = tm.ballot(valid || sf != 0) & full;
+        const unsigned hi = vm & ~((2u << prog) - 1u);              // literal-gap
+        const int np1 = hi ? 31 - __clz(hi) : prog;
+        const int run = __ffs(~(vm >> (prog + 1))) - 1;               // contiguous prefix
+        const int np0 = min(prog + (run < 0 ? 32 : run), W - 1);
+        const int np = pa.mode == 1 ? np1 : np0;
+        if (np == W - 1) {
+            if (TRACE) {
+                if (row) {
+#pragma unroll
+                    for (int k = 0; k < CP_N; k++) trace[((size_t)(it - 1) * W + t) * CP_N + k] = xc[k];
+                }
+                if (t == 0) trace_prog[it - 1] = np;
+            }
+            ok = true;
+            iters = it;
+            prog = np;
+            break;
+        }
+        if (vm & 1u) {   // the query is over: abandon
+            aborted = true;
+            break;
+        }
+        const bool upd = row && t > np;
+#pragma unroll
+        for (int k = 0; k < CP_N; k++) xc[k] = upd ? xn[k] : xc[k];
+        prog = np;
+        if (TRACE) {
+            if (row) {
+#pragma unroll
+                for (int k = 0; k < CP_N; k++) trace[((size_t)(it - 1) * W + t) * CP_N + k] = xc[k];
+            }
+            if (t == 0) trace_prog[it - 1] = np;
+        }
+    }
+    // the last poll lands before the slots are reused
+    asm volatile("cp.async.wait_all;" ::: "memory");
+}
+
 // Project the team's segment in place: Alg. 1 (pure.py:549-577) for modes
 // 0/1, the sequential baseline (pure.py:580-615) for mode 2, then the
 // clamp-and-revalidate finish (maniplan/projection.py:162-180).
 // seg rows [0, W) live in shared memory; lane t owns row t.
 // trace (optional, parity only): after every iteration the buffer is copied
 // to trace[it-1] and the prefix to trace_prog[it-1].
-// stop_flag (planner): the query's stop word, polled once per iteration with
-// the load's latency hidden behind stage 1; when it is set the projection is
-// abandoned (returns false with *iters_out = -1) so a team that lost the race
-// leaves within one iteration instead of finishing its projection.
+// stop_flag (planner): the query's stop word, polled once per iteration
+// through poll_slot (the team's 32-byte, 16-byte aligned shared-memory slot;
+// no poll without it) off the critical path (cp_alg1_loop); when it is set
+// the projection is abandoned (returns false with *iters_out = -1) so a team
+// that lost the race leaves within two iterations instead of finishing its
+// projection.
 __device__ __noinline__ bool cp_project(const Team tm, float (*seg)[CP_NP], int W,
                            const ProjArgs pa, int* iters_out, int* prog_out,
                            float* trace = nullptr, int* trace_prog = nullptr,
-                           unsigned long long* n_stage1 = nullptr, const int* stop_flag = nullptr) {
+                           unsigned long long* n_stage1 = nullptr, const int* stop_flag = nullptr,
+                           int* poll_slot = nullptr) {
     unsigned s1 = 0;
     const int t = (int)tm.lane;
     const bool row = t < W;
@@ -602,7 +712,6 @@ __device__ __noinline__ bool cp_project(const Team tm, float (*seg)[CP_NP], int 
         g = tm.maxf(g);
         tau_sm = g > 0.f ? 1.5f * g : 1e-6f;
     }
-    const unsigned full = (W >= 32) ? 0xffffffffu : ((1u << W) - 1u);
     int prog = 0, iters = pa.max_iters;
     bool ok = false;
     if (pa.mode == 2) {
@@ -651,7 +760,6 @@ __device__ __noinline__ bool cp_project(const Team tm, float (*seg)[CP_NP], int 
         }
         if (ok) { prog = W - 1; iters = total; }
     } else {
-        const bool unconstrained = !(pa.tau_task_dev < cp_inf());
         // each lane keeps its row in registers across iterations and takes the
         // previous row from lane t-1 by shuffle (no shared-memory round trip);
         // the rows go back to seg when the loop ends
@@ -659,76 +767,14 @@ __device__ __noinline__ bool cp_project(const Team tm, float (*seg)[CP_NP], int 
 #pragma unroll
         for (int k = 0; k < CP_N; k++) xc[k] = row ? seg[t][k] : 0.f;
         bool aborted = false;
-        for (int it = 1; it <= pa.max_iters; it++) {
-            const bool act = row && t > prog;
-            // lane 0 loads the stop word (consumed after stage 1); r1 A/B: all
-            // 16 lanes loading it (volatile: one request each) cost 5 %
-            int sf = 0;
-            if (stop_flag && t == 0) sf = *(const volatile int*)stop_flag;
-            float xn[CP_N], xp[CP_N];
-#pragma unroll
-            for (int k = 0; k < CP_N; k++) xp[k] = __shfl_up_sync(tm.mask, xc[k], 1, CP_G);
-            bool valid = false, full_step = true;
-            if (unconstrained) {
-                // tau_task = inf: validity needs no FK (pure.py:545); the
-                // update is computed only if the segment is not accepted as is.
-                bool cheap = true;
-                if (act) {
-                    float s2 = 0.f;
-                    bool fin = true;
-#pragma unroll
-                    for (int k = 0; k < CP_N; k++) { float d = xc[k] - xp[k]; s2 += d * d; fin &= cp_finite(xc[k]); }
-                    cheap = fin && sqrtf(s2) < tau_sm * 0.99999f;
-                }
-                if (!tm.any(!cheap)) { valid = act; full_step = false; }
-            }
-            if (full_step) {
-                // every lane evaluates (branch-free stage 1, no divergent
-                // region); frozen / idle lanes discard the result
-                const bool v = cp_stage1(pa, xc, xp, tau_sm, xn);
-                valid = act && v;
-                if (act) s1++;   // per lane; summed over the team at the end
-            }
-            unsigned vm = tm.ballot(act && valid) & full;
-            int np = prog;
-            if (pa.mode == 1) {   // literal-gap: largest valid index (pure.py:560-563)
-                unsigned hi = vm & ~((2u << prog) - 1u);
-                if (hi) np = 31 - __clz(hi);
-            } else {              // contiguous prefix (pure.py:564-568)
-                unsigned rest = ~(vm >> (prog + 1));
-                int run = __ffs(rest) - 1;
-                if (run < 0) run = 32;
-                np = min(prog + run, W - 1);
-            }
-            if (np == W - 1) {
-                if (trace) {
-                    if (row) {
-#pragma unroll
-                        for (int k = 0; k < CP_N; k++) trace[((size_t)(it - 1) * W + t) * CP_N + k] = xc[k];
-                    }
-                    if (t == 0) trace_prog[it - 1] = np;
-                }
-                ok = true;
-                iters = it;
-                prog = np;
-                break;
-            }
-            if (stop_flag && tm.bcast(sf, 0)) {   // the query is over: abandon
-                aborted = true;
-                break;
-            }
-            if (row && t > np) {
-#pragma unroll
-                for (int k = 0; k < CP_N; k++) xc[k] = xn[k];
-            }
-            prog = np;
-            if (trace) {
-                if (row) {
-#pragma unroll
-                    for (int k = 0; k < CP_N; k++) trace[((size_t)(it - 1) * W + t) * CP_N + k] = xc[k];
-                }
-                if (t == 0) trace_prog[it - 1] = np;
-            }
+        // one loop per (constrained, traced) case: the constrained planner loop
+        // has no data-dependent branch besides its exits
+        if (!(pa.tau_task_dev < cp_inf())) {
+            if (trace) cp_alg1_loop<true, true>(tm, W, pa, tau_sm, xc, prog, iters, ok, aborted, s1, stop_flag, poll_slot, trace, trace_prog);
+            else cp_alg1_loop<true, false>(tm, W, pa, tau_sm, xc, prog, iters, ok, aborted, s1, stop_flag, poll_slot, nullptr, nullptr);
+        } else {
+            if (trace) cp_alg1_loop<false, true>(tm, W, pa, tau_sm, xc, prog, iters, ok, aborted, s1, stop_flag, poll_slot, trace, trace_prog);
+            else cp_alg1_loop<false, false>(tm, W, pa, tau_sm, xc, prog, iters, ok, aborted, s1, stop_flag, poll_slot, nullptr, nullptr);
         }
         tm.sync();
         if (row) {
@@ -1268,7 +1314,9 @@ __device__ __forceinline__ int* cp_par(const PlanArgs& A, int q, int k) {
     return A.parents + (size_t)(2 * q + k) * A.cap;
 }
 
-struct TeamWS {
+// (host mirror: runtime.cpp ws_bytes = 32 + (G + 7) NP floats, rounded up to 16 B)
+struct alignas(16) TeamWS {
+    int poll[8];           // stop-word poll: two 16 B landing slots (cp_alg1_loop)
     float seg[CP_G][CP_NP];
     float qr[CP_NP], qn[CP_NP], qs[CP_NP], qe[CP_NP], qc[CP_NP], qt[CP_NP], qm[CP_NP];
 };
@@ -1322,7 +1370,7 @@ __device__ __noinline__ bool cp_derive_edge(const Team& tm, TeamWS& ws, const Pl
                                const float* a, const float* b, Stats& st, const int* stop = nullptr) {
     cp_interp(tm, ws.seg, A.W, a, b);
     int it, pr;
-    bool okp = cp_project(tm, ws.seg, A.W, A.pa, &it, &pr, nullptr, nullptr, &st.v[ST_STAGE1], stop);
+    bool okp = cp_project(tm, ws.seg, A.W, A.pa, &it, &pr, nullptr, nullptr, &st.v[ST_STAGE1], stop, ws.poll);
     if (it < 0) return false;   // abandoned: the query is over
     st.v[ST_PROJITER] += it;
     if (!okp) {
@@ -1376,7 +1424,7 @@ __device__ __noinline__ int cp_connect(const Team& tm, TeamWS& ws, const PlanArg
         cp_steer(tm, ws.qc, ws.qt, A.step, ws.qs);
         cp_interp(tm, ws.seg, A.W, ws.qc, ws.qs);
         int it, pr;
-        bool okp = cp_project(tm, ws.seg, A.W, A.pa, &it, &pr, nullptr, nullptr, &st.v[ST_STAGE1], &Q.stop);
+        bool okp = cp_project(tm, ws.seg, A.W, A.pa, &it, &pr, nullptr, nullptr, &st.v[ST_STAGE1], &Q.stop, ws.poll);
         if (it < 0) return -1;   // abandoned: the query is over
         st.v[ST_PROJITER] += it;
         if (!okp) { st.v[ST_PFAIL]++; return -1; }
@@ -1414,7 +1462,7 @@ __device__ __noinline__ int cp_extend_once(const Team& tm, TeamWS& ws, const Pla
     if (cp_vec_equal(tm, ws.qs, ws.qn)) return -1;
     cp_interp(tm, ws.seg, W, ws.qn, ws.qs);
     int pit, ppr;
-    bool okp = cp_project(tm, ws.seg, W, A.pa, &pit, &ppr, nullptr, nullptr, &st.v[ST_STAGE1], &Q.stop);
+    bool okp = cp_project(tm, ws.seg, W, A.pa, &pit, &ppr, nullptr, nullptr, &st.v[ST_STAGE1], &Q.stop, ws.poll);
     if (pit < 0) return -1;   // abandoned: the query is over
     st.v[ST_PROJITER] += pit;
     if (!okp) { st.v[ST_PFAIL]++; return -2; }
@@ -1543,14 +1591,37 @@ __device__ void cp_pair_certifier(const Team& tm, TeamWS& ws, PairBox& bx, const
     }
 }
 
+// Developer profile of the winning team's critical path (CPRRTC_DEFINES=
+// CP_PROFILE, tools/pair_profile.py): warp P's clock64 time by phase, written
+// to the query's result stats by the winner in place of the counters.
+#ifdef CP_PROFILE
+enum { PF_LAUNCH_NS = 0, PF_TOTAL, PF_PROJ, PF_PITER, PF_WAIT, PF_NN, PF_SAMPLE, PF_STOP, PF_NSAMP, PF_NPROJ,
+       PF_WINIT, PF_JUNC };
+#define CP_PF_T0(v) const long long v = clock64()
+#define CP_PF_ADD(i, t0) (pf[i] += (u64)(clock64() - (t0)))
+#define CP_PF_INC(i, n) (pf[i] += (u64)(n))
+#else
+#define CP_PF_T0(v)
+#define CP_PF_ADD(i, t0)
+#define CP_PF_INC(i, n)
+#endif
+
 // warp P: the sampling / projection side of cp_plan_query
 __device__ void cp_plan_query_pair(const Team& tm, TeamWS& ws, TeamWS& wsc, PairBox& bx, const PlanArgs& A,
                                    const SceneSm& sc, int qi) {
     QueryState& Q = A.qs[qi];
     Stats st;
     const int W = A.W;
+#ifdef CP_PROFILE
+    u64 pf[ST_NSTAT] = {};
+    pf[PF_LAUNCH_NS] = cp_clock_ns() - Q.t0_ns;
+    const long long pf_entry = clock64();
+#endif
     for (;;) {
+        CP_PF_T0(t_stop);
         if (cp_should_stop(tm, Q, A)) break;
+        CP_PF_ADD(PF_STOP, t_stop);
+        CP_PF_T0(t_samp);
         int it = 0;
         if (tm.lane == 0) it = atomicAdd(&Q.next_sample, 1) + 1;
         it = tm.bcast(it, 0);
@@ -1563,6 +1634,9 @@ __device__ void cp_plan_query_pair(const Team& tm, TeamWS& ws, TeamWS& wsc, Pair
         const int a = (it - 1) & 1, b = a ^ 1;
         if ((int)tm.lane < CP_N) ws.qr[tm.lane] = (float)cp_halton((i64)it + Q.seed_offset, tm.lane);
         tm.sync();
+        CP_PF_ADD(PF_SAMPLE, t_samp);
+        CP_PF_INC(PF_NSAMP, 1);
+        CP_PF_T0(t_nn);
         // extension P1 (planner.py:265-281)
         const int cnt_a = cp_count(A, Q, a);
         st.v[ST_NNODES] += cnt_a;
@@ -1571,14 +1645,22 @@ __device__ void cp_plan_query_pair(const Team& tm, TeamWS& ws, TeamWS& wsc, Pair
         cp_steer(tm, ws.qn, ws.qr, A.step, ws.qs);
         if (cp_vec_equal(tm, ws.qs, ws.qn)) continue;
         cp_interp(tm, ws.seg, W, ws.qn, ws.qs);
+        CP_PF_ADD(PF_NN, t_nn);
         int pit, ppr;
-        bool okp = cp_project(tm, ws.seg, W, A.pa, &pit, &ppr, nullptr, nullptr, &st.v[ST_STAGE1], &Q.stop);
+        CP_PF_T0(t_p1);
+        bool okp = cp_project(tm, ws.seg, W, A.pa, &pit, &ppr, nullptr, nullptr, &st.v[ST_STAGE1], &Q.stop, ws.poll);
+        CP_PF_ADD(PF_PROJ, t_p1);
+        CP_PF_INC(PF_NPROJ, 1);
+        CP_PF_INC(PF_PITER, pit > 0 ? pit : 0);
         if (pit < 0) break;
         st.v[ST_PROJITER] += pit;
         if (!okp) { st.v[ST_PFAIL]++; continue; }
         cp_copy(tm, ws.qe, ws.seg[W - 1]);
         if (cp_vec_equal(tm, ws.qe, ws.qn)) continue;
+        CP_PF_T0(t_post);
         cp_pair_post(tm, bx, wsc, qi, a, inear, !cp_vec_equal(tm, ws.qe, ws.qs), ws.qn, ws.qe, ws.seg, W);
+        CP_PF_ADD(PF_WAIT, t_post);
+        CP_PF_T0(t_nn2);
         // greedy connect of tree b toward q_new while C certifies the extension
         cp_copy(tm, ws.qt, ws.qe);
         const int cnt_b = cp_count(A, Q, b);
@@ -1586,6 +1668,7 @@ __device__ void cp_plan_query_pair(const Team& tm, TeamWS& ws, TeamWS& wsc, Pair
         int icur = cp_nearest(tm, cp_tree(A, qi, b), A.cap, cnt_b, ws.qt);
         cp_load_node(tm, A, qi, b, icur, ws.qc);
         float dist = cp_vec_dist(tm, ws.qc, ws.qt);
+        CP_PF_ADD(PF_NN, t_nn2);
         int node = -1, meet = -1;
         bool pending_ext = true, stop = false, full = false;
         int prev = -1;          // node of the last accepted connect motion
@@ -1601,12 +1684,19 @@ __device__ void cp_plan_query_pair(const Team& tm, TeamWS& ws, TeamWS& wsc, Pair
                 // already stops the projections (they poll the stop word) and the
                 // budget is checked at every sample (r1 A/B: -2.5 % median)
                 if (segs > 0 && (segs & 3) == 0 && cp_should_stop(tm, Q, A)) { stop = true; break; }
+                CP_PF_T0(t_si);
                 cp_steer(tm, ws.qc, ws.qt, A.step, ws.qs);
                 cp_interp(tm, ws.seg, W, ws.qc, ws.qs);
+                CP_PF_ADD(PF_NN, t_si);
                 int it2, pr2;
+                CP_PF_T0(t_p2);
                 const bool ok1 = cp_project(tm, ws.seg, W, A.pa, &it2, &pr2, nullptr, nullptr, &st.v[ST_STAGE1],
-                                            &Q.stop);
+                                            &Q.stop, ws.poll);
+                CP_PF_ADD(PF_PROJ, t_p2);
+                CP_PF_INC(PF_NPROJ, 1);
+                CP_PF_INC(PF_PITER, it2 > 0 ? it2 : 0);
                 if (it2 >= 0) st.v[ST_PROJITER] += it2;
+                CP_PF_T0(t_w);
                 // the previous motion must be accepted before this one builds on it
                 if (pending_ext) {
                     node = cp_pair_result(tm, bx);
@@ -1618,17 +1708,22 @@ __device__ void cp_plan_query_pair(const Team& tm, TeamWS& ws, TeamWS& wsc, Pair
                     if (prev < 0) { full = prev == -4; break; }
                     icur = prev;
                 }
+                CP_PF_ADD(PF_WAIT, t_w);
                 if (it2 < 0) { stop = true; break; }
                 if (!ok1) { st.v[ST_PFAIL]++; break; }
                 cp_copy(tm, ws.qe, ws.seg[W - 1]);
                 const float nd = cp_vec_dist(tm, ws.qe, ws.qt);
                 if (!(nd < dist)) break;
+                CP_PF_T0(t_w2);
                 cp_pair_post(tm, bx, wsc, qi, b, icur, !cp_vec_equal(tm, ws.qe, ws.qs), ws.qc, ws.qe, ws.seg, W);
                 pending_con = true;
                 cp_copy(tm, ws.qc, ws.qe);
                 dist = nd;
+                CP_PF_ADD(PF_WAIT, t_w2);
                 if (dist <= A.tol) {
+                    CP_PF_T0(t_w3);
                     const int r = cp_pair_result(tm, bx);
+                    CP_PF_ADD(PF_WAIT, t_w3);
                     pending_con = false;
                     if (r >= 0) meet = r;
                     else full = r == -4;
@@ -1647,6 +1742,7 @@ __device__ void cp_plan_query_pair(const Team& tm, TeamWS& ws, TeamWS& wsc, Pair
         }
         if (stop) break;
         if (node < 0 || meet < 0) continue;
+        CP_PF_T0(t_j);
         // junction (planner.py:466-481): q_new (tree a) against the meet node (tree b)
         cp_load_node(tm, A, qi, b, meet, ws.qm);
         const float* js = a == 0 ? ws.qt : ws.qm;
@@ -1657,9 +1753,18 @@ __device__ void cp_plan_query_pair(const Team& tm, TeamWS& ws, TeamWS& wsc, Pair
             cp_copy(tm, ws.qn, jg);
             ok = cp_derive_edge(tm, ws, A, sc, ws.qr, ws.qn, st, &Q.stop);
         }
+        CP_PF_ADD(PF_JUNC, t_j);
         if (ok) {
             int won = 0;
+#ifdef CP_PROFILE
+            pf[PF_TOTAL] = (u64)(clock64() - pf_entry);
+            pf[PF_WINIT] = (u64)it;
+#endif
             if (tm.lane == 0 && atomicCAS(&Q.solved, 0, 1) == 0) {
+#ifdef CP_PROFILE
+#pragma unroll
+                for (int i = 0; i < ST_NSTAT; i++) A.out[qi].stats[i] = pf[i];
+#endif
                 Q.meet[a] = node;
                 Q.meet[b] = meet;
                 Q.t_end_ns = cp_clock_ns();
@@ -1861,8 +1966,10 @@ __device__ __noinline__ void cp_extract_query(const Team tm, const PlanArgs& A, 
     QueryOut& O = A.out[qi];
     const int lane = (int)tm.lane, cap = A.cap;
     const int ns = min(cp_ldvol(&Q.count[0]), cap), ng = min(cp_ldvol(&Q.count[1]), cap);
+#ifndef CP_PROFILE
     if (lane < ST_NSTAT) O.stats[lane] = __ldcg(&Q.stats[lane]);
     if (ST_NSTAT > CP_G && lane + CP_G < ST_NSTAT) O.stats[lane + CP_G] = __ldcg(&Q.stats[lane + CP_G]);
+#endif
     const int solved = cp_ldvol(&Q.solved);
     if (lane == 0) {
         if (!solved) {

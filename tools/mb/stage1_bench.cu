@@ -97,8 +97,9 @@ extern "C" __global__ void halton_bench(int iters, long long seed, long long* cy
 
 // one Alg. 1 projection of a 16-waypoint segment from an on-manifold start
 // toward a point 0.5 rad away (the planner's P1), repeated
-extern "C" __global__ void proj_bench(int reps, long long* cyc, int* iters_out) {
+extern "C" __global__ void proj_bench(int reps, long long* cyc, int* iters_out, const int* stop) {
     __shared__ float seg[CP_G][CP_NP];
+    __shared__ __align__(16) int pslot[8];
     Team tm;
     const float qa[7] = {-0.07434654f, 0.54688579f, 2.74340846f, -2.4217312f, -0.20725576f, 1.89866585f, 2.79144559f};
     const float dq[7] = {0.25f, -0.2f, -0.15f, 0.2f, -0.15f, 0.1f, -0.2f};
@@ -113,7 +114,7 @@ extern "C" __global__ void proj_bench(int reps, long long* cyc, int* iters_out) 
         __syncwarp();
         int it, pr;
         long long t0 = clock64();
-        bool okp = cp_project(tm, seg, 16, pa, &it, &pr);
+        bool okp = cp_project(tm, seg, 16, pa, &it, &pr, nullptr, nullptr, nullptr, stop, stop ? pslot : nullptr);
         long long t1 = clock64();
         if (r == 0 && threadIdx.x == 0) printf("ok %d iters %d prog %d err0 %g\n", (int)okp, it, pr, cp_err_norm(seg[0]));
         total += t1 - t0;
@@ -155,10 +156,17 @@ int main() {
     }
     int* its; int hi;
     cudaMalloc(&its, 4);
-    proj_bench<<<1, 16>>>(20, cyc, its);
-    proj_bench<<<1, 16>>>(20, cyc, its);
-    cudaMemcpy(&h, cyc, 8, cudaMemcpyDeviceToHost);
-    cudaMemcpy(&hi, its, 4, cudaMemcpyDeviceToHost);
-    printf("projection: %d iterations per call, %.0f cycles per iteration\n", hi / 20, (double)h / hi);
+    int* stop;
+    cudaMalloc(&stop, 1 << 20);
+    cudaMemset(stop, 0, 1 << 20);
+    for (int v = 0; v < 3; v++) {
+        const int* sp = v == 0 ? nullptr : stop + (v - 1) * 4096;
+        proj_bench<<<1, 16>>>(20, cyc, its, sp);
+        proj_bench<<<1, 16>>>(20, cyc, its, sp);
+        cudaMemcpy(&h, cyc, 8, cudaMemcpyDeviceToHost);
+        cudaMemcpy(&hi, its, 4, cudaMemcpyDeviceToHost);
+        printf("projection (stop word %s): %d iterations per call, %.0f cycles per iteration\n",
+               v == 0 ? "none" : (v == 1 ? "A" : "B"), hi / 20, (double)h / hi);
+    }
     return 0;
 }
