@@ -1995,6 +1995,10 @@ cp_plan_kernel(const __grid_constant__ PlanArgs A) {
     extern __shared__ float4 cp_smem[];
     SceneSm sc = cp_stage_scene(A.scene_g, cp_smem);
     TeamWS* wsa = reinterpret_cast<TeamWS*>(cp_smem + cp_scene_f4(A.scene_g));
+    // launched as a programmatic dependent of cp_init_kernel: the scene staging
+    // above overlapped it; query state, trees and queue counters are read only
+    // after its writes (a no-op in a plain launch)
+    asm volatile("griddepcontrol.wait;" ::: "memory");
     if (A.pair) {   // pair mailboxes live in shared memory: set them up before any warp uses one
         for (int w = 2 * threadIdx.x; w < (int)(blockDim.x >> 5); w += 2 * blockDim.x) {
             PairBox* b = cp_pair_box(&wsa[w * (32 / CP_G) + 1]);
@@ -2140,6 +2144,9 @@ __device__ int cp_check_config_d(const SetupArgs& S, const double* q, int lane) 
 // query.  The NaN refill of the previous run's node slots already happened at
 // the end of that run (cp_reset_kernel, outside the timed region).
 extern "C" __global__ void __launch_bounds__(32) cp_init_kernel(const __grid_constant__ SetupArgs S) {
+    // the planner may start its prologue (scene staging) now; it waits for
+    // this grid's writes before touching query state (griddepcontrol.wait)
+    asm volatile("griddepcontrol.launch_dependents;");
     const int qi = blockIdx.x, lane = threadIdx.x;
     QueryState& Q = S.qs[qi];
     if (qi == 0 && lane < 16 && S.counters) S.counters[lane] = 0;
@@ -2150,11 +2157,13 @@ extern "C" __global__ void __launch_bounds__(32) cp_init_kernel(const __grid_con
     if (lane == 0) {
         S.parents[(size_t)(2 * qi) * S.cap] = 0;
         S.parents[(size_t)(2 * qi + 1) * S.cap] = 0;
-        Q.setup_code = 0;
+        // stop and setup_code belong to the endpoint checks, which run
+        // concurrently (cp_check_kernel); the previous run's cp_reset_kernel
+        // cleared them
         Q.seed_offset = S.seeds[qi];
         Q.count[0] = 1; Q.count[1] = 1;
         Q.next_sample = 0;
-        Q.solved = 0; Q.stop = 0; Q.timed_out = 0; Q.overflow = 0; Q.exhausted = 0; Q.race_stopped = 0;
+        Q.solved = 0; Q.timed_out = 0; Q.overflow = 0; Q.exhausted = 0; Q.race_stopped = 0;
         Q.active = 0;
         Q.meet[0] = -1; Q.meet[1] = -1;
         Q.t0_ns = cp_clock_ns();
@@ -2187,11 +2196,13 @@ extern "C" __global__ void __launch_bounds__(64) cp_check_kernel(const __grid_co
     }
 }
 
-// Reset the node slots used by the previous run to NaN (publication marker).
+// Reset the node slots used by the previous run to NaN (publication marker),
+// and the stop / setup words for the next run's concurrent endpoint checks.
 extern "C" __global__ void cp_reset_kernel(QueryState* qs, float* trees, int cap, int nq) {
     for (int qk = blockIdx.y; qk < 2 * nq; qk += gridDim.y) {
         const int qi = qk >> 1, k = qk & 1;
         const int h = min(qs[qi].hwm[k], cap);
+        if (k == 0 && blockIdx.x == 0 && threadIdx.x == 0) { qs[qi].stop = 0; qs[qi].setup_code = 0; }
         float* base = trees + (size_t)qk * CP_N * cap;
         const float nan = __int_as_float(0x7fffffff);
         for (int d = 0; d < CP_N; d++)
