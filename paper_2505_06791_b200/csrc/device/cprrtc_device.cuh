@@ -1221,10 +1221,13 @@ __device__ __noinline__ int cp_nearest(const Team tm, const float* nodes, int ca
 // ---------------------------------------------------------------------------
 // Halton sampling, FP64, bit-exact with maniplan/sampling.py:32-81
 // ---------------------------------------------------------------------------
+// the k-th prime (k < 32) from four packed immediates: no table load (a
+// cold constant-bank miss right after an L2 flush costs a DRAM round trip)
 __device__ __forceinline__ int cp_prime(int k) {
-    const int pr[32] = {2, 3, 5, 7, 11, 13, 17, 19, 23, 29, 31, 37, 41, 43, 47, 53,
-                        59, 61, 67, 71, 73, 79, 83, 89, 97, 101, 103, 107, 109, 113, 127, 131};
-    return pr[k];
+    const u64 p0 = 0x13110d0b07050302ull, p1 = 0x352f2b29251f1d17ull;
+    const u64 p2 = 0x59534f4947433d3bull, p3 = 0x837f716d6b676561ull;
+    const u64 w = k < 8 ? p0 : (k < 16 ? p1 : (k < 24 ? p2 : p3));
+    return (int)((w >> (8 * (k & 7))) & 0xffull);
 }
 __device__ __forceinline__ double cp_radical_inverse(i64 index, int base) {
     double f = 0.0;
@@ -1242,18 +1245,29 @@ __device__ __forceinline__ double cp_radical_inverse(i64 index, int base) {
 // division: the scale sequence is the generated table cp_hscale (the
 // reference's own values, bit for bit) and i / b is a 64-bit multiply-high by
 // cp_hmagic (exact for i < 2^32).  k = joint index (base = k-th prime).
+// Base 2 (k = 0): every term and partial sum is a dyadic rational with at
+// most 32 significant bits, so the reference's sum is exactly the bit
+// reversal of the index times 2^-32.
 __device__ __forceinline__ double cp_radical_inverse_k(i64 index, int k) {
     if (index < 0 || index >= (1ll << 32)) return cp_radical_inverse(index, cp_prime(k));
+    if (k == 0) return __dmul_rn((double)__brev((unsigned)index), 0x1p-32);
     const u64 M = cp_hmagic[k], b = (u64)cp_prime(k);
     const double* sc = cp_hscale[k];
     u64 i = (u64)index;
     double f = 0.0;
     for (int d = 0; i > 0; d++) {
         const u64 q = __umul64hi(i << 24, M);
-        f = __dadd_rn(f, __dmul_rn((double)(i - q * b), sc[d]));
+        f = __dadd_rn(f, __dmul_rn((double)(unsigned)(i - q * b), sc[d]));
         i = q;
     }
     return f;
+}
+// pull joint k's Halton tables toward the SM (kernel prologues: after an L2
+// flush their first use would otherwise wait on DRAM inside the sample)
+__device__ __forceinline__ void cp_halton_prefetch(int k) {
+    asm volatile("prefetch.global.L1 [%0];" ::"l"(&cp_hmagic[k]));
+#pragma unroll
+    for (int d = 0; d < 48; d += 16) asm volatile("prefetch.global.L1 [%0];" ::"l"(&cp_hscale[k][d]));
 }
 __device__ __forceinline__ double cp_halton(i64 index, int k) {
     double u = cp_radical_inverse_k(index, k);
@@ -1607,8 +1621,13 @@ enum { PF_LAUNCH_NS = 0, PF_TOTAL, PF_PROJ, PF_PITER, PF_WAIT, PF_NN, PF_SAMPLE,
 #endif
 
 // warp P: the sampling / projection side of cp_plan_query
+//
+// first_it > 0 (single-query launches): the team's first sample index, handed
+// out statically (team k draws k + 1; the shared counter then continues
+// above n_teams), and no stop poll before it -- a team's first extension
+// starts without an L2 round trip.
 __device__ void cp_plan_query_pair(const Team& tm, TeamWS& ws, TeamWS& wsc, PairBox& bx, const PlanArgs& A,
-                                   const SceneSm& sc, int qi) {
+                                   const SceneSm& sc, int qi, int first_it, int n_teams) {
     QueryState& Q = A.qs[qi];
     Stats st;
     const int W = A.W;
@@ -1617,14 +1636,16 @@ __device__ void cp_plan_query_pair(const Team& tm, TeamWS& ws, TeamWS& wsc, Pair
     pf[PF_LAUNCH_NS] = cp_clock_ns() - Q.t0_ns;
     const long long pf_entry = clock64();
 #endif
-    for (;;) {
+    for (int round = 0;; round++) {
         CP_PF_T0(t_stop);
-        if (cp_should_stop(tm, Q, A)) break;
+        if (!(round == 0 && first_it > 0) && cp_should_stop(tm, Q, A)) break;
         CP_PF_ADD(PF_STOP, t_stop);
         CP_PF_T0(t_samp);
-        int it = 0;
-        if (tm.lane == 0) it = atomicAdd(&Q.next_sample, 1) + 1;
-        it = tm.bcast(it, 0);
+        int it = first_it;
+        if (round > 0 || first_it <= 0) {
+            if (tm.lane == 0) it = atomicAdd(&Q.next_sample, 1) + 1 + (first_it > 0 ? n_teams : 0);
+            it = tm.bcast(it, 0);
+        }
         if (it > A.max_iterations) {
             if (tm.lane == 0) atomicExch(&Q.exhausted, 1);
             break;
@@ -1632,7 +1653,9 @@ __device__ void cp_plan_query_pair(const Team& tm, TeamWS& ws, TeamWS& wsc, Pair
         st.v[ST_ITER]++;
         st.v[ST_ATT]++;
         const int a = (it - 1) & 1, b = a ^ 1;
-        if ((int)tm.lane < CP_N) ws.qr[tm.lane] = (float)cp_halton((i64)it + Q.seed_offset, tm.lane);
+        // (round 0 of a single query: drawn in the kernel prologue)
+        if ((round > 0 || first_it <= 0) && (int)tm.lane < CP_N)
+            ws.qr[tm.lane] = (float)cp_halton((i64)it + Q.seed_offset, tm.lane);
         tm.sync();
         CP_PF_ADD(PF_SAMPLE, t_samp);
         CP_PF_INC(PF_NSAMP, 1);
@@ -1786,15 +1809,19 @@ __device__ void cp_plan_query_pair(const Team& tm, TeamWS& ws, TeamWS& wsc, Pair
 }
 
 // One team works on query qi until it is solved / stopped / out of samples.
-__device__ void cp_plan_query(const Team& tm, TeamWS& ws, const PlanArgs& A, const SceneSm& sc, int qi) {
+// first_it / n_teams: as for cp_plan_query_pair.
+__device__ void cp_plan_query(const Team& tm, TeamWS& ws, const PlanArgs& A, const SceneSm& sc, int qi,
+                              int first_it, int n_teams) {
     QueryState& Q = A.qs[qi];
     Stats st;
     const int W = A.W;
-    for (;;) {
-        if (cp_should_stop(tm, Q, A)) break;
-        int it = 0;
-        if (tm.lane == 0) it = atomicAdd(&Q.next_sample, 1) + 1;
-        it = tm.bcast(it, 0);
+    for (int round = 0;; round++) {
+        if (!(round == 0 && first_it > 0) && cp_should_stop(tm, Q, A)) break;
+        int it = first_it;
+        if (round > 0 || first_it <= 0) {
+            if (tm.lane == 0) it = atomicAdd(&Q.next_sample, 1) + 1 + (first_it > 0 ? n_teams : 0);
+            it = tm.bcast(it, 0);
+        }
         if (it > A.max_iterations) {
             // out of samples: no new extensions, but extensions already in
             // flight (other teams) finish their connect
@@ -1805,7 +1832,9 @@ __device__ void cp_plan_query(const Team& tm, TeamWS& ws, const PlanArgs& A, con
         st.v[ST_ATT]++;
         const int a = (it - 1) & 1, b = a ^ 1;   // start tree extends on odd iterations
         // sample (sampling.py:65-81) -- FP64 Halton, bit-exact with the reference
-        if ((int)tm.lane < CP_N) ws.qr[tm.lane] = (float)cp_halton((i64)it + Q.seed_offset, tm.lane);
+        // (round 0 of a single query: drawn in the kernel prologue)
+        if ((round > 0 || first_it <= 0) && (int)tm.lane < CP_N)
+            ws.qr[tm.lane] = (float)cp_halton((i64)it + Q.seed_offset, tm.lane);
         tm.sync();
         // _attempt_extend (planner.py:265-306) + commit
         const int node = cp_extend_once(tm, ws, A, sc, Q, qi, a, st);
@@ -1993,11 +2022,30 @@ __device__ __noinline__ void cp_extract_query(const Team tm, const PlanArgs& A, 
 extern "C" __global__ void __launch_bounds__(CP_NTHREADS, 1)
 cp_plan_kernel(const __grid_constant__ PlanArgs A) {
     extern __shared__ float4 cp_smem[];
+    if (A.nq == 1 && (int)(threadIdx.x & 31) < CP_N) cp_halton_prefetch((int)(threadIdx.x & 31));
     SceneSm sc = cp_stage_scene(A.scene_g, cp_smem);
     TeamWS* wsa = reinterpret_cast<TeamWS*>(cp_smem + cp_scene_f4(A.scene_g));
+    const int team_in_cta = (threadIdx.x >> 5) * (32 / CP_G) + (threadIdx.x & 31) / CP_G;
+    // a single query: every team starts on it at once with a static first
+    // sample -- team k draws sample k + 1, computed here, before the wait
+    // below (the seeds were copied before init ran) -- with no queue / steal
+    // round trips, and leaves the kernel after it
+#ifdef CP_NO_FASTSTART
+    const bool single = false;
+#else
+    const bool single = A.nq == 1;
+#endif
+    const int teams_per_cta = A.pair ? (int)(blockDim.x >> 6) : (A.solo ? (int)(blockDim.x >> 5) : (int)blockDim.x / CP_G);
+    const int n_teams = (int)gridDim.x * teams_per_cta;
+    const int gteam = (int)blockIdx.x * teams_per_cta + (A.pair ? (int)(threadIdx.x >> 6) : team_in_cta / (A.solo ? 32 / CP_G : 1));
+    const bool sampler = !(A.solo && (int)(threadIdx.x & 31) >= CP_G) && !(A.pair && ((threadIdx.x >> 5) & 1));
+    if (single && sampler && (int)(threadIdx.x % CP_G) < CP_N && gteam < A.max_iterations) {
+        const int k = (int)(threadIdx.x % CP_G);
+        wsa[team_in_cta].qr[k] = (float)cp_halton((i64)(gteam + 1) + A.seeds[0], k);
+    }
     // launched as a programmatic dependent of cp_init_kernel: the scene staging
-    // above overlapped it; query state, trees and queue counters are read only
-    // after its writes (a no-op in a plain launch)
+    // and first samples above overlapped it; query state, trees and queue
+    // counters are read only after its writes (a no-op in a plain launch)
     asm volatile("griddepcontrol.wait;" ::: "memory");
     if (A.pair) {   // pair mailboxes live in shared memory: set them up before any warp uses one
         for (int w = 2 * threadIdx.x; w < (int)(blockDim.x >> 5); w += 2 * blockDim.x) {
@@ -2012,7 +2060,6 @@ cp_plan_kernel(const __grid_constant__ PlanArgs A) {
     // latency mode: one team per warp, so divergent teams never share a warp
     if (A.solo && (int)(threadIdx.x & 31) >= CP_G) return;
     Team tm;
-    const int team_in_cta = (threadIdx.x >> 5) * (32 / CP_G) + (threadIdx.x & 31) / CP_G;
     TeamWS& ws = wsa[team_in_cta];
     // pair mode (solo, CP_G = 16): odd warps certify for the even warp before
     // them; the pair's mailbox is the unused half-team slot of the even warp
@@ -2029,6 +2076,10 @@ cp_plan_kernel(const __grid_constant__ PlanArgs A) {
     for (;;) {
         int qi = -1;
         int h = 0;
+        if (single) {
+            if (visits > 0) break;
+            qi = 0;
+        } else {
         if (tm.lane == 0) h = atomicAdd(A.queue_head, 1);
         h = tm.bcast(h, 0);
         if (h < A.nq) {
@@ -2054,11 +2105,13 @@ cp_plan_kernel(const __grid_constant__ PlanArgs A) {
                 if (mk) qi = (s0 + base + __ffs(mk) - 1) % A.nq;
             }
         }
+        }
         if (qi < 0 || ++visits > 4 * A.nq + 4) break;
         QueryState& Q = A.qs[qi];
         if (tm.lane == 0) atomicAdd(&Q.active, 1);
-        if (bx) cp_plan_query_pair(tm, ws, wsa[((threadIdx.x >> 5) + 1) * (32 / CP_G)], *bx, A, sc, qi);
-        else cp_plan_query(tm, ws, A, sc, qi);
+        const int first = single ? gteam + 1 : 0;
+        if (bx) cp_plan_query_pair(tm, ws, wsa[((threadIdx.x >> 5) + 1) * (32 / CP_G)], *bx, A, sc, qi, first, n_teams);
+        else cp_plan_query(tm, ws, A, sc, qi, first, n_teams);
         // the last team to leave the query extracts its result (a late
         // joiner may extract again: identical values)
         int last = 0;

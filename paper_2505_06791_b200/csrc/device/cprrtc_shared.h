@@ -101,6 +101,7 @@ struct PlanArgs {
     int* chain;            // (nq, path_cap) device scratch: path position -> node
     int path_cap;
     int pair;              // 1: two-warp teams (single queries; warp P projects, warp C certifies)
+    const i64* seeds;      // (nq) Halton offsets (= QueryState.seed_offset; read before init completes)
 };
 
 struct SetupArgs {

@@ -1331,6 +1331,7 @@ static int plan_launch(Ctx* c, const cprrtc_params* prm, int B, const double* st
     A.sources = c->h_src.dev<int>();
     A.chain = c->chain.as<int>();
     A.path_cap = path_cap;
+    A.seeds = S.seeds;
     S.out = A.out;
     if (race) {
         A.race_flag = race->own;
