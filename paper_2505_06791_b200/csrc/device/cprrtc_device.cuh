@@ -1218,6 +1218,73 @@ __device__ __noinline__ int cp_nearest(const Team tm, const float* nodes, int ca
     return bi == CP_INTMAX ? 0 : bi;
 }
 
+// The planner's nearest neighbour in one L2 round trip instead of three: the
+// first chunk (nodes 4 lane .. 4 lane + 3) is loaded together with the tree's
+// node counter -- slots past the end are NaN (never written, or refilled by
+// the previous run's cp_reset_kernel) and drop out, and nodes appended after
+// the counter was read are legitimate tree nodes -- and each lane keeps the
+// coordinates of its best node, so the winner's configuration comes from a
+// shuffle instead of a reload.  Writes it to out (lanes < CP_N), the node
+// count to *count_out; same argmin and ties as cp_nearest.
+__device__ __noinline__ int cp_nearest_ld(const Team tm, const float* nodes, int cap, const int* cnt,
+                                          const float* q, float* out, int* count_out) {
+    float qq[CP_N];
+#pragma unroll
+    for (int k = 0; k < CP_N; k++) qq[k] = q[k];
+    const int lane = (int)tm.lane;
+    float4 v[CP_N];
+#pragma unroll
+    for (int k = 0; k < CP_N; k++) v[k] = cp_ldcg4(nodes + (size_t)k * cap + 4 * lane);   // 4 CP_G <= 128 <= cap
+    int count = lane == 0 ? cp_ldvol(cnt) : 0;
+    count = min(tm.bcast(count, 0), cap);
+    float best = cp_inf(), bc[CP_N];
+    int bi = CP_INTMAX;
+    auto take = [&](const float4* w, int i0) {
+        float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+        for (int k = 0; k < CP_N; k++) {
+            float a = w[k].x - qq[k], b = w[k].y - qq[k], cc = w[k].z - qq[k], d = w[k].w - qq[k];
+            acc.x = fmaf(a, a, acc.x); acc.y = fmaf(b, b, acc.y);
+            acc.z = fmaf(cc, cc, acc.z); acc.w = fmaf(d, d, acc.w);
+        }
+        const bool tx = acc.x < best;
+        best = tx ? acc.x : best; bi = tx ? i0 : bi;
+        const bool ty = acc.y < best;
+        best = ty ? acc.y : best; bi = ty ? i0 + 1 : bi;
+        const bool tz = acc.z < best;
+        best = tz ? acc.z : best; bi = tz ? i0 + 2 : bi;
+        const bool tw = acc.w < best;
+        best = tw ? acc.w : best; bi = tw ? i0 + 3 : bi;
+#pragma unroll
+        for (int k = 0; k < CP_N; k++)
+            bc[k] = tw ? w[k].w : (tz ? w[k].z : (ty ? w[k].y : (tx ? w[k].x : bc[k])));
+    };
+#pragma unroll
+    for (int k = 0; k < CP_N; k++) bc[k] = 0.f;
+    take(v, 4 * lane);
+    const int n4 = (count + 3) >> 2;
+    for (int i4 = lane + CP_G; i4 < n4; i4 += CP_G) {
+#pragma unroll
+        for (int k = 0; k < CP_N; k++) v[k] = cp_ldcg4(nodes + (size_t)k * cap + 4 * i4);
+        take(v, 4 * i4);
+    }
+    const int my_bi = bi;
+    tm.argmin(best, bi);
+    const unsigned own = tm.ballot(my_bi == bi && bi != CP_INTMAX);
+    const int src = own ? __ffs(own) - 1 : 0;
+    float x = 0.f;
+#pragma unroll
+    for (int k = 0; k < CP_N; k++) {
+        const float c = __shfl_sync(tm.mask, bc[k], src, CP_G);
+        x = lane == k ? c : x;
+    }
+    tm.sync();   // every lane's reads of the previous contents of out are done
+    if (lane < CP_N) out[lane] = x;
+    tm.sync();
+    *count_out = count;
+    return bi == CP_INTMAX ? 0 : bi;
+}
+
 // ---------------------------------------------------------------------------
 // Halton sampling, FP64, bit-exact with maniplan/sampling.py:32-81
 // ---------------------------------------------------------------------------
@@ -1425,10 +1492,9 @@ __device__ __forceinline__ void cp_load_node(const Team& tm, const PlanArgs& A, 
 __device__ __noinline__ int cp_connect(const Team& tm, TeamWS& ws, const PlanArgs& A, const SceneSm& sc,
                           QueryState& Q, int qi, int k, Stats& st, int* segments_out = nullptr) {
     int segs_added = 0;
-    const int cnt = cp_count(A, Q, k);
+    int cnt;
+    int icur = cp_nearest_ld(tm, cp_tree(A, qi, k), A.cap, &Q.count[k], ws.qt, ws.qc, &cnt);
     st.v[ST_NNODES] += cnt;
-    int icur = cp_nearest(tm, cp_tree(A, qi, k), A.cap, cnt, ws.qt);
-    cp_load_node(tm, A, qi, k, icur, ws.qc);
     float dist = cp_vec_dist(tm, ws.qc, ws.qt);
     if (segments_out) *segments_out = 0;
     if (dist <= A.tol) return icur;
@@ -1468,10 +1534,9 @@ __device__ __noinline__ int cp_connect(const Team& tm, TeamWS& ws, const PlanArg
 __device__ __noinline__ int cp_extend_once(const Team& tm, TeamWS& ws, const PlanArgs& A, const SceneSm& sc,
                                            QueryState& Q, int qi, int a, Stats& st) {
     const int W = A.W;
-    const int cnt_a = cp_count(A, Q, a);
+    int cnt_a;
+    const int inear = cp_nearest_ld(tm, cp_tree(A, qi, a), A.cap, &Q.count[a], ws.qr, ws.qn, &cnt_a);
     st.v[ST_NNODES] += cnt_a;
-    const int inear = cp_nearest(tm, cp_tree(A, qi, a), A.cap, cnt_a, ws.qr);
-    cp_load_node(tm, A, qi, a, inear, ws.qn);
     cp_steer(tm, ws.qn, ws.qr, A.step, ws.qs);
     if (cp_vec_equal(tm, ws.qs, ws.qn)) return -1;
     cp_interp(tm, ws.seg, W, ws.qn, ws.qs);
@@ -1661,10 +1726,9 @@ __device__ void cp_plan_query_pair(const Team& tm, TeamWS& ws, TeamWS& wsc, Pair
         CP_PF_INC(PF_NSAMP, 1);
         CP_PF_T0(t_nn);
         // extension P1 (planner.py:265-281)
-        const int cnt_a = cp_count(A, Q, a);
+        int cnt_a;
+        const int inear = cp_nearest_ld(tm, cp_tree(A, qi, a), A.cap, &Q.count[a], ws.qr, ws.qn, &cnt_a);
         st.v[ST_NNODES] += cnt_a;
-        const int inear = cp_nearest(tm, cp_tree(A, qi, a), A.cap, cnt_a, ws.qr);
-        cp_load_node(tm, A, qi, a, inear, ws.qn);
         cp_steer(tm, ws.qn, ws.qr, A.step, ws.qs);
         if (cp_vec_equal(tm, ws.qs, ws.qn)) continue;
         cp_interp(tm, ws.seg, W, ws.qn, ws.qs);
@@ -1686,10 +1750,9 @@ __device__ void cp_plan_query_pair(const Team& tm, TeamWS& ws, TeamWS& wsc, Pair
         CP_PF_T0(t_nn2);
         // greedy connect of tree b toward q_new while C certifies the extension
         cp_copy(tm, ws.qt, ws.qe);
-        const int cnt_b = cp_count(A, Q, b);
+        int cnt_b;
+        int icur = cp_nearest_ld(tm, cp_tree(A, qi, b), A.cap, &Q.count[b], ws.qt, ws.qc, &cnt_b);
         st.v[ST_NNODES] += cnt_b;
-        int icur = cp_nearest(tm, cp_tree(A, qi, b), A.cap, cnt_b, ws.qt);
-        cp_load_node(tm, A, qi, b, icur, ws.qc);
         float dist = cp_vec_dist(tm, ws.qc, ws.qt);
         CP_PF_ADD(PF_NN, t_nn2);
         int node = -1, meet = -1;
