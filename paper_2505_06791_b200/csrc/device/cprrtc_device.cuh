@@ -1448,17 +1448,23 @@ __device__ __forceinline__ bool cp_check_motion(const Team& tm, TeamWS& ws, cons
 
 // derive_edge (planner.py:223-245): the motion a->b re-derivable from its endpoints
 __device__ __noinline__ bool cp_derive_edge(const Team& tm, TeamWS& ws, const PlanArgs& A, const SceneSm& sc,
-                               const float* a, const float* b, Stats& st, const int* stop = nullptr) {
+                               const float* a, const float* b, Stats& st, const int* stop = nullptr,
+                               unsigned long long* prof = nullptr) {
+    const long long t0 = prof ? clock64() : 0;
     cp_interp(tm, ws.seg, A.W, a, b);
     int it, pr;
     bool okp = cp_project(tm, ws.seg, A.W, A.pa, &it, &pr, nullptr, nullptr, &st.v[ST_STAGE1], stop, ws.poll);
+    const long long t1 = prof ? clock64() : 0;
+    if (prof) { prof[0] += (unsigned long long)(t1 - t0); prof[5] += it > 0 ? it : 0; }
     if (it < 0) return false;   // abandoned: the query is over
     st.v[ST_PROJITER] += it;
     if (!okp) {
         st.v[ST_PFAIL]++;
         return false;
     }
-    return cp_check_motion(tm, ws, A, sc, st);
+    const bool ok = cp_check_motion(tm, ws, A, sc, st);
+    if (prof) prof[1] += (unsigned long long)(clock64() - t1);
+    return ok;
 }
 
 // append q to tree k of query qi with parent par; returns index or -1 (full)
@@ -1578,6 +1584,9 @@ struct PairBox {
     int qi, tree, parent, derive, exit;
     int p_ndone, p_pend;             // P's bookkeeping: done phases consumed, a result outstanding
     float from[CP_NP], to[CP_NP];
+#ifdef CP_PROFILE
+    unsigned long long cprof[6];     // warp C clock64 phases: P2, CC, append, jobs, idle, P2 iterations
+#endif
 };
 __device__ __forceinline__ PairBox* cp_pair_box(TeamWS* slot) {
     return reinterpret_cast<PairBox*>((reinterpret_cast<unsigned long long>(slot) + 7ull) & ~7ull);
@@ -1634,9 +1643,22 @@ __device__ __forceinline__ int cp_pair_result(const Team& tm, PairBox& bx) {
 
 // warp C: certify jobs until P posts the exit job
 __device__ void cp_pair_certifier(const Team& tm, TeamWS& ws, PairBox& bx, const PlanArgs& A, const SceneSm& sc) {
+#ifdef CP_PROFILE
+    unsigned long long cpf[6] = {};
+#define CP_CPROF cpf
+#else
+#define CP_CPROF nullptr
+#endif
     for (int nfull = 0;; nfull++) {
+#ifdef CP_PROFILE
+        const long long t_idle = clock64();
+#endif
         cp_mb_wait(&bx.full, nfull & 1);
         tm.sync();
+#ifdef CP_PROFILE
+        cpf[4] += (unsigned long long)(clock64() - t_idle);
+        cpf[3]++;
+#endif
         if (bx.exit) break;
         const int qi = bx.qi, tree = bx.tree;
         QueryState& Q = A.qs[qi];
@@ -1647,18 +1669,34 @@ __device__ void cp_pair_certifier(const Team& tm, TeamWS& ws, PairBox& bx, const
             if ((int)tm.lane < CP_N) { ws.qr[tm.lane] = bx.from[tm.lane]; ws.qn[tm.lane] = bx.to[tm.lane]; }
             tm.sync();
             const unsigned long long pf0 = st.v[ST_PFAIL];
-            ok = cp_derive_edge(tm, ws, A, sc, ws.qr, ws.qn, st, &Q.stop);
+            ok = cp_derive_edge(tm, ws, A, sc, ws.qr, ws.qn, st, &Q.stop, CP_CPROF);
             res = ok ? 0 : (st.v[ST_PFAIL] != pf0 ? -2 : -3);
         } else {
+#ifdef CP_PROFILE
+            const long long t_cc = clock64();
+#endif
             ok = cp_check_motion(tm, ws, A, sc, st);
+#ifdef CP_PROFILE
+            cpf[1] += (unsigned long long)(clock64() - t_cc);
+#endif
             res = ok ? 0 : -3;
         }
         if (ok) {
+#ifdef CP_PROFILE
+            const long long t_ap = clock64();
+#endif
             if ((int)tm.lane < CP_N) ws.qe[tm.lane] = bx.to[tm.lane];
             tm.sync();
             const int node = cp_append(tm, A, Q, qi, tree, ws.qe, bx.parent);
             res = node < 0 ? -4 : node;
+#ifdef CP_PROFILE
+            cpf[2] += (unsigned long long)(clock64() - t_ap);
+#endif
         }
+#ifdef CP_PROFILE
+        if (tm.lane == 0)
+            for (int i = 0; i < 6; i++) bx.cprof[i] = cpf[i];
+#endif
         if (tm.lane == 0) {
 #pragma unroll
             for (int i = 0; i < ST_NSTAT; i++)
@@ -1848,6 +1886,11 @@ __device__ void cp_plan_query_pair(const Team& tm, TeamWS& ws, TeamWS& wsc, Pair
 #endif
             if (tm.lane == 0 && atomicCAS(&Q.solved, 0, 1) == 0) {
 #ifdef CP_PROFILE
+#if CP_PROFILE == 2
+                // warp C's phases (as of its last finished job) in place of P's NN / sample / stop slots
+                pf[5] = bx.cprof[0]; pf[6] = bx.cprof[1]; pf[8] = bx.cprof[2]; pf[9] = bx.cprof[3];
+                pf[10] = bx.cprof[4]; pf[11] = bx.cprof[5];
+#endif
 #pragma unroll
                 for (int i = 0; i < ST_NSTAT; i++) A.out[qi].stats[i] = pf[i];
 #endif

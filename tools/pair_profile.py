@@ -3,7 +3,8 @@ team's warp P spends its time (CPRRTC_DEFINES=CP_PROFILE build; the winner
 writes clock64 phase totals into the result stats).  Prints medians over the
 bench workload's solved queries."""
 import os, sys
-os.environ["CPRRTC_DEFINES"] = ",".join(x for x in [os.environ.get("CPRRTC_DEFINES", ""), "CP_PROFILE"] if x)
+MODE = int(os.environ.get("PP_MODE", "1"))   # 1: warp P's phases; 2: warp C's phases (P2, CC, append, idle)
+os.environ["CPRRTC_DEFINES"] = ",".join(x for x in [os.environ.get("CPRRTC_DEFINES", ""), f"CP_PROFILE={MODE}"] if x)
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path[:0] = [ROOT, os.path.join(ROOT, "tests")]
 import numpy as np
@@ -26,6 +27,17 @@ for step in range(4):
                          s.collision_rejections, s.cc_performed, s.cc_possible, s.stage1_evals,
                          s.cc_fk_evals, s.nn_nodes, s.proj_iters, r.stats.device_ms * 1e3])
 a = np.array(rows, dtype=np.float64)
+clk = 1.965e3   # cycles per us (approximate; fractions below are clock-free)
+if MODE == 2:
+    launch_ns, total, proj, piter, wait, c_p2, c_cc, c_app, c_jobs, c_idle, c_it, dev_us = a.T
+    print(f"{len(a)} solved queries; median device {np.median(dev_us):.1f} us; team start->win {np.median(total) / clk:.1f} us")
+    print(f"warp P: projection {np.median(proj / total) * 100:.1f} %, waiting for C {np.median(wait / total) * 100:.1f} %")
+    for name, v in [("P2 re-projection", c_p2), ("collision check", c_cc), ("append", c_app), ("idle (no job)", c_idle)]:
+        print(f"warp C: {name:18s} median {np.median(v / total) * 100:5.1f} % of P's team time, {np.median(v) / clk:6.1f} us")
+    print(f"warp C jobs (incl. exit) {np.median(c_jobs):.0f}; P2 iterations {np.median(c_it):.0f}; "
+          f"P2 cycles/iteration {np.median(c_p2 / np.maximum(c_it, 1)):.0f}; "
+          f"CC cycles/job {np.median(c_cc / np.maximum(c_jobs - 1, 1)):.0f}; append cycles/job {np.median(c_app / np.maximum(c_jobs - 1, 1)):.0f}")
+    sys.exit(0)
 launch_ns, total, proj, piter, wait, nn, samp, nsamp, nproj, winit, junc, dev_us = a.T
 clk = 1.965e3   # cycles per us (approximate; fractions below are clock-free)
 print(f"{len(a)} solved queries; median device {np.median(dev_us):.1f} us")
