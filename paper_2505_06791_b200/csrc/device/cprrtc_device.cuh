@@ -605,7 +605,11 @@ __device__ __forceinline__ void cp_alg1_loop(const Team tm, int W, const ProjArg
     const unsigned long long sbase = (unsigned long long)stop_flag & ~15ull;
     const unsigned slot = pslot ? (unsigned)__cvta_generic_to_shared(pslot) : 0u;   // 2 x 16 B slots
     const unsigned soff = (unsigned)((unsigned long long)stop_flag - sbase);
-    // prologue poll into slot 0 (read by iteration 1)
+    // the previous projection's last poll has landed (long ago, normally: the
+    // wait sits here rather than at that projection's exit, where it would
+    // cost an L2 round trip per projection), then the prologue poll into
+    // slot 0 (read by iteration 1)
+    asm volatile("cp.async.wait_all;" ::: "memory");
     asm volatile("{ .reg .pred p; setp.ne.u32 p, %2, 0; @p cp.async.cg.shared.global [%0], [%1], 16; "
                  "cp.async.commit_group; }" ::"r"(slot), "l"(sbase), "r"((unsigned)poll));
     const float tsm = tau_sm * 0.99999f;
@@ -676,8 +680,6 @@ __device__ __forceinline__ void cp_alg1_loop(const Team tm, int W, const ProjArg
             if (t == 0) trace_prog[it - 1] = np;
         }
     }
-    // the last poll lands before the slots are reused
-    asm volatile("cp.async.wait_all;" ::: "memory");
 }
 
 // Project the team's segment in place: Alg. 1 (pure.py:549-577) for modes
@@ -2175,6 +2177,7 @@ cp_plan_kernel(const __grid_constant__ PlanArgs A) {
         bx = cp_pair_box(&wsa[(w & ~1) * (32 / CP_G) + 1]);
         if (w & 1) {
             cp_pair_certifier(tm, ws, *bx, A, sc);
+            asm volatile("cp.async.wait_all;" ::: "memory");   // the last stop-word poll has landed
             return;
         }
     }
@@ -2232,6 +2235,7 @@ cp_plan_kernel(const __grid_constant__ PlanArgs A) {
     }
     if (bx)   // release the certifier warp
         cp_pair_post(tm, *bx, ws, 0, 0, 0, true, ws.qr, ws.qr, ws.seg, 0, 1);
+    asm volatile("cp.async.wait_all;" ::: "memory");   // the last stop-word poll has landed
 }
 
 #endif  // !CP_PARITY
@@ -2654,5 +2658,6 @@ cp_step_kernel(const __grid_constant__ PlanArgs A, int op, int k, const float* q
         out[2] = min(Q.count[k], A.cap);
         for (int i = 0; i < ST_NSTAT; i++) stats[i] = st.v[i];
     }
+    asm volatile("cp.async.wait_all;" ::: "memory");   // the last stop-word poll has landed
 }
 #endif  // !CP_PARITY
