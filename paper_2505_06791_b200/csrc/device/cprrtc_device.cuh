@@ -711,7 +711,10 @@ __device__ __noinline__ bool cp_project(const Team tm, float (*seg)[CP_NP], int 
             for (int k = 0; k < CP_N; k++) { float d = seg[t][k] - seg[t - 1][k]; s2 += d * d; }
             g = sqrtf(s2);
         }
-        g = tm.maxf(g);
+        // max over the team in one REDUX: non-negative floats order as their
+        // bit patterns; NaN drops out as in fmaxf (an all-NaN team gives 0,
+        // and so the same 1e-6 as NaN would below)
+        g = __uint_as_float(__reduce_max_sync(tm.mask, g == g ? __float_as_uint(g) : 0u));
         tau_sm = g > 0.f ? 1.5f * g : 1e-6f;
     }
     int prog = 0, iters = pa.max_iters;

@@ -97,7 +97,7 @@ extern "C" __global__ void halton_bench(int iters, long long seed, long long* cy
 
 // one Alg. 1 projection of a 16-waypoint segment from an on-manifold start
 // toward a point 0.5 rad away (the planner's P1), repeated
-extern "C" __global__ void proj_bench(int reps, long long* cyc, int* iters_out, const int* stop) {
+extern "C" __global__ void proj_bench(int reps, long long* cyc, int* iters_out, const int* stop, float span = 1.f) {
     __shared__ float seg[CP_G][CP_NP];
     __shared__ __align__(16) int pslot[8];
     Team tm;
@@ -110,7 +110,7 @@ extern "C" __global__ void proj_bench(int reps, long long* cyc, int* iters_out, 
     int its = 0;
     for (int r = 0; r < reps; r++) {
         const int t = tm.lane;
-        for (int k = 0; k < CP_N; k++) seg[t][k] = qa[k] + (float)t / 15.f * dq[k];
+        for (int k = 0; k < CP_N; k++) seg[t][k] = qa[k] + span * (float)t / 15.f * dq[k];
         __syncwarp();
         int it, pr;
         long long t0 = clock64();
@@ -167,6 +167,16 @@ int main() {
         cudaMemcpy(&hi, its, 4, cudaMemcpyDeviceToHost);
         printf("projection (stop word %s): %d iterations per call, %.0f cycles per iteration\n",
                v == 0 ? "none" : (v == 1 ? "A" : "B"), hi / 20, (double)h / hi);
+    }
+    // short motions (the certifier's re-projections converge in a few
+    // iterations): the per-call fixed cost shows
+    for (float span : {0.05f, 0.01f}) {
+        proj_bench<<<1, 16>>>(20, cyc, its, stop, span);
+        proj_bench<<<1, 16>>>(20, cyc, its, stop, span);
+        cudaMemcpy(&h, cyc, 8, cudaMemcpyDeviceToHost);
+        cudaMemcpy(&hi, its, 4, cudaMemcpyDeviceToHost);
+        printf("short projection (span %.2f): %d iterations per call, %.0f cycles per call\n", span, hi / 20,
+               (double)h / 20);
     }
     return 0;
 }
