@@ -218,6 +218,43 @@ def test_upright_suite_matches_reference_success(oracle):
         _check_path(oracle, probs[k], res[k])
 
 
+_FALLBACK_CODE = r"""
+import sys, numpy as np
+sys.path[:0] = ['.', 'tests']
+import fixtures as fx
+from oracle import oracle
+from test_gpu_planner import _check_path
+from paper_2505_06791_b200.planner import PlanParams, PlanProblem, plan
+m, sc, sp = fx.robot('arm7'), fx.scene('table'), fx.spec('upright')
+prs = fx.pairs()
+feas = np.nonzero(fx.upright_feasible())[0][:6]
+for k in feas:
+    prob = PlanProblem(m, sc, sp, prs['upright_start'][k], prs['upright_goal'][k],
+                       PlanParams(width=16, max_iterations=10**6, seed_offset=int(k)))
+    r = plan(prob)
+    assert r.solved, r.status
+    _check_path(oracle, prob, r)
+print('ok')
+"""
+
+
+def _run_fallback(**env_over):
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = dict(os.environ, **env_over)
+    out = subprocess.run([sys.executable, "-c", _FALLBACK_CODE], cwd=root, env=env, capture_output=True,
+                         text=True, timeout=600)
+    assert out.returncode == 0 and "ok" in out.stdout, out.stderr[-2000:]
+
+
+def test_plain_launch_fallback():
+    """CPRRTC_PDL=0 (the planner as a plain launch bracketed by timing events,
+    not a programmatic dependent of init) plans the same queries soundly."""
+    _run_fallback(CPRRTC_PDL="0")
+
+
 def test_one_warp_teams_fallback():
     """CPRRTC_PAIR=0 (one-warp teams, the batch code path) still plans single
     queries soundly; run in a subprocess because the switch is read once."""
