@@ -586,7 +586,11 @@ __device__ __noinline__ float cp_err_norm(const float* q) {
 // per iteration: no register scoreboard); after stage 1 the loop reads the
 // copy issued one iteration earlier, behind cp.async.wait_group 1 -- which
 // never waits in practice (an iteration, ~1200 cycles, covers the L2 round
-// trip), wherever ptxas places it.  A stop is seen one iteration late.  r1
+// trip), wherever ptxas places it.  A stop is seen one iteration late, and
+// not in a projection's first iteration: the slots alternate across
+// projections (the parity persists in the workspace), so a projection starts
+// with neither a prologue poll nor a wait for the previous one's last poll
+// (r1: ~1 L2 round trip per call, which short re-projections felt).  r1
 // (B200): a plain load cost ~300 cycles per iteration of ~1500 (ptxas turned
 // its value into a predicate right after issue, stalling on the round trip),
 // and a same-iteration cp.async.wait_all was hoisted the same way.
@@ -605,17 +609,12 @@ __device__ __forceinline__ void cp_alg1_loop(const Team tm, int W, const ProjArg
     const unsigned long long sbase = (unsigned long long)stop_flag & ~15ull;
     const unsigned slot = pslot ? (unsigned)__cvta_generic_to_shared(pslot) : 0u;   // 2 x 16 B slots
     const unsigned soff = (unsigned)((unsigned long long)stop_flag - sbase);
-    // the previous projection's last poll has landed (long ago, normally: the
-    // wait sits here rather than at that projection's exit, where it would
-    // cost an L2 round trip per projection), then the prologue poll into
-    // slot 0 (read by iteration 1)
-    asm volatile("cp.async.wait_all;" ::: "memory");
-    asm volatile("{ .reg .pred p; setp.ne.u32 p, %2, 0; @p cp.async.cg.shared.global [%0], [%1], 16; "
-                 "cp.async.commit_group; }" ::"r"(slot), "l"(sbase), "r"((unsigned)poll));
+    unsigned par = poll ? (unsigned)pslot[8] : 0u;   // slot of the next poll (lane 0; persists)
     const float tsm = tau_sm * 0.99999f;
     for (int it = 1; it <= pa.max_iters; it++) {
         const bool act = row && t > prog;
-        const unsigned put = slot + 16u * (it & 1), get = slot + 16u * ((it + 1) & 1) + soff;
+        const unsigned put = slot + 16u * (par & 1u), get = slot + 16u * ((par + 1u) & 1u) + soff;
+        par ^= 1u;
         asm volatile("{ .reg .pred p; setp.ne.u32 p, %2, 0; @p cp.async.cg.shared.global [%0], [%1], 16; "
                      "cp.async.commit_group; }" ::"r"(put), "l"(sbase), "r"((unsigned)poll));
         float xn[CP_N], xp[CP_N];
@@ -644,7 +643,7 @@ __device__ __forceinline__ void cp_alg1_loop(const Team tm, int W, const ProjArg
         }
         int sf;   // lane 0 only; no "memory" clobber (it would pin stage 1's constant-bank reads)
         asm volatile("{ .reg .pred p; setp.ne.u32 p, %2, 0; cp.async.wait_group 1; mov.u32 %0, 0; "
-                     "@p ld.shared.b32 %0, [%1]; }" : "=r"(sf) : "r"(get), "r"((unsigned)poll));
+                     "@p ld.shared.b32 %0, [%1]; }" : "=r"(sf) : "r"(get), "r"((unsigned)(poll && it > 1)));
         const unsigned vm = tm.ballot(valid || sf != 0) & full;
         const unsigned hi = vm & ~((2u << prog) - 1u);              // literal-gap
         const int np1 = hi ? 31 - __clz(hi) : prog;
@@ -680,6 +679,7 @@ __device__ __forceinline__ void cp_alg1_loop(const Team tm, int W, const ProjArg
             if (t == 0) trace_prog[it - 1] = np;
         }
     }
+    if (poll) pslot[8] = (int)par;
 }
 
 // Project the team's segment in place: Alg. 1 (pure.py:549-577) for modes
@@ -689,7 +689,7 @@ __device__ __forceinline__ void cp_alg1_loop(const Team tm, int W, const ProjArg
 // trace (optional, parity only): after every iteration the buffer is copied
 // to trace[it-1] and the prefix to trace_prog[it-1].
 // stop_flag (planner): the query's stop word, polled once per iteration
-// through poll_slot (the team's 32-byte, 16-byte aligned shared-memory slot;
+// through poll_slot (the team's 48-byte, 16-byte aligned shared-memory slot;
 // no poll without it) off the critical path (cp_alg1_loop); when it is set
 // the projection is abandoned (returns false with *iters_out = -1) so a team
 // that lost the race leaves within two iterations instead of finishing its
@@ -1400,9 +1400,9 @@ __device__ __forceinline__ int* cp_par(const PlanArgs& A, int q, int k) {
     return A.parents + (size_t)(2 * q + k) * A.cap;
 }
 
-// (host mirror: runtime.cpp ws_bytes = 32 + (G + 7) NP floats, rounded up to 16 B)
+// (host mirror: runtime.cpp ws_bytes = 48 + (G + 7) NP floats, rounded up to 16 B)
 struct alignas(16) TeamWS {
-    int poll[8];           // stop-word poll: two 16 B landing slots (cp_alg1_loop)
+    int poll[12];          // stop-word poll: two 16 B landing slots + the next slot's parity (cp_alg1_loop)
     float seg[CP_G][CP_NP];
     float qr[CP_NP], qn[CP_NP], qs[CP_NP], qe[CP_NP], qc[CP_NP], qt[CP_NP], qm[CP_NP];
 };

@@ -416,8 +416,8 @@ int get_module(Ctx* c, int G, int kind, int orient, int parity, Module** out) {
     m->G = G;
     m->kind = kind;
     m->orient = orient;
-    // sizeof(TeamWS): the two 16-byte poll slots, G segment rows and 7 vectors, 16-byte aligned
-    m->ws_bytes = ((size_t)32 + (size_t)(G + 7) * c->NP * sizeof(float) + 15) & ~(size_t)15;
+    // sizeof(TeamWS): the poll slots (48 B), G segment rows and 7 vectors, 16-byte aligned
+    m->ws_bytes = ((size_t)48 + (size_t)(G + 7) * c->NP * sizeof(float) + 15) & ~(size_t)15;
     for (const char* k : {"cp_plan_kernel", "cp_validate_kernel", "cp_validate_cull_kernel", "cp_project_kernel",
                           "cp_dense_kernel", "cp_step_kernel"})
         if (m->fn.count(k)) drv().funcSetAttribute(m->fn[k], CU_FUNC_ATTRIBUTE_MAX_DYNAMIC_SHARED_SIZE_BYTES, 200 * 1024);

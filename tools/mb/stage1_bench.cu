@@ -99,7 +99,7 @@ extern "C" __global__ void halton_bench(int iters, long long seed, long long* cy
 // toward a point 0.5 rad away (the planner's P1), repeated
 extern "C" __global__ void proj_bench(int reps, long long* cyc, int* iters_out, const int* stop, float span = 1.f) {
     __shared__ float seg[CP_G][CP_NP];
-    __shared__ __align__(16) int pslot[8];
+    __shared__ __align__(16) int pslot[12];
     Team tm;
     const float qa[7] = {-0.07434654f, 0.54688579f, 2.74340846f, -2.4217312f, -0.20725576f, 1.89866585f, 2.79144559f};
     const float dq[7] = {0.25f, -0.2f, -0.15f, 0.2f, -0.15f, 0.1f, -0.2f};
