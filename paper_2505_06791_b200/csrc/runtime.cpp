@@ -1351,6 +1351,9 @@ static int plan_launch(Ctx* c, const cprrtc_params* prm, int B, const double* st
     // 256 / 320 / 384 -> 0.178 / 0.177 / 0.185 / 0.186 ms, p90 0.334-0.343
     // (r1 A/B on the 999-box shelf: pairs also win for unconstrained queries,
     // arm8 0.28 -> 0.23 ms, arm7 equal)
+    // (r1 re-sweep after the fast start, tools/team_sweep.sh: 160-222 pairs
+    // ~2 % under 256 on upright Panda, but the shelf and configs[3] medians
+    // 4-5 % over; 256 kept)
     static const bool pair_off = getenv("CPRRTC_PAIR") && atoi(getenv("CPRRTC_PAIR")) == 0;
     const bool pair = solo && !pair_off;
     const int tpw = solo ? 1 : 32 / m->G;         // teams per warp
