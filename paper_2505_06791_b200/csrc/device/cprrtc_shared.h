@@ -94,7 +94,8 @@ struct PlanArgs {
     int n_race;            // racers of a cprrtc_plan_race call (0: no race)
     int* race_flag;        // this racer's first-solution word (polled)
     int* race_peers[8];    // every racer's word (peer-mapped); the winner stores 1 to each
-    // results, written by the last team to leave each query (planner.py:488-505)
+    // results (planner.py:488-505): the path by the solving team, status and
+    // counters by the last team to leave each query
     struct QueryOut* out;  // (nq) mapped host memory
     float* paths;          // (nq, path_cap, CP_N) mapped host memory
     int* sources;          // (nq, path_cap) mapped host memory
