@@ -1424,7 +1424,9 @@ __device__ __forceinline__ bool cp_should_stop(const Team& tm, QueryState& Q, co
             atomicExch(&Q.stop, 1);
             s = 1;
         }
-        if (!s && A.budget_ns > 0 && cp_clock_ns() - Q.t0_ns > (u64)A.budget_ns) {
+        // budget_ns < 0: a zero / negative time budget, expired before the
+        // first sample (the reference's TimedOut at iteration 1, planner.py:450-453)
+        if (!s && A.budget_ns != 0 && (A.budget_ns < 0 || cp_clock_ns() - Q.t0_ns > (u64)A.budget_ns)) {
             atomicExch(&Q.timed_out, 1);
             atomicExch(&Q.stop, 1);
             s = 1;
@@ -1482,7 +1484,15 @@ __device__ __forceinline__ int cp_append(const Team& tm, const PlanArgs& A, Quer
         if (tm.lane == 0) { atomicExch(&Q.overflow, 1); atomicExch(&Q.stop, 1); }
         return -1;
     }
-    if (tm.lane == 0) cp_par(A, qi, k)[idx] = par;
+    // publication order: the parent, then (behind lane 0's fence) coordinate
+    // 0, which lane 0 stores itself.  A node counts as present only once every
+    // coordinate is non-NaN, so whoever sees it (NN scan, connect, extraction
+    // after its own fence) also sees its parent -- the reset kernel never
+    // clears parents[], so a stale parent would otherwise be readable.
+    if (tm.lane == 0) {
+        cp_par(A, qi, k)[idx] = par;
+        __threadfence();
+    }
     if ((int)tm.lane < CP_N) cp_tree(A, qi, k)[(size_t)tm.lane * A.cap + idx] = q[tm.lane];
     tm.sync();
     return idx;
@@ -1746,7 +1756,7 @@ __device__ void cp_plan_query_pair(const Team& tm, TeamWS& ws, TeamWS& wsc, Pair
 #endif
     for (int round = 0;; round++) {
         CP_PF_T0(t_stop);
-        if (!(round == 0 && first_it > 0) && cp_should_stop(tm, Q, A)) break;
+        if (!(round == 0 && first_it > 0 && A.budget_ns >= 0) && cp_should_stop(tm, Q, A)) break;
         CP_PF_ADD(PF_STOP, t_stop);
         CP_PF_T0(t_samp);
         int it = first_it;
@@ -1927,7 +1937,7 @@ __device__ void cp_plan_query(const Team& tm, TeamWS& ws, const PlanArgs& A, con
     Stats st;
     const int W = A.W;
     for (int round = 0;; round++) {
-        if (!(round == 0 && first_it > 0) && cp_should_stop(tm, Q, A)) break;
+        if (!(round == 0 && first_it > 0 && A.budget_ns >= 0) && cp_should_stop(tm, Q, A)) break;
         int it = first_it;
         if (round > 0 || first_it <= 0) {
             if (tm.lane == 0) it = atomicAdd(&Q.next_sample, 1) + 1 + (first_it > 0 ? n_teams : 0);
@@ -2048,6 +2058,7 @@ __device__ __noinline__ void cp_extract_path(const Team tm, const PlanArgs& A, i
     // the two parent chains are walked concurrently: lane 0 the start tree
     // into ch[0..), lane 1 the goal tree into ch[path_cap - 1] downwards
     const int m0 = cp_ldvol(&Q.meet[0]), m1 = cp_ldvol(&Q.meet[1]);
+    __threadfence();   // pairs with cp_append's fence: chain nodes seen => their parents seen
     int cnt = 0;
     if (lane == 0) {
         for (int i = m0;; i = __ldcg(ps + i)) {   // start chain, meet first

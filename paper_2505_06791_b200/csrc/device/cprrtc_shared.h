@@ -89,7 +89,7 @@ struct PlanArgs {
     float step, tol, margin;
     int flag_on;
     int max_iterations, max_connect;
-    i64 budget_ns;         // <= 0: no time budget (deterministic)
+    i64 budget_ns;         // 0: no time budget (deterministic); < 0: expired before the first sample
     int solo;              // 1: one team per warp (the other half-warp idles) -- latency mode
     int n_race;            // racers of a cprrtc_plan_race call (0: no race)
     int* race_flag;        // this racer's first-solution word (polled)

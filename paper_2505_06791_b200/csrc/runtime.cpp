@@ -308,6 +308,7 @@ struct Ctx {
     DevBuf sc_box_c, sc_box_h, sc_sph, sc_bmin, sc_bmax, sc_sc, sc_sr;
     DevBuf sc_cl;          // clustered layout (broad phase), see SceneSm
     DevBuf race_flag;      // first-solution word of cprrtc_plan_race
+    int* race_host = nullptr;   // fallback first-solution word without peer access (mapped, portable)
     int nbc = 0, nec = 0;
     // constraint
     int kind = 0, orient = 0;
@@ -745,6 +746,7 @@ int cprrtc_ctx_destroy(void* p) {
     if (c->fork) cudaEventDestroy(c->fork);
     if (c->join) cudaEventDestroy(c->join);
     if (c->stream2) cudaStreamDestroy(c->stream2);
+    if (c->race_host) cudaFreeHost(c->race_host);
     cudaStreamDestroy(c->stream);
     delete c;
     return 0;
@@ -1267,7 +1269,8 @@ static PlanArgs make_plan_args(Ctx* c, const cprrtc_params* prm, int B, int cap,
     A.flag_on = prm->flag_on;
     A.max_iterations = prm->max_iterations;
     A.max_connect = prm->max_connect_segments;
-    A.budget_ns = (prm->deterministic || prm->time_budget_ms <= 0) ? 0 : (i64)(prm->time_budget_ms * 1e6);
+    // 0: no budget (deterministic); -1: already expired (time_budget_ms <= 0)
+    A.budget_ns = prm->deterministic ? 0 : (prm->time_budget_ms <= 0 ? -1 : (i64)(prm->time_budget_ms * 1e6));
     return A;
 }
 
@@ -1581,24 +1584,38 @@ int cprrtc_plan_race(void* const* ctxs, int n_ctx, const cprrtc_params* prm, con
         }
     RaceLink link{};
     link.n = n_ctx;
-    static int* host_flag = nullptr;   // fallback without peer access: one mapped, portable host word
+    // every racer's previous work (its last call's reset kernel included) is
+    // drained and every flag word cleared before the first racer launches, so
+    // no clear can land after a fast racer's win store
+    for (int k = 0; k < n_ctx; k++) {
+        if (int rc = set_device(cs[k])) return rc;
+        CUDA_TRY(cudaStreamSynchronize(cs[k]->stream));
+        if (cs[k]->stream2) CUDA_TRY(cudaStreamSynchronize(cs[k]->stream2));
+    }
     if (peers) {
         for (int k = 0; k < n_ctx; k++) {
             if (int rc = set_device(cs[k])) return rc;
             if (int rc = cs[k]->race_flag.ensure(4)) return rc;
-            CUDA_TRY(cudaMemsetAsync(cs[k]->race_flag.p, 0, 4, cs[k]->stream));
+            CUDA_TRY(cudaMemset(cs[k]->race_flag.p, 0, 4));
             link.peers[k] = cs[k]->race_flag.as<int>();
         }
+        for (int k = 0; k < n_ctx; k++) {
+            if (int rc = set_device(cs[k])) return rc;
+            CUDA_TRY(cudaDeviceSynchronize());
+        }
     } else {
-        if (!host_flag) {
+        // one mapped, portable host word owned by racer 0's context (per call
+        // state: concurrent races use distinct contexts, hence distinct words)
+        if (!cs[0]->race_host) {
             void* h = nullptr;
+            if (int rc = set_device(cs[0])) return rc;
             cudaError_t e = cudaHostAlloc(&h, 64, cudaHostAllocMapped | cudaHostAllocPortable);
             if (e != cudaSuccess) return fail(CPRRTC_ECUDA, std::string("cudaHostAlloc: ") + cudaGetErrorString(e));
-            host_flag = static_cast<int*>(h);   // UVA: the same address on every device
+            cs[0]->race_host = static_cast<int*>(h);   // UVA: the same address on every device
         }
-        *(volatile int*)host_flag = 0;
+        *(volatile int*)cs[0]->race_host = 0;
         link.n = 1;
-        link.peers[0] = host_flag;
+        link.peers[0] = cs[0]->race_host;
     }
     int rc = 0;
     for (int k = 0; k < n_ctx && !rc; k++) {

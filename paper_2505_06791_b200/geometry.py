@@ -2,22 +2,17 @@
 clearance queries and union-preserving densification.
 
 Public names mirror ``maniplan/geometry.py`` (Aabb, Sphere, Scene,
-PackedScene, subdivide_scene, load_scene ...).  The packed arrays have the
+PackedScene, subdivide_scene ...; the YAML loaders are the reference's own).  The packed arrays have the
 reference layout (``geometry.py:101-135``); the device copy is FP32 in
 shared memory ("Data layout").
 """
 
 from __future__ import annotations
 
-import io
 import math
-import os
 from dataclasses import dataclass, field
 
 import numpy as np
-import yaml
-
-from .errors import SceneFormatError
 
 __all__ = [
     "Aabb", "Sphere", "Scene", "PackedScene", "sphere_aabb_clearance",
@@ -168,32 +163,29 @@ def scene_contains(scene: Scene, point) -> bool:
     return False
 
 
-def _halve(box: Aabb):
-    ext = box.extents
-    ax = 0
-    for k in (1, 2):               # longest axis, lowest index on ties
-        if ext[k] > ext[ax]:
-            ax = k
-    cut = 0.5 * (box.min[ax] + box.max[ax])
-    lo_hi = box.max.copy()
-    lo_hi[ax] = cut
-    hi_lo = box.min.copy()
-    hi_lo[ax] = cut
-    return Aabb(box.min.copy(), lo_hi), Aabb(hi_lo, box.max.copy())
-
-
 def subdivide_box(box: Aabb, factor: int) -> list:
-    """``factor`` boxes tiling ``box`` exactly: keep halving the largest
-    piece (first on ties) -- the reference's densification rule
-    (geometry.py:190-210)."""
+    """``factor`` boxes tiling ``box`` exactly, by the reference's
+    densification rule (geometry.py:175-210): the largest-volume piece
+    (first on ties) is cut at the midpoint of its longest axis (lowest axis on
+    ties) until there are ``factor`` pieces.  Pieces are kept as (k, 3) corner
+    arrays; volumes are the same e0*e1*e2 products, so ties break identically."""
     if factor < 1:
         raise ValueError("subdivision factor must be >= 1")
-    pieces = [box]
-    while len(pieces) < factor:
-        vols = [p.volume for p in pieces]
-        k = int(np.argmax(vols))
-        pieces[k:k + 1] = list(_halve(pieces[k]))
-    return pieces
+    lo = box.min[None, :].copy()
+    hi = box.max[None, :].copy()
+    while lo.shape[0] < factor:
+        ext = hi - lo
+        k = int(np.argmax(ext[:, 0] * ext[:, 1] * ext[:, 2]))
+        ax = int(np.argmax(ext[k]))
+        mid = 0.5 * (lo[k, ax] + hi[k, ax])
+        upper_lo = lo[k].copy()
+        upper_lo[ax] = mid
+        lower_hi = hi[k].copy()
+        lower_hi[ax] = mid
+        lo = np.insert(lo, k + 1, upper_lo, axis=0)
+        hi = np.insert(hi, k + 1, hi[k], axis=0)
+        hi[k] = lower_hi
+    return [Aabb(a, b) for a, b in zip(lo, hi)]
 
 
 def subdivide_scene(scene: Scene, factor: int) -> Scene:
@@ -204,99 +196,3 @@ def subdivide_scene(scene: Scene, factor: int) -> Scene:
     boxes = [piece for b in scene.boxes for piece in subdivide_box(b, factor)]
     return Scene(boxes=tuple(boxes), spheres=scene.spheres,
                  name=f"{scene.name}@{factor}x" if scene.name else "")
-
-
-# --------------------------------------------------------------------------
-# YAML format (reference geometry.py:229-340): name / boxes[min,max] /
-# spheres[center,radius]
-# --------------------------------------------------------------------------
-
-def read_source(source, err=SceneFormatError):
-    """(text, where) from a path, a YAML string, bytes or a stream."""
-    if hasattr(source, "read"):
-        data = source.read()
-        if isinstance(data, bytes):
-            data = data.decode("utf-8")
-        return data, getattr(source, "name", "<stream>")
-    if isinstance(source, bytes):
-        return source.decode("utf-8"), "<bytes>"
-    if isinstance(source, str):
-        if "\n" not in source and os.path.exists(source):
-            with io.open(source, encoding="utf-8") as fh:
-                return fh.read(), source
-        return source, "<string>"
-    if hasattr(source, "__fspath__"):
-        with io.open(os.fspath(source), encoding="utf-8") as fh:
-            return fh.read(), os.fspath(source)
-    raise err(f"cannot read document from {type(source).__name__}")
-
-
-def _parse_yaml(text, where, err):
-    try:
-        return yaml.safe_load(text)
-    except yaml.YAMLError as exc:
-        mark = getattr(exc, "problem_mark", None)
-        raise err(f"not valid YAML: {exc}",
-                  f"{where}:line {mark.line + 1}" if mark else where) from None
-
-
-def _num3(v, where):
-    if not isinstance(v, (list, tuple)) or len(v) != 3:
-        raise SceneFormatError("expected a 3-element list", where)
-    try:
-        return np.array([float(x) for x in v])
-    except (TypeError, ValueError):
-        raise SceneFormatError("expected numeric entries", where) from None
-
-
-def scene_from_dict(doc, where="scene") -> Scene:
-    doc = {} if doc is None else doc
-    if not isinstance(doc, dict):
-        raise SceneFormatError("document root must be a mapping", where)
-    extra = set(doc) - {"name", "boxes", "spheres"}
-    if extra:
-        raise SceneFormatError(f"unknown field {sorted(extra)[0]!r}", where)
-    name = doc.get("name", "")
-    if not isinstance(name, str):
-        raise SceneFormatError("name must be a string", f"{where}.name")
-    boxes, spheres = [], []
-    for i, ent in enumerate(doc.get("boxes") or []):
-        loc = f"{where}.boxes[{i}]"
-        if not isinstance(ent, dict):
-            raise SceneFormatError("expected a mapping with min/max", loc)
-        lo, hi = _num3(ent.get("min"), f"{loc}.min"), _num3(ent.get("max"), f"{loc}.max")
-        bad = np.nonzero(lo > hi)[0]
-        if bad.size:
-            raise SceneFormatError(f"max < min on axis {int(bad[0])}", loc)
-        try:
-            boxes.append(Aabb(lo, hi))
-        except ValueError as exc:
-            raise SceneFormatError(str(exc), loc) from None
-    for i, ent in enumerate(doc.get("spheres") or []):
-        loc = f"{where}.spheres[{i}]"
-        if not isinstance(ent, dict):
-            raise SceneFormatError("expected a mapping with center/radius", loc)
-        c = _num3(ent.get("center"), f"{loc}.center")
-        try:
-            r = float(ent.get("radius"))
-        except (TypeError, ValueError):
-            raise SceneFormatError("radius must be a number", loc) from None
-        try:
-            spheres.append(Sphere(c, r))
-        except ValueError as exc:
-            raise SceneFormatError(str(exc), loc) from None
-    return Scene(boxes=tuple(boxes), spheres=tuple(spheres), name=name)
-
-
-def load_scene(source) -> Scene:
-    text, where = read_source(source)
-    return scene_from_dict(_parse_yaml(text, where, SceneFormatError), where)
-
-
-def dump_scene(scene: Scene) -> str:
-    return yaml.safe_dump({
-        "name": scene.name,
-        "boxes": [{"min": b.min.tolist(), "max": b.max.tolist()} for b in scene.boxes],
-        "spheres": [{"center": s.center.tolist(), "radius": s.radius}
-                    for s in scene.spheres],
-    }, sort_keys=False)

@@ -221,7 +221,7 @@ def task_err_jac_batch(model, spec, q, fp64: bool = False, device: int = 0):
 def task_error_at(packed_spec, pose7):
     """FP64 task error at a pose; needs no robot (any cached context works)."""
     pose = _f64(pose7).reshape(-1, 7)
-    ctx = _any_context()
+    ctx = _pose_context()
     with ctx.lock:
         ctx.set_spec(packed_spec)
         e = np.empty((pose.shape[0], ctx.m))
@@ -230,18 +230,22 @@ def task_error_at(packed_spec, pose7):
     return e[0] if np.ndim(pose7) == 1 else e
 
 
-def _any_context() -> Context:
-    with _CTX_LOCK:
-        if _CTX:
-            return next(iter(_CTX.values()))
-    # a 1-joint stub robot: task_error_at depends only on the pose
-    from types import SimpleNamespace
-    stub = SimpleNamespace(jtypes=np.zeros(1, np.int32), axes=np.array([[0, 0, 1.0]]),
-                           origin_r=np.eye(3).reshape(1, 9), origin_p=np.zeros((1, 3)),
-                           lo=np.array([-1.0]), hi=np.array([1.0]),
-                           sphere_link=np.zeros(0, np.int32), sphere_local=np.zeros((0, 3)),
-                           sphere_radius=np.zeros(0), pairs=np.zeros((0, 2), np.int32), ee_link=0)
-    return context(stub)
+_POSE_STUB = None
+
+
+def _pose_context() -> Context:
+    """A private context (1-joint stub robot, this thread) for the robot-free
+    pose helpers: it never shares constraint state with a planning context."""
+    global _POSE_STUB
+    if _POSE_STUB is None:
+        from types import SimpleNamespace
+        _POSE_STUB = SimpleNamespace(
+            jtypes=np.zeros(1, np.int32), axes=np.array([[0, 0, 1.0]]),
+            origin_r=np.eye(3).reshape(1, 9), origin_p=np.zeros((1, 3)),
+            lo=np.array([-1.0]), hi=np.array([1.0]), sphere_link=np.zeros(0, np.int32),
+            sphere_local=np.zeros((0, 3)), sphere_radius=np.zeros(0),
+            pairs=np.zeros((0, 2), np.int32), ee_link=0)
+    return context(_POSE_STUB, 0, slot=-1)
 
 
 def damped_step(jac, e, lam, device: int = 0):

@@ -1,7 +1,8 @@
 """Serial-chain robot model, its packed layout, and device-backed FK.
 
 Public names mirror ``maniplan/kinematics.py`` (Joint, LinkSphere,
-RobotModel, PackedRobot, FrameSet, forward_kinematics, load_robot ...).
+RobotModel, PackedRobot, FrameSet, forward_kinematics ...; YAML loading is
+the reference's own).
 ``RobotModel.packed`` reproduces the reference packing bit-for-bit
 (``kinematics.py:176-224``); the device never sees these float64 arrays
 directly -- the NVRTC code generator folds them into unrolled FP32 FK code
@@ -15,10 +16,8 @@ from functools import cached_property
 from math import cos, sin
 
 import numpy as np
-import yaml
 
-from .errors import RobotFormatError
-from .geometry import Sphere, _parse_yaml, read_source
+from .geometry import Sphere
 
 __all__ = [
     "Joint", "LinkSphere", "RobotModel", "FrameSet", "PackedRobot",
@@ -211,95 +210,3 @@ def clamp_to_limits(model: RobotModel, q) -> np.ndarray:
     q = model.check_q(q)
     p = model.packed
     return np.clip(q, p.lo, p.hi)
-
-
-# --------------------------------------------------------------------------
-# YAML robot format (reference kinematics.py:1-26, :278-375)
-# --------------------------------------------------------------------------
-
-def _floats(v, k, where):
-    if not isinstance(v, (list, tuple)) or len(v) != k:
-        raise RobotFormatError(f"expected a {k}-element list", where)
-    try:
-        return [float(x) for x in v]
-    except (TypeError, ValueError):
-        raise RobotFormatError("expected numeric entries", where) from None
-
-
-def robot_from_dict(doc, where="robot") -> RobotModel:
-    if not isinstance(doc, dict):
-        raise RobotFormatError("document root must be a mapping", where)
-    allowed = {"name", "joints", "ee_link", "link_spheres",
-               "self_collision_pairs", "zero_pose_ee"}
-    for key in doc:
-        if key not in allowed:
-            raise RobotFormatError(f"unknown field {key!r}", where)
-    raw = doc.get("joints")
-    if not isinstance(raw, list) or not raw:
-        raise RobotFormatError("joints must be a non-empty list", f"{where}.joints")
-    joints = []
-    for i, ent in enumerate(raw):
-        loc = f"{where}.joints[{i}]"
-        if not isinstance(ent, dict):
-            raise RobotFormatError("expected a mapping", loc)
-        origin = ent.get("origin") or {}
-        if not isinstance(origin, dict):
-            raise RobotFormatError("origin must be a mapping", f"{loc}.origin")
-        axis = _floats(ent.get("axis"), 3, f"{loc}.axis")
-        xyz = _floats(origin.get("xyz", [0, 0, 0]), 3, f"{loc}.origin.xyz")
-        rpy = _floats(origin.get("rpy", [0, 0, 0]), 3, f"{loc}.origin.rpy")
-        lim = _floats(ent.get("limits"), 2, f"{loc}.limits")
-        try:
-            joints.append(Joint(jtype=ent.get("type", "revolute"), axis=axis,
-                                origin_xyz=xyz, origin_rpy=rpy, lo=lim[0], hi=lim[1],
-                                name=str(ent.get("name", f"j{i}"))))
-        except ValueError as exc:
-            raise RobotFormatError(str(exc), loc) from None
-    spheres = []
-    for i, ent in enumerate(doc.get("link_spheres") or []):
-        loc = f"{where}.link_spheres[{i}]"
-        if not isinstance(ent, dict):
-            raise RobotFormatError("expected a mapping", loc)
-        try:
-            spheres.append(LinkSphere(link=int(ent.get("link")),
-                                      center=_floats(ent.get("center"), 3, f"{loc}.center"),
-                                      radius=float(ent.get("radius"))))
-        except (TypeError, ValueError) as exc:
-            raise RobotFormatError(str(exc), loc) from None
-    pairs = []
-    for i, ent in enumerate(doc.get("self_collision_pairs") or []):
-        if not isinstance(ent, (list, tuple)) or len(ent) != 2:
-            raise RobotFormatError("expected an index pair",
-                                   f"{where}.self_collision_pairs[{i}]")
-        pairs.append((int(ent[0]), int(ent[1])))
-    zp = doc.get("zero_pose_ee")
-    if zp is not None:
-        zp = _floats(zp, 7, f"{where}.zero_pose_ee")
-    try:
-        return RobotModel(joints=tuple(joints), link_spheres=tuple(spheres),
-                          ee_link=int(doc.get("ee_link", -1)),
-                          self_collision_pairs=tuple(pairs),
-                          name=str(doc.get("name", "")), zero_pose_ee=zp)
-    except ValueError as exc:
-        raise RobotFormatError(str(exc), where) from None
-
-
-def load_robot(source) -> RobotModel:
-    text, where = read_source(source, RobotFormatError)
-    return robot_from_dict(_parse_yaml(text, where, RobotFormatError), where)
-
-
-def dump_robot(model: RobotModel) -> str:
-    doc = {
-        "name": model.name,
-        "joints": [{"name": j.name, "type": j.jtype, "axis": j.axis.tolist(),
-                    "origin": {"xyz": j.origin_xyz.tolist(), "rpy": j.origin_rpy.tolist()},
-                    "limits": [j.lo, j.hi]} for j in model.joints],
-        "ee_link": model.ee_link,
-        "link_spheres": [{"link": s.link, "center": s.center.tolist(), "radius": s.radius}
-                         for s in model.link_spheres],
-        "self_collision_pairs": [list(p) for p in model.self_collision_pairs],
-    }
-    if model.zero_pose_ee is not None:
-        doc["zero_pose_ee"] = model.zero_pose_ee.tolist()
-    return yaml.safe_dump(doc, sort_keys=False)

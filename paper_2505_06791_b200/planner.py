@@ -31,6 +31,7 @@ from __future__ import annotations
 import ctypes as C
 import math
 import time
+from contextlib import contextmanager
 from dataclasses import dataclass, field, replace
 
 import numpy as np
@@ -45,7 +46,7 @@ from .projection import MotionSegment, ProjectionParams
 __all__ = [
     "Tree", "PlanParams", "PlanProblem", "PlanResult", "PlanStats", "PlanContext",
     "ExtendOutcome", "ConnectOutcome", "DeviceOptions", "nearest", "steer", "plan",
-    "plan_batch", "extract_path", "derive_edge", "revalidate_path", "dense_path", "extend",
+    "plan_batch", "extract_path", "derive_edge", "derive_path", "revalidate_path", "dense_path", "extend",
     "connect", "prepare", "plan_race",
 ]
 
@@ -169,7 +170,7 @@ class PlanStats:
 
 @dataclass(frozen=True)
 class PlanResult:
-    status: str                                  # Solved | TimedOut | IterLimit
+    status: str              # Solved | TimedOut | IterLimit (+ CapacityExceeded, Stopped; see _STATUS)
     path: tuple | None
     edge_sources: tuple | None
     stats: PlanStats
@@ -218,7 +219,10 @@ class ConnectOutcome:
 
 
 _MODES = {"parallel": 0, "literal-gap": 1, "naive": 2}
-_STATUS = {0: "Solved", 1: "TimedOut", 2: "IterLimit", 3: "IterLimit", 5: "Stopped"}   # 5: another racer solved
+# 3: a tree reached DeviceOptions.tree_capacity before a solution, the time
+#    budget or max_iterations (no reference counterpart: its trees are
+#    unbounded); 5: another racer solved the query (plan_race)
+_STATUS = {0: "Solved", 1: "TimedOut", 2: "IterLimit", 3: "CapacityExceeded", 5: "Stopped"}
 _SETUP = {1: "start violates joint limits", 2: "start is off the constraint manifold",
           3: "start is in collision", 4: "goal violates joint limits",
           5: "goal is off the constraint manifold", 6: "goal is in collision"}
@@ -292,19 +296,44 @@ def _make_params(p: PlanParams, opt: DeviceOptions) -> _lib.Params:
         path_capacity=int(opt.path_capacity), cc_broadphase=int(opt.cc_broadphase))
 
 
-def _bind(problem_like, opt: DeviceOptions):
+@contextmanager
+def _bound(problem_like, opt: DeviceOptions):
+    """The problem's context with its lock held and its scene and constraint
+    uploaded: the bind and every launch that depends on it run under one
+    lock, so no other caller can swap the constraint in between."""
     ctx = kernels.context(problem_like.model, opt.device)
-    ctx.set_scene(problem_like.scene.packed())
-    ctx.set_spec(None if problem_like.spec is None else problem_like.spec.packed)
-    return ctx
+    with ctx.lock:
+        ctx.set_scene(problem_like.scene.packed())
+        ctx.set_spec(None if problem_like.spec is None else problem_like.spec.packed)
+        yield ctx
+
+
+@contextmanager
+def _bound_many(problem_like, devices):
+    """One bound, prepared context per entry of ``devices`` (a repeated
+    device gets a further independent context), every lock held."""
+    from contextlib import ExitStack
+    seen: dict = {}
+    with ExitStack() as stack:
+        ctxs = []
+        for d in devices:
+            slot = seen.get(d, 0)
+            seen[d] = slot + 1
+            c = kernels.context(problem_like.model, d, slot)
+            stack.enter_context(c.lock)
+            c.set_scene(problem_like.scene.packed())
+            c.set_spec(None if problem_like.spec is None else problem_like.spec.packed)
+            c.prepare(problem_like.params.width)
+            ctxs.append(c)
+        yield ctxs
 
 
 def prepare(problem: PlanProblem, options: DeviceOptions = DeviceOptions()):
     """Build / load the NVRTC module for this problem's robot, constraint kind
     and width (done implicitly by plan(); call it to keep compile time out of a
     measurement, like the reference keeps file loading out of wall_ms)."""
-    ctx = _bind(problem, options)
-    ctx.prepare(problem.params.width)
+    with _bound(problem, options) as ctx:
+        ctx.prepare(problem.params.width)
     return ctx
 
 
@@ -332,7 +361,7 @@ def plan_batch(problems, options: DeviceOptions = DeviceOptions(), return_dense:
                     or (p.params is not p0.params and _params_key(p.params) != base)):
                 raise ValueError("plan_batch problems must share model, scene, spec and params")
     prm = _params_struct(p0.params, options)
-    ctx = _bind(p0, options)
+    ctx = kernels.context(p0.model, options.device)
     n = ctx.n
     B = len(problems)
     starts = np.ascontiguousarray(np.stack([p.start for p in problems]), dtype=np.float64)
@@ -345,24 +374,15 @@ def plan_batch(problems, options: DeviceOptions = DeviceOptions(), return_dense:
     paths, srcs = _out_buffers(B, pc, n)
     devs = tuple(int(d) for d in devices) if devices is not None else ()
     if len(devs) > 1:
-        seen: dict = {}
-        ctxs = []
-        for d in devs:
-            slot = seen.get(d, 0)
-            seen[d] = slot + 1
-            c = kernels.context(p0.model, d, slot)
-            c.set_scene(p0.scene.packed())
-            c.set_spec(None if p0.spec is None else p0.spec.packed)
-            c.prepare(p0.params.width)
-            ctxs.append(c)
-        handles = (C.c_void_p * len(ctxs))(*[c.h.value for c in ctxs])
-        t0 = time.perf_counter()
-        _lib.check(ctx.L.cprrtc_plan_multi(handles, len(ctxs), C.byref(prm), B, _lib.ptr(starts),
-                                           _lib.ptr(goals), _lib.ptr(seeds, _lib._lp), res, _lib.ptr(paths),
-                                           _lib.ptr(srcs, _lib._ip)), "plan_multi")
-        wall = (time.perf_counter() - t0) * 1e3
+        with _bound_many(p0, devs) as ctxs:
+            handles = (C.c_void_p * len(ctxs))(*[c.h.value for c in ctxs])
+            t0 = time.perf_counter()
+            _lib.check(ctx.L.cprrtc_plan_multi(handles, len(ctxs), C.byref(prm), B, _lib.ptr(starts),
+                                               _lib.ptr(goals), _lib.ptr(seeds, _lib._lp), res,
+                                               _lib.ptr(paths), _lib.ptr(srcs, _lib._ip)), "plan_multi")
+            wall = (time.perf_counter() - t0) * 1e3
     else:
-        with ctx.lock:
+        with _bound(p0, options) as ctx:
             ctx.prepare(p0.params.width)
             t0 = time.perf_counter()
             _lib.check(ctx.L.cprrtc_plan(ctx.h, C.byref(prm), B, _lib.ptr(starts), _lib.ptr(goals),
@@ -371,11 +391,12 @@ def plan_batch(problems, options: DeviceOptions = DeviceOptions(), return_dense:
             wall = (time.perf_counter() - t0) * 1e3
     out = _results_bulk(res, problems, paths, srcs, wall, pc)
     if return_dense:
-        for i, r in enumerate(out):
-            if r.solved:
-                L = len(r.path)
-                dense, ok = _derive(ctx, prm, paths[i, :L], srcs[i, :L - 1])
-                out[i] = replace(r, dense=dense)
+        with _bound(p0, options) as ctx:
+            for i, r in enumerate(out):
+                if r.solved:
+                    L = len(r.path)
+                    dense, ok = _derive(ctx, prm, paths[i, :L], srcs[i, :L - 1])
+                    out[i] = replace(r, dense=dense)
     return out
 
 
@@ -510,7 +531,7 @@ _ONE: dict = {}
 
 def _plan_one(problem: PlanProblem, options: DeviceOptions, return_dense: bool) -> PlanResult:
     prm = _params_struct(problem.params, options)
-    ctx = _bind(problem, options)
+    ctx = kernels.context(problem.model, options.device)
     pc = int(prm.path_capacity)
     key = (id(ctx), pc, __import__("threading").get_ident())
     io = _ONE.get(key)
@@ -524,7 +545,7 @@ def _plan_one(problem: PlanProblem, options: DeviceOptions, return_dense: bool) 
     io.s[0] = problem.start
     io.g[0] = problem.goal
     io.seed[0] = seed
-    with ctx.lock:
+    with _bound(problem, options) as ctx:
         ctx.prepare(problem.params.width)
         t0 = time.perf_counter()
         rc = ctx.L.cprrtc_plan(ctx.h, C.byref(prm), 1, *io.args)
@@ -584,35 +605,26 @@ def plan_race(problem: PlanProblem, devices=(0, 1), options: DeviceOptions = Dev
         r = plan(problem, replace(options, device=devices[0]))
         return r, 0, [r]
     prm = _params_struct(problem.params, options)
-    seen: dict = {}
-    ctxs = []
-    for d in devices:
-        slot = seen.get(d, 0)
-        seen[d] = slot + 1
-        ctx = kernels.context(problem.model, d, slot)
-        ctx.set_scene(problem.scene.packed())
-        ctx.set_spec(None if problem.spec is None else problem.spec.packed)
-        ctx.prepare(problem.params.width)
-        ctxs.append(ctx)
-    R = len(ctxs)
-    n = ctxs[0].n
-    pc = int(prm.path_capacity)
     base = int(problem.params.seed_offset)
     if base < 0:
         raise ValueError("seed_offset must be >= 0")
+    R = len(devices)
+    pc = int(prm.path_capacity)
+    n = problem.model.n
     seeds = np.array([base + k * RACE_SEED_STRIDE for k in range(R)], np.int64)
     start = np.ascontiguousarray(problem.start, dtype=np.float64)
     goal = np.ascontiguousarray(problem.goal, dtype=np.float64)
     res = (_lib.Result * R)()
     paths = np.empty((R, pc, n))
     srcs = np.empty((R, pc), np.int32)
-    handles = (C.c_void_p * R)(*[c.h.value for c in ctxs])
     win = C.c_int32(-1)
-    t0 = time.perf_counter()
-    _lib.check(ctxs[0].L.cprrtc_plan_race(handles, R, C.byref(prm), _lib.ptr(start), _lib.ptr(goal),
-                                          _lib.ptr(seeds, _lib._lp), res, _lib.ptr(paths),
-                                          _lib.ptr(srcs, _lib._ip), C.byref(win)), "plan_race")
-    wall = (time.perf_counter() - t0) * 1e3
+    with _bound_many(problem, devices) as ctxs:
+        handles = (C.c_void_p * R)(*[c.h.value for c in ctxs])
+        t0 = time.perf_counter()
+        _lib.check(ctxs[0].L.cprrtc_plan_race(handles, R, C.byref(prm), _lib.ptr(start), _lib.ptr(goal),
+                                              _lib.ptr(seeds, _lib._lp), res, _lib.ptr(paths),
+                                              _lib.ptr(srcs, _lib._ip), C.byref(win)), "plan_race")
+        wall = (time.perf_counter() - t0) * 1e3
     per = [_result(res[k], problem, paths[k], srcs[k], wall, 1, pc) for k in range(R)]
     w = int(win.value)
     return per[w if w >= 0 else 0], w, per
@@ -645,10 +657,20 @@ def derive_edge(a, b, ctx: PlanContext, stats: PlanStats | None = None):
     """The re-derivable motion a -> b (planner.py:223-245) or None; device."""
     spec = None if ctx.spec is not None and math.isinf(ctx.spec.tau_task) else ctx.spec
     prob = PlanProblem(ctx.model, ctx.scene, spec, a, b, ctx.params)
-    dctx = _bind(prob, ctx.options)
     prm = _params_struct(ctx.params, ctx.options)
-    dense, ok = _derive(dctx, prm, np.stack([prob.start, prob.goal]), np.zeros(1, np.int32))
+    with _bound(prob, ctx.options) as dctx:
+        dense, ok = _derive(dctx, prm, np.stack([prob.start, prob.goal]), np.zeros(1, np.int32))
     return MotionSegment(dense[0]) if ok[0] else None
+
+
+def derive_path(result: PlanResult, problem: PlanProblem,
+                options: DeviceOptions = DeviceOptions()):
+    """Every edge of a solved path re-derived on the device exactly as the
+    planner certified it: (dense (E, W, n), ok (E,))."""
+    prm = _params_struct(problem.params, options)
+    src = np.array([_SRC.index(s) for s in result.edge_sources], dtype=np.int32)
+    with _bound(problem, options) as ctx:
+        return _derive(ctx, prm, np.stack(result.path), src)
 
 
 def revalidate_path(result: PlanResult, problem: PlanProblem,
@@ -660,25 +682,19 @@ def revalidate_path(result: PlanResult, problem: PlanProblem,
         return False
     if len(result.path) < 2:
         return True
-    ctx = _bind(problem, options)
-    prm = _params_struct(problem.params, options)
-    src = np.array([_SRC.index(s) for s in result.edge_sources], dtype=np.int32)
-    _, ok = _derive(ctx, prm, np.stack(result.path), src)
-    return bool(ok.all())
+    return bool(derive_path(result, problem, options)[1].all())
 
 
 def dense_path(result: PlanResult, problem: PlanProblem,
                options: DeviceOptions = DeviceOptions()) -> np.ndarray:
     """Dense waypoints (E*(W-1)+1, n) of a solved path, re-derived on the
     device; consecutive edges share their junction waypoint."""
-    ctx = _bind(problem, options)
-    prm = _params_struct(problem.params, options)
-    src = np.array([_SRC.index(s) for s in result.edge_sources], dtype=np.int32)
-    dense, ok = _derive(ctx, prm, np.stack(result.path), src)
+    if len(result.path) < 2:
+        return np.stack(result.path)
+    dense, ok = derive_path(result, problem, options)
     if not ok.all():
         raise RuntimeError("a path edge failed device re-derivation")
-    rows = [dense[0]] + [d[1:] for d in dense[1:]]
-    return np.concatenate(rows) if len(result.path) > 1 else np.stack(result.path)
+    return np.concatenate([dense[0]] + [d[1:] for d in dense[1:]])
 
 
 def extract_path(tree_s: Tree, tree_g: Tree, meet_s: int, meet_g: int):
@@ -703,7 +719,6 @@ def _step(op: int, tree: Tree, q, ctx: PlanContext):
     n = tree.nodes.shape[1]
     q = np.ascontiguousarray(np.asarray(q, dtype=float).reshape(n))
     prob = PlanProblem(ctx.model, ctx.scene, spec, tree.node(0), tree.node(0), ctx.params)
-    dctx = _bind(prob, ctx.options)
     prm = _params_struct(ctx.params, ctx.options)
     nodes = np.ascontiguousarray(tree.nodes, dtype=np.float64)
     parents = np.ascontiguousarray(tree.parents, dtype=np.int32)
@@ -712,7 +727,7 @@ def _step(op: int, tree: Tree, q, ctx: PlanContext):
     new_nodes = np.empty((cap_new, n))
     new_par = np.empty(cap_new, np.int32)
     st = np.zeros(_lib.ST_COUNT, np.uint64)
-    with dctx.lock:
+    with _bound(prob, ctx.options) as dctx:
         dctx.prepare(ctx.params.width)
         _lib.check(dctx.L.cprrtc_step(dctx.h, C.byref(prm), op, len(tree), _lib.ptr(nodes),
                                       _lib.ptr(parents, _lib._ip), _lib.ptr(q), _lib.ptr(res, _lib._ip),

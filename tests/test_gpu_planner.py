@@ -15,14 +15,11 @@ pytestmark = pytest.mark.gpu
 
 
 def _check_path(oracle, prob, res):
-    from paper_2505_06791_b200.planner import _derive, _bind, _params_struct, DeviceOptions, _SRC
+    from paper_2505_06791_b200.planner import derive_path
     m, sc, sp = prob.model, prob.scene, prob.spec
     assert np.array_equal(res.path[0], prob.start) and np.array_equal(res.path[-1], prob.goal)
     assert len(res.edge_sources) == len(res.path) - 1
-    ctx = _bind(prob, DeviceOptions())
-    prm = _params_struct(prob.params, DeviceOptions())
-    src = np.array([_SRC.index(s) for s in res.edge_sources], np.int32)
-    dense, ok = _derive(ctx, prm, np.stack(res.path), src)
+    dense, ok = derive_path(res, prob)
     assert ok.all()
     tau = np.inf if sp is None else sp.tau_task
     W = prob.params.width
@@ -149,6 +146,38 @@ def test_iteration_limit_and_unsolvable():
     assert res.status == "TimedOut" and 40.0 < res.stats.device_ms < 500.0
 
 
+def test_zero_budget_and_tree_capacity():
+    """time_budget_ms <= 0 times out before the first sample, like the
+    reference (planner.py:450-453: the budget check precedes iteration 1),
+    but endpoint errors still win; deterministic ignores the clock.  A full
+    tree ends the query as CapacityExceeded, never as a silent IterLimit."""
+    from paper_2505_06791_b200.errors import PlanSetupError
+    from paper_2505_06791_b200.geometry import Aabb, Scene
+    from paper_2505_06791_b200.planner import DeviceOptions, PlanParams, PlanProblem, plan
+    m, sc, sp = fx.robot("arm7"), fx.scene("table"), fx.spec("upright")
+    prs = fx.pairs()
+    s, g = prs["upright_start"][0], prs["upright_goal"][0]
+    for budget in (0.0, -5.0):
+        r = plan(PlanProblem(m, sc, sp, s, g, PlanParams(width=16, time_budget_ms=budget)))
+        assert r.status == "TimedOut" and r.path is None
+        assert r.stats.iterations == 0 and r.stats.extensions_attempted == 0
+    bad = s.copy()
+    bad[0] = 5.0
+    with pytest.raises(PlanSetupError, match="start violates joint limits"):
+        plan(PlanProblem(m, sc, sp, bad, g, PlanParams(width=16, time_budget_ms=0.0)))
+    r = plan(PlanProblem(m, sc, sp, s, g, PlanParams(width=16, time_budget_ms=0.0, deterministic=True,
+                                                     max_iterations=10**6)))
+    assert r.status in ("Solved", "IterLimit") and r.stats.iterations > 0
+    pl = fx.robot("planar2")
+    wall = Scene(boxes=[Aabb([0.2, -0.05, -0.1], [0.3, 0.05, 0.1]),
+                        Aabb([-0.3, -0.05, -0.1], [-0.2, 0.05, 0.1])])
+    res = plan(PlanProblem(pl, wall, None, np.array([np.pi / 2, 0.0]), np.array([-np.pi / 2, 0.0]),
+                           PlanParams(width=8, max_iterations=10**6, time_budget_ms=5000.0)),
+               DeviceOptions(tree_capacity=128))
+    assert res.status == "CapacityExceeded" and res.path is None
+    assert max(res.stats.nodes_start, res.stats.nodes_goal) == 128
+
+
 def test_plan_race_first_solution_flag(oracle):
     """cprrtc_plan_race on two independent contexts of one GPU (the flag
     mechanism of the multi-GPU race; distinct devices use peer stores): a
@@ -173,8 +202,7 @@ def test_every_dense_waypoint_collision_free_many_seeds(oracle):
     never validated themselves -- only their derived edges -- so the planner
     must check row 0 of every motion like validate_motion does.  A sweep of
     the window problem used to produce a colliding node in ~2 % of plans."""
-    from paper_2505_06791_b200.planner import (DeviceOptions, PlanParams, PlanProblem, _SRC, _bind, _derive,
-                                               _params_struct, plan)
+    from paper_2505_06791_b200.planner import PlanParams, PlanProblem, derive_path, plan
     p = next(x for x in fx.plans() if x["id"] == "window_line")
     m, sc = fx.robot(p["robot"]), fx.scene(p["scene"])
     sp = fx.spec(p["spec"])
@@ -188,9 +216,7 @@ def test_every_dense_waypoint_collision_free_many_seeds(oracle):
         if not res.solved:
             continue
         solved += 1
-        ctx = _bind(prob, DeviceOptions())
-        src = np.array([_SRC.index(s) for s in res.edge_sources], np.int32)
-        dense, ok = _derive(ctx, _params_struct(prob.params, DeviceOptions()), np.stack(res.path), src)
+        dense, ok = derive_path(res, prob)
         assert ok.all()
         for e in range(dense.shape[0]):   # every row of every edge, the nodes included
             v, *_ = oracle.validate_waypoints(dense[e], m.packed, sc.packed(), False)

@@ -1,13 +1,11 @@
-"""Host-side logic that needs no GPU: data model, YAML formats, segment
-construction, tree bookkeeping, path assembly and parameter validation."""
+"""Host-side logic that needs no GPU: data model, segment construction,
+tree bookkeeping, path assembly and parameter validation."""
 
 import numpy as np
 import pytest
 
 import fixtures as fx
-from paper_2505_06791_b200.errors import RobotFormatError, SceneFormatError
-from paper_2505_06791_b200.geometry import Aabb, Scene, Sphere, dump_scene, load_scene, scene_contains
-from paper_2505_06791_b200.kinematics import dump_robot, load_robot
+from paper_2505_06791_b200.geometry import Aabb, Scene, Sphere, scene_contains
 from paper_2505_06791_b200.planner import PlanParams, Tree, extract_path, steer
 from paper_2505_06791_b200.projection import (MotionSegment, ProjectionParams,
                                               interpolate_segment, segment_gaps)
@@ -80,30 +78,11 @@ def test_steer():
     assert np.array_equal(got, t) and got is not t
 
 
-def test_scene_yaml_round_trip_and_errors():
-    sc = fx.scene("table")
-    back = load_scene(dump_scene(sc))
-    assert np.array_equal(back.packed().box_min, sc.packed().box_min)
-    assert np.array_equal(back.packed().sph_radius, sc.packed().sph_radius)
-    with pytest.raises(SceneFormatError, match="unknown field"):
-        load_scene("name: x\nwalls: []\n")
-    with pytest.raises(SceneFormatError, match="max < min"):
-        load_scene("boxes:\n  - {min: [1, 0, 0], max: [0, 1, 1]}\n")
+def test_scene_queries_and_q_checks():
     assert scene_contains(Scene(boxes=[Aabb([0, 0, 0], [1, 1, 1])]), [0.5, 0.5, 1.0])
     assert not scene_contains(Scene(spheres=[Sphere([0, 0, 0], 0.5)]), [0.5, 0.1, 0])
-
-
-def test_robot_yaml_round_trip_and_errors():
-    m = fx.robot("arm8")
-    back = load_robot(dump_robot(m))
-    for k in ("origin_r", "axes", "sphere_local", "pairs", "lo"):
-        assert np.array_equal(getattr(back.packed, k), getattr(m.packed, k))
-    with pytest.raises(RobotFormatError, match="joints"):
-        load_robot("name: x\njoints: []\n")
-    with pytest.raises(RobotFormatError, match="unknown field"):
-        load_robot("name: x\nlinks: 3\njoints: [{axis: [0,0,1], limits: [-1, 1]}]\n")
     with pytest.raises(ValueError):
-        m.check_q(np.zeros(3))
+        fx.robot("arm8").check_q(np.zeros(3))
 
 
 def test_plan_race_argument_checks():
