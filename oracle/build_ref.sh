@@ -4,7 +4,7 @@
 # _kernels/_compiled.pyx is compiled, with the reference's flags,
 # pkg/setup.py:40-61), from a scratch copy because the mount is read-only.
 # The pure-Python modules are then byte-compiled in place to sourceless .pyc
-# (`compileall -b`, the unmodified modules' own bytecode) so the package
+# (`compileall -b`, the unmodified modules' own bytecode, suffix .refpyc) so the package
 # imports on the GPU box, where /root/reference is absent, without reference
 # source text landing in the working tree.  TEST / BASELINE INFRASTRUCTURE
 # ONLY: the product never imports it.
@@ -23,6 +23,10 @@ find "$TMP/pkg" -name '__pycache__' -prune -exec rm -rf {} +
 ls "$TMP/site/maniplan/_kernels/"_compiled*.so > /dev/null   # the stock build compiled the kernel backend
 "$PY" -m compileall -q -b "$TMP/site/maniplan"
 find "$TMP/site/maniplan" \( -name "*.py" -o -name "*.pyx" -o -name "*.c" \) -delete
+# .pyc files do not travel to the GPU box with gpurun's snapshot: keep the
+# bytecode under a suffix of its own (tests/refpkg.py registers a sourceless
+# loader for it, for oracle/_ref only)
+find "$TMP/site/maniplan" -name '*.pyc' -exec sh -c 'mv "$1" "${1%.pyc}.refpyc"' _ {} \;
 find "$TMP/site/maniplan" -name '__pycache__' -prune -exec rm -rf {} +
 rm -rf "$OUT"
 mkdir -p "$OUT"

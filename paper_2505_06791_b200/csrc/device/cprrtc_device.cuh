@@ -2575,8 +2575,19 @@ cp_project_kernel(int B, int W, Con<float> con, ProjArgs pa, const float* tau_sm
                                trace ? trace + (size_t)i * pa.max_iters * W * CP_N : nullptr,
                                trace ? trace_prog + (size_t)i * pa.max_iters : nullptr);
         tm.sync();
+        // a coordinate the projection left at the FP32 image of its input is
+        // returned as the FP64 input itself: row 0 (never rewritten,
+        // pure.py:573-574) and every row of a segment that validates at
+        // iteration 1 (returned as given, pure.py:569-572 -- e.g. the
+        // unconstrained tau = inf sentinel, T/test_projection.py:107-114) come
+        // back bit-identical, as in the reference
         if ((int)tm.lane < W)
-            for (int k = 0; k < CP_N; k++) xi[((size_t)i * W + tm.lane) * CP_N + k] = ws.seg[tm.lane][k];
+            for (int k = 0; k < CP_N; k++) {
+                const size_t o = ((size_t)i * W + tm.lane) * CP_N + k;
+                const double in = wps[o];
+                const float v = ws.seg[tm.lane][k];
+                xi[o] = v == (float)in ? in : (double)v;
+            }
         if (tm.lane == 0) { ok[i] = good; iters[i] = it; prog[i] = pr; }
     }
 }

@@ -195,6 +195,8 @@ def test_projection_contract(K, oracle):
     k = fx.kats()
     keys = sorted({key[5:-4] for key in k if key.startswith("proj_") and key.endswith("_wps")})
     agree = total = 0
+    from collections import Counter
+    cat = Counter()
     for key in keys:
         parts = key.split("_")
         rname, mode = parts[0], int(parts[-1][1:])
@@ -204,15 +206,27 @@ def test_projection_contract(K, oracle):
         taus = k[f"proj_{key}_tausm"]
         r = K.project_batch(m, sp, wps, sp.tau_task, taus, 0.1, 1e-3, 128, mode)
         for i in range(len(wps)):
-            assert np.array_equal(r["xi"][i][0], wps[i][0].astype(np.float32))
+            assert np.array_equal(r["xi"][i][0], wps[i][0])   # row 0 is returned as given
             if r["ok"][i] and mode != 1:   # literal-gap vouches only for the end (T/test_projection.py:285)
                 lo, hi = m.packed.lo, m.packed.hi
                 # rows >= 1 are clamped inside the limits; row 0 is the input start
                 assert (r["xi"][i][1:] >= lo).all() and (r["xi"][i][1:] <= hi).all()
                 assert _fp64_projection_ok(oracle, m, sp, r["xi"][i], sp.tau_task, taus[i]), (key, i)
-            agree += int(bool(r["ok"][i]) == bool(k[f"proj_{key}_ok"][i]))
+            dev, ref = bool(r["ok"][i]), bool(k[f"proj_{key}_ok"][i])
+            cat[(dev, ref)] += 1
+            agree += int(dev == ref)
             total += 1
-    assert agree >= 0.85 * total, (agree, total)
+    # disagreements by direction: FP32 fails where the FP64 reference
+    # projects (the device's inward safety margins) vs
+    # FP32 projects where FP64 fails (every such segment passed the FP64
+    # re-check above, so it is a sound projection the reference missed)
+    print(f"\nprojection outcome agreement {agree}/{total} = {agree / total:.3f}; "
+          f"device fail / reference ok {cat[(False, True)]}, device ok / reference fail {cat[(True, False)]}, "
+          f"both ok {cat[(True, True)]}, both fail {cat[(False, False)]}")
+    # measured on B200 (r2): 203/216 = 0.940, all 13 disagreements "device fails
+    # where FP64 projects" (the FP32 margins), none the other way
+    assert agree >= 0.92 * total, (agree, total)
+    assert cat[(True, False)] <= 0.01 * total
 
 
 def test_unconstrained_projection_is_identity(K):
@@ -222,7 +236,7 @@ def test_unconstrained_projection_is_identity(K):
     wps = np.stack([np.linspace(qs[2 * i], qs[2 * i + 1], 16) for i in range(20)])
     r = K.project_batch(m, unconstrained(), wps, np.inf, None)
     assert r["ok"].all() and (r["iters"] == 1).all()
-    assert np.array_equal(r["xi"], wps.astype(np.float32).astype(np.float64))
+    assert np.array_equal(r["xi"], wps)   # bit-identical, like the reference (T/test_projection.py:107-114)
 
 
 def test_projection_trace_invariants(K):

@@ -216,6 +216,8 @@ def test_extend_outcomes_match_reference(oracle, spec_name, scene_name):
         root = prs[("upright" if spec_name == "upright" else "table_plane") + "_start"][3]
     samples = kernels.halton_batch(m, 60, 1, 777)
     agree = close = both = 0
+    from collections import Counter
+    diff = Counter()
     for q in samples:
         ctx = _ctx(m, sc, sp, width=16)
         tree = Tree(root, "start")
@@ -223,8 +225,14 @@ def test_extend_outcomes_match_reference(oracle, spec_name, scene_name):
         reason, q_end = _ref_extend(oracle, m, sc, sp, root, q)
         dev = None if out.added else out.reason
         agree += dev == reason
+        if dev != reason:
+            diff[f"device {dev or 'added'} / reference {reason or 'added'}"] += 1
         if out.added and reason is None:
             both += 1
             close += np.abs(tree.node(1) - q_end).max() < 2e-3
-    assert agree >= 0.9 * len(samples), agree
-    assert both >= 5 and close >= 0.9 * both, (both, close)
+    print(f"\nextend outcome agreement ({spec_name}, {scene_name}) {agree}/{len(samples)}; "
+          f"same node (2e-3) {close}/{both}; disagreements {dict(diff)}")
+    # measured on B200 (r2): 60/60 outcomes and every common node within 2e-3
+    # on all four (spec, scene) cases
+    assert agree >= 0.95 * len(samples), agree
+    assert both >= 5 and close >= 0.95 * both, (both, close)
