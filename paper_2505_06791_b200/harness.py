@@ -22,7 +22,7 @@ from . import kernels
 from .sampling import trial_seed_offset
 
 __all__ = ["generate_pairs", "generate_pair", "TrialRecord", "CSV_COLUMNS", "run_trials",
-           "write_records", "read_records", "emit_cdf", "summarize", "PAIR_SEED_BASE"]
+           "write_records", "read_records", "emit_cdf", "write_cdfs", "summarize", "PAIR_SEED_BASE"]
 
 PAIR_SEED_BASE = 500_000_000      # pair streams sit far above planner streams
 PAIR_MAX_DRAWS = 4000
@@ -131,57 +131,85 @@ def run_trials(problems, trials: int = 1, base_offset: int = 0, projection=None,
     return recs
 
 
-def write_records(path, records):
+def write_records(records, path):
+    """records.csv in the reference's column order (bench.py:72-109, 466-472)."""
     with open(path, "w", newline="") as fh:
         w = csv.writer(fh)
         w.writerow(CSV_COLUMNS)
-        for r in records:
-            w.writerow(r.row())
+        w.writerows(r.row() for r in records)
 
 
-def read_records(path):
-    with open(path, newline="") as fh:
-        rows = list(csv.reader(fh))
-    if not rows or rows[0] != CSV_COLUMNS:
-        raise ValueError(f"{path}: not a records file")
-    return [TrialRecord.from_row(r) for r in rows[1:]]
+def read_records(source):
+    """write_records' inverse; a path or an open text stream (bench.py:475-492)."""
+    def parse(fh):
+        rows = csv.reader(fh)
+        head = next(rows, None)
+        if head != CSV_COLUMNS:
+            from .errors import ProblemFormatError
+            raise ProblemFormatError(f"unexpected CSV header: {head}")
+        return [TrialRecord.from_row(r) for r in rows if r]
+    if hasattr(source, "read"):
+        return parse(source)
+    with open(source, newline="") as fh:
+        return parse(fh)
 
 
-def emit_cdf(records):
-    """[(t_ms, fraction solved by t)] over all records (solution-time CDF)."""
-    n = len(records)
-    if n == 0:
-        return []
-    times = sorted(r.wall_ms for r in records if r.status == "Solved")
-    return [(t, (i + 1) / n) for i, t in enumerate(times)]
+GROUP_KEYS = ("projection", "cc_flag", "densify")
 
 
-def summarize(records):
-    """Per (problem, projection, cc_flag, densify): success rate, mean/median
-    solved time, mean checks saved on colliding work."""
-    groups = {}
+def _groups(records, keys):
+    """{group key tuple: [records]} in sorted key order (bench.py:499-501)."""
+    out: dict = {}
     for r in records:
-        groups.setdefault((r.problem, r.projection, r.cc_flag, r.densify), []).append(r)
+        out.setdefault(tuple(getattr(r, k) for k in keys), []).append(r)
+    return dict(sorted(out.items(), key=lambda kv: kv[0]))
+
+
+def _label(key) -> str:
+    return "_".join(map(str, key))
+
+
+def emit_cdf(records, keys=GROUP_KEYS):
+    """{group label: [(wall_ms, fraction of the group's trials solved by
+    then)]}; the fraction's denominator is every trial of the group, so a
+    group with failures tops out below 1 (bench.py:489-504)."""
     out = {}
-    for k, rs in groups.items():
-        solved = [r.wall_ms for r in rs if r.status == "Solved"]
-        saved = [1.0 - r.checks_performed / r.checks_possible for r in rs
-                 if r.checks_possible > 0 and r.checks_performed < r.checks_possible]
-        out[k] = {"trials": len(rs), "success_rate": len(solved) / len(rs),
-                  "mean_ms": float(np.mean(solved)) if solved else None,
-                  "median_ms": float(np.median(solved)) if solved else None,
-                  "checks_saved": float(np.mean(saved)) if saved else 0.0}
+    for key, rs in _groups(records, keys).items():
+        t = np.sort(np.array([r.wall_ms for r in rs if r.status == "Solved"], dtype=float))
+        out[_label(key)] = [(float(x), (k + 1) / len(rs)) for k, x in enumerate(t)]
     return out
 
 
-def write_cdfs(out_dir, records):
+def write_cdfs(records, out_dir, keys=GROUP_KEYS):
+    """One cdf_<group>.csv (time_ms, fraction_solved) per group; returns the
+    paths (bench.py:507-519)."""
     os.makedirs(out_dir, exist_ok=True)
-    groups = {}
-    for r in records:
-        groups.setdefault(r.problem, []).append(r)
-    for name, rs in groups.items():
-        with open(os.path.join(out_dir, f"cdf_{name.replace('#', '_')}.csv"), "w", newline="") as fh:
+    paths = []
+    for label, pts in emit_cdf(records, keys).items():
+        path = os.path.join(out_dir, f"cdf_{label}.csv")
+        with open(path, "w", newline="") as fh:
             w = csv.writer(fh)
             w.writerow(["time_ms", "fraction_solved"])
-            for t, f in emit_cdf(rs):
-                w.writerow([repr(t), repr(f)])
+            w.writerows([repr(t), repr(f)] for t, f in pts)
+        paths.append(path)
+    return paths
+
+
+def summarize(records, keys=GROUP_KEYS):
+    """{group label: trials, solved, success_rate, and when defined
+    mean_wall_ms / median_wall_ms (solved trials) and mean_checks_saved (trials
+    where the early-exit flag skipped work)} (bench.py:522-552)."""
+    out = {}
+    for key, rs in _groups(records, keys).items():
+        t = sorted(r.wall_ms for r in rs if r.status == "Solved")
+        e = {"trials": len(rs), "solved": len(t), "success_rate": len(t) / len(rs)}
+        if t:
+            e["mean_wall_ms"] = sum(t) / len(t)
+            h = len(t) // 2
+            e["median_wall_ms"] = t[h] if len(t) % 2 else 0.5 * (t[h - 1] + t[h])
+        saved = [1.0 - r.checks_performed / r.checks_possible for r in rs
+                 if r.checks_possible and r.checks_performed < r.checks_possible]
+        if saved:
+            e["mean_checks_saved"] = sum(saved) / len(saved)
+        out[_label(key)] = e
+    return out

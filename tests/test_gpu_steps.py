@@ -148,7 +148,7 @@ def test_trial_records_round_trip(tmp_path):
              for i in range(3)]
     recs = run_trials(probs, trials=2)
     assert len(recs) == 6 and all(r.status == "Solved" for r in recs)
-    write_records(tmp_path / "records.csv", recs)
+    write_records(recs, tmp_path / "records.csv")
     back = read_records(tmp_path / "records.csv")
     assert [r.row() for r in back] == [r.row() for r in recs]
     summ = summarize(recs)
