@@ -32,6 +32,7 @@ import ctypes as C
 import math
 import time
 from contextlib import contextmanager
+from collections.abc import Sequence
 from dataclasses import dataclass, field, replace
 
 import numpy as np
@@ -47,7 +48,7 @@ __all__ = [
     "Tree", "PlanParams", "PlanProblem", "PlanResult", "PlanStats", "PlanContext",
     "ExtendOutcome", "ConnectOutcome", "DeviceOptions", "nearest", "steer", "plan",
     "plan_batch", "extract_path", "derive_edge", "derive_path", "revalidate_path", "dense_path", "extend",
-    "connect", "prepare", "plan_race",
+    "connect", "prepare", "plan_race", "plan_many", "BatchResult",
 ]
 
 
@@ -337,79 +338,188 @@ def prepare(problem: PlanProblem, options: DeviceOptions = DeviceOptions()):
     return ctx
 
 
+class BatchResult(Sequence):
+    """Columnar results of one batched launch (plan_many / plan_batch).
+
+    The arrays are the decoded device output: ``codes`` (B,) int (0 Solved,
+    1 TimedOut, 2 IterLimit, 3 CapacityExceeded, 5 Stopped, -1 setup error),
+    ``setup_codes``, ``path_len``, ``nodes`` (B, 2), ``device_ms``, ``stats``
+    (B, ST_COUNT) and the path rows (B, max path length, n) with their edge
+    sources.  Indexing gives the reference's PlanResult, built on first access
+    (a 1024-query batch costs ~5 ms of Python object construction when every
+    result is materialised, several times the launch itself)."""
+
+    def __init__(self, a, rows, sources, starts, goals, wall_ms, single):
+        self.codes = a["status"].copy()
+        self.setup_codes = a["setup_code"].copy()
+        self.path_len = np.where(self.codes == 0, a["path_len"], 0)
+        self.nodes = np.stack([a["ns"], a["ng"]], axis=1)
+        self.device_ms = a["device_ms"].copy()
+        self.stats = a["stats"].copy()
+        self.rows, self.sources = rows, sources
+        self.starts, self.goals = starts, goals
+        self.wall_ms = wall_ms
+        self._single = single
+        self._cache: dict = {}
+
+    def __len__(self):
+        return self.codes.shape[0]
+
+    @property
+    def solved(self) -> np.ndarray:
+        return self.codes == 0
+
+    @property
+    def status(self) -> list:
+        return [_status_name(int(c)) for c in self.codes]
+
+    def path(self, i: int) -> np.ndarray:
+        """(L, n) path of query i; the roots are the exact FP64 endpoints."""
+        L = int(self.path_len[i])
+        out = np.array(self.rows[i, :L])
+        if L:
+            out[0], out[-1] = self.starts[i], self.goals[i]
+        return out
+
+    def __getitem__(self, i):
+        if isinstance(i, slice):
+            return [self[k] for k in range(*i.indices(len(self)))]
+        i = range(len(self))[i]
+        r = self._cache.get(i)
+        if r is None:
+            r = self._cache[i] = self._build(i)
+        return r
+
+    def _build(self, i):
+        s = self.stats[i].tolist()
+        stats = PlanStats(s[0], s[1], s[2], s[3], s[4], s[5], s[6], self.wall_ms, int(self.nodes[i, 0]),
+                          int(self.nodes[i, 1]), float(self.device_ms[i]), s[8], s[9], s[10], s[11])
+        code = int(self.codes[i])
+        if code == 0:
+            L = int(self.path_len[i])
+            return _solved(tuple(self.path(i)), tuple(map(_SRC.__getitem__, self.sources[i, :L - 1].tolist())),
+                           stats)
+        if code == -1:
+            if self._single:
+                raise PlanSetupError(_SETUP.get(int(self.setup_codes[i]), "invalid start/goal"))
+            return PlanResult("Error:PlanSetupError", None, None, stats)
+        return PlanResult(_status_name(code), None, None, stats)
+
+
+def _status_name(code: int) -> str:
+    return "Error:PlanSetupError" if code == -1 else _STATUS.get(code, "IterLimit")
+
+
+def plan_many(model, scene, spec, starts, goals, seed_offsets, params: PlanParams = PlanParams(),
+              options: DeviceOptions = DeviceOptions(), devices=None) -> BatchResult:
+    """Plan B independent queries of one (model, scene, spec, params) in one
+    persistent launch (per device): starts / goals (B, n), seed_offsets (B,).
+    The columnar form of plan_batch -- no per-query Python objects on the way
+    in or out.  ``devices`` (e.g. ``range(8)``) shards the batch into
+    contiguous slices, one persistent launch per device, all launched before
+    any is awaited (cprrtc_plan_multi; no collective).  A device may repeat
+    (independent contexts on one GPU)."""
+    like = _Like(model, scene, spec, params)
+    starts = np.ascontiguousarray(starts, dtype=np.float64)
+    goals = np.ascontiguousarray(goals, dtype=np.float64)
+    seeds = np.ascontiguousarray(seed_offsets, dtype=np.int64)
+    B = starts.shape[0]
+    n = model.n
+    if starts.shape != (B, n) or goals.shape != (B, n) or seeds.shape != (B,):
+        raise ValueError(f"starts / goals must be (B, {n}) and seed_offsets (B,)")
+    if B == 0:
+        raise ValueError("empty batch")
+    if (seeds < 0).any():
+        raise ValueError("seed_offset must be >= 0")
+    prm = _params_struct(params, options)
+    res = (_lib.Result * B)()
+    pc = int(prm.path_capacity)
+    paths, srcs = _out_buffers(B, pc, n)
+    devs = tuple(int(d) for d in devices) if devices is not None else ()
+    if len(devs) > 1:
+        with _bound_many(like, devs) as ctxs:
+            handles = (C.c_void_p * len(ctxs))(*[c.h.value for c in ctxs])
+            t0 = time.perf_counter()
+            _lib.check(ctxs[0].L.cprrtc_plan_multi(handles, len(ctxs), C.byref(prm), B, _lib.ptr(starts),
+                                                   _lib.ptr(goals), _lib.ptr(seeds, _lib._lp), res,
+                                                   _lib.ptr(paths), _lib.ptr(srcs, _lib._ip)), "plan_multi")
+            wall = (time.perf_counter() - t0) * 1e3
+    else:
+        opt = options if not devs else replace(options, device=devs[0])
+        with _bound(like, opt) as ctx:
+            ctx.prepare(params.width)
+            t0 = time.perf_counter()
+            _lib.check(ctx.L.cprrtc_plan(ctx.h, C.byref(prm), B, _lib.ptr(starts), _lib.ptr(goals),
+                                         _lib.ptr(seeds, _lib._lp), res, _lib.ptr(paths),
+                                         _lib.ptr(srcs, _lib._ip)), "plan")
+            wall = (time.perf_counter() - t0) * 1e3
+    a = np.frombuffer(res, dtype=_RESULT_DT)
+    if (a["status"] == 4).any():
+        raise RuntimeError(f"solution path longer than path_capacity={pc}")
+    lmax = int(a["path_len"][a["status"] == 0].max(initial=0))
+    # the rows and sources leave the reused output buffers (one copy)
+    return BatchResult(a, np.array(paths[:, :lmax]), np.array(srcs[:, :max(lmax - 1, 0)]), starts, goals,
+                       wall, single=(B == 1))
+
+
+class _Like:
+    """The (model, scene, spec, params) a context is bound to."""
+
+    __slots__ = ("model", "scene", "spec", "params")
+
+    def __init__(self, model, scene, spec, params):
+        self.model, self.scene, self.spec, self.params = model, scene, spec, params
+
+
 def plan_batch(problems, options: DeviceOptions = DeviceOptions(), return_dense: bool = False,
                devices=None):
-    """Plan many independent queries in one persistent launch.
+    """Plan many independent queries in one persistent launch (plan_many on
+    the problems' starts, goals and seeds).
 
     All problems must share model, scene, spec and params (apart from
-    start, goal and params.seed_offset).  Returns a list of PlanResult; a bad
-    start/goal raises PlanSetupError for that problem only if it is the sole
-    problem, else the result carries status 'Error:PlanSetupError'.
-    ``devices`` (e.g. ``range(8)``) shards the batch into contiguous slices,
-    one persistent launch per device, all launched before any is awaited
-    (cprrtc_plan_multi; no collective).  A device may repeat (independent
-    contexts on one GPU).
+    start, goal and params.seed_offset).  Returns a BatchResult (a sequence
+    of PlanResult, built lazily); a bad start/goal raises PlanSetupError for
+    that problem only if it is the sole problem, else its result carries
+    status 'Error:PlanSetupError'.  ``devices``: as for plan_many.
     """
     problems = list(problems)
     if not problems:
         return []
     p0 = problems[0]
     if len(problems) > 1:
-        base = _params_key(p0.params)
+        key = _params_getter()
+        base = key(p0.params)
         for p in problems[1:]:
             if (p.model is not p0.model or p.scene is not p0.scene or p.spec is not p0.spec
-                    or (p.params is not p0.params and _params_key(p.params) != base)):
+                    or (p.params is not p0.params and key(p.params) != base)):
                 raise ValueError("plan_batch problems must share model, scene, spec and params")
-    prm = _params_struct(p0.params, options)
-    ctx = kernels.context(p0.model, options.device)
-    n = ctx.n
-    B = len(problems)
-    starts = np.ascontiguousarray(np.stack([p.start for p in problems]), dtype=np.float64)
-    goals = np.ascontiguousarray(np.stack([p.goal for p in problems]), dtype=np.float64)
-    seeds = np.array([int(p.params.seed_offset) for p in problems], dtype=np.int64)
-    if (seeds < 0).any():
-        raise ValueError("seed_offset must be >= 0")
-    res = (_lib.Result * B)()
-    pc = int(prm.path_capacity)
-    paths, srcs = _out_buffers(B, pc, n)
-    devs = tuple(int(d) for d in devices) if devices is not None else ()
-    if len(devs) > 1:
-        with _bound_many(p0, devs) as ctxs:
-            handles = (C.c_void_p * len(ctxs))(*[c.h.value for c in ctxs])
-            t0 = time.perf_counter()
-            _lib.check(ctx.L.cprrtc_plan_multi(handles, len(ctxs), C.byref(prm), B, _lib.ptr(starts),
-                                               _lib.ptr(goals), _lib.ptr(seeds, _lib._lp), res,
-                                               _lib.ptr(paths), _lib.ptr(srcs, _lib._ip)), "plan_multi")
-            wall = (time.perf_counter() - t0) * 1e3
-    else:
-        with _bound(p0, options) as ctx:
-            ctx.prepare(p0.params.width)
-            t0 = time.perf_counter()
-            _lib.check(ctx.L.cprrtc_plan(ctx.h, C.byref(prm), B, _lib.ptr(starts), _lib.ptr(goals),
-                                         _lib.ptr(seeds, _lib._lp), res, _lib.ptr(paths),
-                                         _lib.ptr(srcs, _lib._ip)), "plan")
-            wall = (time.perf_counter() - t0) * 1e3
-    out = _results_bulk(res, problems, paths, srcs, wall, pc)
+    out = plan_many(p0.model, p0.scene, p0.spec, np.stack([p.start for p in problems]),
+                    np.stack([p.goal for p in problems]), [int(p.params.seed_offset) for p in problems],
+                    p0.params, options, devices)
     if return_dense:
+        out = list(out)
+        prm = _params_struct(p0.params, options)
         with _bound(p0, options) as ctx:
             for i, r in enumerate(out):
-                if r.solved:
-                    L = len(r.path)
-                    dense, ok = _derive(ctx, prm, paths[i, :L], srcs[i, :L - 1])
+                if r.solved and len(r.path) > 1:
+                    src = np.array([_SRC.index(x) for x in r.edge_sources], np.int32)
+                    dense, ok = _derive(ctx, prm, np.stack(r.path), src)
                     out[i] = replace(r, dense=dense)
     return out
 
 
-_PARAM_FIELDS = None
+_PARAMS_GETTER = None
 
 
-def _params_key(p) -> tuple:
-    """PlanParams fields except seed_offset (plan_batch consistency check)."""
-    global _PARAM_FIELDS
-    if _PARAM_FIELDS is None:
+def _params_getter():
+    """PlanParams fields except seed_offset, as one C-level attrgetter
+    (plan_batch's consistency check)."""
+    global _PARAMS_GETTER
+    if _PARAMS_GETTER is None:
         from dataclasses import fields
-        _PARAM_FIELDS = tuple(f.name for f in fields(PlanParams) if f.name != "seed_offset")
-    return tuple(getattr(p, f) for f in _PARAM_FIELDS)
+        from operator import attrgetter
+        _PARAMS_GETTER = attrgetter(*(f.name for f in fields(PlanParams) if f.name != "seed_offset"))
+    return _PARAMS_GETTER
 
 
 _RESULT_DT = np.dtype({"names": ["status", "setup_code", "path_len", "ns", "ng", "device_ms", "stats"],
@@ -448,41 +558,6 @@ def _result_one(r, p, paths_i, srcs_i, wall, pc) -> "PlanResult":
     if code == 4:
         raise RuntimeError(f"solution path longer than path_capacity={pc}")
     return PlanResult(_STATUS.get(code, "IterLimit"), None, None, stats)
-
-
-def _results_bulk(res, problems, paths, srcs, wall, pc):
-    """PlanResults of a batch: one structured numpy view of the result array
-    and bulk conversions instead of per-field ctypes access."""
-    a = np.frombuffer(res, dtype=_RESULT_DT)
-    status = a["status"].tolist()
-    plen = a["path_len"].tolist()
-    ns, ng, dms = a["ns"].tolist(), a["ng"].tolist(), a["device_ms"].tolist()
-    st = a["stats"].tolist()
-    # one copy of every returned row (the per-query paths are views of it)
-    lmax = max(plen) if plen else 0
-    rows = np.array(paths[:, :lmax]) if lmax else paths[:, :0]
-    src_of = _SRC.__getitem__
-    out = []
-    for i, p in enumerate(problems):
-        s = st[i]
-        stats = PlanStats(s[0], s[1], s[2], s[3], s[4], s[5], s[6], wall, ns[i], ng[i], dms[i],
-                          s[8], s[9], s[10], s[11])
-        code = status[i]
-        if code == 0:
-            L = plen[i]
-            path = list(rows[i, :L])
-            path[0] = p.start.copy()                 # roots are the exact FP64 endpoints
-            path[-1] = p.goal.copy()
-            out.append(_solved(tuple(path), tuple(map(src_of, srcs[i, :L - 1].tolist())), stats))
-        elif code == -1:
-            if len(problems) == 1:
-                raise PlanSetupError(_SETUP.get(int(a["setup_code"][0]), "invalid start/goal"))
-            out.append(PlanResult("Error:PlanSetupError", None, None, stats))
-        elif code == 4:
-            raise RuntimeError(f"solution path longer than path_capacity={pc}")
-        else:
-            out.append(PlanResult(_STATUS.get(code, "IterLimit"), None, None, stats))
-    return out
 
 
 def _result(r, p, paths_i, srcs_i, wall, B, pc) -> PlanResult:
