@@ -354,7 +354,7 @@ def run_b200(args, world, rank, local):
                      "peak": fp32_peak, "unit": "TFLOP/s", "frac": achieved / fp32_peak,
                      "population": f"{len(solved)} solved queries (the headline's); "
                                    f"{len(all_recs) - len(solved)} unsolved queries ran the full budget and "
-                                   f"took {100 * (1 - kern_s / kern_all) if kern_all else 0:.1f} % of the "
+                                   f"took {100 * (1 - kern_s / kern_all) if kern_all else 0:.2f} % of the "
                                    "kernel time",
                      "peak_source": f"nominal FP32 FMA ({sms} SM x 128 lanes x 2 x {max_mhz} MHz); "
                                     "MEASURED_PEAKS.json has no FP32 entry",
@@ -730,9 +730,10 @@ def cpu_arms(args, line, recs):
             "sample": f"the {BATCH} configs[4] queries of the first timed step, reference plan() on {cores} "
                       f"processes ({el:.1f} s)"}
         # CC checks/s: validate_waypoints on one core
-        done, secs = ex.submit(_ref_cc_job, (48, 16)).result()
+        done, secs = ex.submit(_ref_cc_job, (args.cpu_cc_motions, 16)).result()
         line["cpu_cc_checks_per_s"] = {"value": done / secs, "unit": "checks/s", "cores": 1,
-                                       "sample": f"48 motions x 16 waypoints vs the 999-box shelf, flag off, "
+                                       "sample": f"{args.cpu_cc_motions} motions x 16 waypoints vs the 999-box "
+                                                 "shelf, flag off, "
                                                  f"reference _compiled.validate_waypoints ({secs:.1f} s)"}
     line["cpu_arms_s"] = time.perf_counter() - t_all
     write_trial_records(args, line, recs, head, res1)
@@ -835,7 +836,9 @@ def main():
     ap.add_argument("--cc-broadphase", type=int, default=-1,
                     help="planner CC: 1 clustered broad phase, 0 reference lockstep order, -1 auto")
     ap.add_argument("--budget-ms", type=float, default=2000.0)
-    ap.add_argument("--cpu-queries", type=int, default=20)
+    ap.add_argument("--cpu-queries", type=int, default=100,
+                    help="reference configs[1] sample: the first K timed GPU queries")
+    ap.add_argument("--cpu-cc-motions", type=int, default=2000)
     ap.add_argument("--records-dir", default=os.path.join(ROOT, "bench_records"))
     ap.add_argument("--no-extras", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
