@@ -1484,16 +1484,28 @@ __device__ __forceinline__ int cp_append(const Team& tm, const PlanArgs& A, Quer
         if (tm.lane == 0) { atomicExch(&Q.overflow, 1); atomicExch(&Q.stop, 1); }
         return -1;
     }
-    // publication order: the parent, then (behind lane 0's fence) coordinate
-    // 0, which lane 0 stores itself.  A node counts as present only once every
+    // publication order: the parent, then coordinate 0, which lane 0 stores
+    // itself with release semantics (ordered after its parent store).  A node counts as present only once every
     // coordinate is non-NaN, so whoever sees it (NN scan, connect, extraction
     // after its own fence) also sees its parent -- the reset kernel never
     // clears parents[], so a stale parent would otherwise be readable.
+#ifndef CP_APPEND_ORDER
+#define CP_APPEND_ORDER 2   // 2: coordinate 0 by st.release; 1: __threadfence; 0: unordered (A/B only)
+#endif
+    float* row = cp_tree(A, qi, k) + idx;
     if (tm.lane == 0) {
         cp_par(A, qi, k)[idx] = par;
+#if CP_APPEND_ORDER == 2
+        asm volatile("st.release.gpu.global.f32 [%0], %1;" :: "l"(row), "f"(q[0]) : "memory");
+#else
+#if CP_APPEND_ORDER == 1
         __threadfence();
+#endif
+        row[0] = q[0];
+#endif
+    } else if ((int)tm.lane < CP_N) {
+        row[(size_t)tm.lane * A.cap] = q[tm.lane];
     }
-    if ((int)tm.lane < CP_N) cp_tree(A, qi, k)[(size_t)tm.lane * A.cap + idx] = q[tm.lane];
     tm.sync();
     return idx;
 }
