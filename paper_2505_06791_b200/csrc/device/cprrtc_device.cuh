@@ -694,11 +694,18 @@ __device__ __forceinline__ void cp_alg1_loop(const Team tm, int W, const ProjArg
 // the projection is abandoned (returns false with *iters_out = -1) so a team
 // that lost the race leaves within two iterations instead of finishing its
 // projection.
-__device__ __noinline__ bool cp_project(const Team tm, float (*seg)[CP_NP], int W,
-                           const ProjArgs pa, int* iters_out, int* prog_out,
-                           float* trace = nullptr, int* trace_prog = nullptr,
-                           unsigned long long* n_stage1 = nullptr, const int* stop_flag = nullptr,
-                           int* poll_slot = nullptr) {
+// The outcome travels back in registers (a struct return of the out-of-line
+// body; cp_project below is the inline adapter): out-pointers into the
+// caller's frame would pin its locals in local memory.
+struct ProjRes {
+    bool ok;
+    int iters, prog;   // iters < 0: abandoned (the query is over)
+    unsigned s1;       // stage-1 evaluations
+};
+
+__device__ __noinline__ ProjRes cp_project_body(const Team tm, float (*seg)[CP_NP], int W, const ProjArgs pa,
+                                                float* trace, int* trace_prog, const int* stop_flag,
+                                                int* poll_slot) {
     unsigned s1 = 0;
     const int t = (int)tm.lane;
     const bool row = t < W;
@@ -787,12 +794,7 @@ __device__ __noinline__ bool cp_project(const Team tm, float (*seg)[CP_NP], int 
             for (int k = 0; k < CP_N; k++) seg[t][k] = xc[k];
         }
         tm.sync();
-        if (aborted) {
-            *iters_out = -1;
-            *prog_out = prog;
-            if (n_stage1) *n_stage1 += __reduce_add_sync(tm.mask, s1);
-            return false;
-        }
+        if (aborted) return ProjRes{false, -1, prog, __reduce_add_sync(tm.mask, s1)};
     }
     if (ok) {
         // clamp to limits; if anything moved, re-check both tolerances
@@ -816,7 +818,7 @@ __device__ __noinline__ bool cp_project(const Team tm, float (*seg)[CP_NP], int 
             }
             tm.sync();
             if (row) {
-                good = cp_err_norm(qc) < pa.tau_task_dev;
+                good = cp_err_norm(seg[t]) < pa.tau_task_dev;   // the clamped row, from shared memory
                 if (t >= 1) {
                     float s2 = 0.f;
 #pragma unroll
@@ -838,10 +840,18 @@ __device__ __noinline__ bool cp_project(const Team tm, float (*seg)[CP_NP], int 
     } else {
         iters = pa.max_iters;
     }
-    *iters_out = iters;
-    *prog_out = prog;
-    if (n_stage1) *n_stage1 += __reduce_add_sync(tm.mask, s1);
-    return ok;
+    return ProjRes{ok, iters, prog, __reduce_add_sync(tm.mask, s1)};
+}
+
+__device__ __forceinline__ bool cp_project(const Team tm, float (*seg)[CP_NP], int W, const ProjArgs pa,
+                                           int* iters_out, int* prog_out, float* trace = nullptr,
+                                           int* trace_prog = nullptr, unsigned long long* n_stage1 = nullptr,
+                                           const int* stop_flag = nullptr, int* poll_slot = nullptr) {
+    const ProjRes r = cp_project_body(tm, seg, W, pa, trace, trace_prog, stop_flag, poll_slot);
+    *iters_out = r.iters;
+    *prog_out = r.prog;
+    if (n_stage1) *n_stage1 += r.s1;
+    return r.ok;
 }
 
 // ---------------------------------------------------------------------------
@@ -876,6 +886,70 @@ __device__ __forceinline__ bool cp_hit_sph(float cx, float cy, float cz, float r
     return fmaf(dx, dx, fmaf(dy, dy, dz * dz)) < rr * rr;
 }
 
+// Packed FP32x2 arithmetic (sm_100a FADD2 / FMUL2 / FFMA2: two FP32 lanes per
+// instruction on a 64-bit register pair).  The lockstep CC pass tests robot
+// spheres s and s+1 against each staged primitive together: their centres sit
+// packed per axis, a primitive coordinate is the broadcast operand, and the
+// squared distance is built with the same fused operations in the same order
+// as the scalar tests (cp_hit_box / cp_hit_sph), so every verdict is the
+// scalar one; the work per primitive drops from ~26 to ~19 instructions
+// (boxes) and from 18 to 10 (spheres) on an issue-bound kernel.
+typedef unsigned long long cp_f2;
+__device__ __forceinline__ cp_f2 cp_pk(float a, float b) {
+    cp_f2 r;
+    asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(a), "f"(b));
+    return r;
+}
+__device__ __forceinline__ void cp_upk(cp_f2 r, float& a, float& b) {
+    asm("mov.b64 {%0, %1}, %2;" : "=f"(a), "=f"(b) : "l"(r));
+}
+__device__ __forceinline__ cp_f2 cp_sub2(cp_f2 a, cp_f2 b) {
+    cp_f2 r;
+    asm("sub.rn.ftz.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
+    return r;
+}
+__device__ __forceinline__ cp_f2 cp_add2(cp_f2 a, cp_f2 b) {
+    cp_f2 r;
+    asm("add.rn.ftz.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
+    return r;
+}
+__device__ __forceinline__ cp_f2 cp_mul2(cp_f2 a, cp_f2 b) {
+    cp_f2 r;
+    asm("mul.rn.ftz.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
+    return r;
+}
+__device__ __forceinline__ cp_f2 cp_fma2(cp_f2 a, cp_f2 b, cp_f2 c) {
+    cp_f2 r;
+    asm("fma.rn.ftz.f32x2 %0, %1, %2, %3;" : "=l"(r) : "l"(a), "l"(b), "l"(c));
+    return r;
+}
+// spheres (cx, cy, cz packed, squared radii r20 / r21) vs one box (centre c,
+// half extent h): cp_hit_box for both
+__device__ __forceinline__ void cp_hit_box2(cp_f2 cx, cp_f2 cy, cp_f2 cz, float r20, float r21, float4 c, float4 h,
+                                            bool& a0, bool& a1) {
+    float dx0, dx1, dy0, dy1, dz0, dz1;
+    cp_upk(cp_sub2(cx, cp_pk(c.x, c.x)), dx0, dx1);
+    cp_upk(cp_sub2(cy, cp_pk(c.y, c.y)), dy0, dy1);
+    cp_upk(cp_sub2(cz, cp_pk(c.z, c.z)), dz0, dz1);
+    const cp_f2 ex = cp_pk(fmaxf(fabsf(dx0) - h.x, 0.f), fmaxf(fabsf(dx1) - h.x, 0.f));
+    const cp_f2 ey = cp_pk(fmaxf(fabsf(dy0) - h.y, 0.f), fmaxf(fabsf(dy1) - h.y, 0.f));
+    const cp_f2 ez = cp_pk(fmaxf(fabsf(dz0) - h.z, 0.f), fmaxf(fabsf(dz1) - h.z, 0.f));
+    float s0, s1;
+    cp_upk(cp_fma2(ex, ex, cp_fma2(ey, ey, cp_mul2(ez, ez))), s0, s1);
+    a0 |= s0 < r20;
+    a1 |= s1 < r21;
+}
+// spheres (packed centres, radii r) vs one obstacle sphere o: cp_hit_sph for both
+__device__ __forceinline__ void cp_hit_sph2(cp_f2 cx, cp_f2 cy, cp_f2 cz, cp_f2 r, float4 o, bool& a0, bool& a1) {
+    const cp_f2 dx = cp_sub2(cx, cp_pk(o.x, o.x)), dy = cp_sub2(cy, cp_pk(o.y, o.y)),
+                dz = cp_sub2(cz, cp_pk(o.z, o.z)), rr = cp_add2(r, cp_pk(o.w, o.w));
+    float s0, s1, q0, q1;
+    cp_upk(cp_fma2(dx, dx, cp_fma2(dy, dy, cp_mul2(dz, dz))), s0, s1);
+    cp_upk(cp_mul2(rr, rr), q0, q1);
+    a0 |= s0 < q0;
+    a1 |= s1 < q1;
+}
+
 // The environment checks of cp_validate for one flag setting (compile-time,
 // so the flag-off pass carries no votes): updates first_r (smallest round with
 // a hit), rounds_done (checks per waypoint row evaluated) and stop.
@@ -900,6 +974,7 @@ __device__ __forceinline__ void cp_env_pass(const Team& tm, const float4* sp, bo
         const float4 c1 = two ? sp[s + 1] : make_float4(-3e18f, -3e18f, -3e18f, 0.f);
         const float ra = cp_rad_tab[s] + margin, rb = (two ? cp_rad_tab[s + 1] : 0.f) + margin;
         const float r0 = ra * ra, r1 = rb * rb;
+        const cp_f2 px = cp_pk(c0.x, c1.x), py = cp_pk(c0.y, c1.y), pz = cp_pk(c0.z, c1.z), pr = cp_pk(ra, rb);
         const int rb0 = s * E, rb1 = (s + 1) * E;
         const int per_chunk = two ? 2 * CP_CHUNK : CP_CHUNK;
         bool only0 = false;
@@ -908,11 +983,8 @@ __device__ __forceinline__ void cp_env_pass(const Team& tm, const float4* sp, bo
             bool a0 = false, a1 = false;
             if (!only0) {
 #pragma unroll
-                for (int j = 0; j < CP_CHUNK; j++) {
-                    const float4 bc = cp_lds4(sc.box_c + p0 + j), bh = cp_lds4(sc.box_h + p0 + j);
-                    a0 |= cp_hit_box(c0.x, c0.y, c0.z, r0, bc, bh);
-                    a1 |= cp_hit_box(c1.x, c1.y, c1.z, r1, bc, bh);
-                }
+                for (int j = 0; j < CP_CHUNK; j++)
+                    cp_hit_box2(px, py, pz, r0, r1, cp_lds4(sc.box_c + p0 + j), cp_lds4(sc.box_h + p0 + j), a0, a1);
                 rounds_done += per_chunk;
             } else {
 #pragma unroll
@@ -948,11 +1020,7 @@ __device__ __forceinline__ void cp_env_pass(const Team& tm, const float4* sp, bo
             bool a0 = false, a1 = false;
             if (!only0) {
 #pragma unroll
-                for (int j = 0; j < CP_CHUNK; j++) {
-                    const float4 o = cp_lds4(sc.sph + p0 + j);
-                    a0 |= cp_hit_sph(c0.x, c0.y, c0.z, ra, o);
-                    a1 |= cp_hit_sph(c1.x, c1.y, c1.z, rb, o);
-                }
+                for (int j = 0; j < CP_CHUNK; j++) cp_hit_sph2(px, py, pz, pr, cp_lds4(sc.sph + p0 + j), a0, a1);
                 rounds_done += per_chunk;
             } else {
 #pragma unroll
@@ -1050,11 +1118,25 @@ __device__ __forceinline__ unsigned cp_team_or(const Team& tm, unsigned v) {
     return __reduce_or_sync(tm.mask, v);
 }
 
+// Robot sphere centres of the lane's waypoint: registers when the robot has
+// at most CP_SREG_MAX spheres (every access below then has a compile-time
+// index -- unrolled loops, the self pairs through the folded cp_pair_a/b
+// switches, and a select chain for the narrow phase's warp-uniform sphere
+// index), else a local array (dynamically indexed: the 36-sphere arm).
+#define CP_SREG_MAX 16
+#define CP_SREG (CP_S > 0 && CP_S <= CP_SREG_MAX)
+
 __device__ __noinline__ ValOut cp_validate_cull(const Team tm, const float (*seg)[CP_NP], int W, int t_first,
                                                 bool flag_on, float margin, const SceneSm sc) {
     const int t = (int)tm.lane;
     const bool mine = t >= t_first && t < W;
+#if CP_SREG
+    float sx[CP_S], sy[CP_S], sz[CP_S], sr[CP_S];
+#define CP_SPH(s) make_float4(sx[s], sy[s], sz[s], sr[s])
+#else
     float4 sp[CP_S > 0 ? CP_S : 1];
+#define CP_SPH(s) sp[s]
+#endif
     float4 rc, rh;   // robot box of my waypoint (centre / half extent)
     {
         float q[CP_N];
@@ -1066,7 +1148,11 @@ __device__ __noinline__ ValOut cp_validate_cull(const Team tm, const float (*seg
 #pragma unroll
         for (int s = 0; s < CP_S; s++) {
             const float r = cp_rad_tab[s] + margin;
+#if CP_SREG
+            sx[s] = SPH[3 * s]; sy[s] = SPH[3 * s + 1]; sz[s] = SPH[3 * s + 2]; sr[s] = r;
+#else
             sp[s] = make_float4(SPH[3 * s], SPH[3 * s + 1], SPH[3 * s + 2], r);
+#endif
             lx = fminf(lx, SPH[3 * s] - r); hx = fmaxf(hx, SPH[3 * s] + r);
             ly = fminf(ly, SPH[3 * s + 1] - r); hy = fmaxf(hy, SPH[3 * s + 1] + r);
             lz = fminf(lz, SPH[3 * s + 2] - r); hz = fmaxf(hz, SPH[3 * s + 2] + r);
@@ -1076,6 +1162,33 @@ __device__ __noinline__ ValOut cp_validate_cull(const Team tm, const float (*seg
         rh = mine ? make_float4(0.5f * (hx - lx) + 1e-5f, 0.5f * (hy - ly) + 1e-5f, 0.5f * (hz - lz) + 1e-5f, 0.f)
                   : make_float4(-1e30f, -1e30f, -1e30f, 0.f);
     }
+    // sphere s (warp-uniform, runtime) of the narrow phase
+    auto sph_at = [&](int s) -> float4 {
+#if CP_SREG
+        float4 c = CP_SPH(0);
+#pragma unroll
+        for (int i = 1; i < CP_S; i++)
+            if (s == i) c = CP_SPH(i);
+        return c;
+#else
+        return sp[s];
+#endif
+    };
+    // robot spheres that reach a chunk bound (bc, bh): one bit per sphere,
+    // tested two spheres per packed FP32x2 step (cp_hit_box2 = cp_hit_box)
+    auto bound_mask = [&](float4 bc, float4 bh, unsigned* m) {
+#pragma unroll
+        for (int s = 0; s + 1 < CP_S; s += 2) {
+            const float4 a = CP_SPH(s), b = CP_SPH(s + 1);
+            bool h0 = false, h1 = false;
+            cp_hit_box2(cp_pk(a.x, b.x), cp_pk(a.y, b.y), cp_pk(a.z, b.z), a.w * a.w, b.w * b.w, bc, bh, h0, h1);
+            m[s >> 5] |= (h0 ? 1u << (s & 31) : 0u) | (h1 ? 1u << ((s + 1) & 31) : 0u);
+        }
+        if (CP_S & 1) {
+            const float4 a = CP_SPH(CP_S - 1);
+            if (cp_hit_box(a.x, a.y, a.z, a.w * a.w, bc, bh)) m[(CP_S - 1) >> 5] |= 1u << ((CP_S - 1) & 31);
+        }
+    };
     bool hit = false, stop = false;
     i64 narrow = 0, bound = 0;
     const float4* cl = sc.cl;
@@ -1102,9 +1215,7 @@ __device__ __noinline__ ValOut cp_validate_cull(const Team tm, const float (*seg
         if (!tm.any(ov)) continue;
         unsigned m[(CP_S + 31) / 32 > 0 ? (CP_S + 31) / 32 : 1] = {};
         if (ov) {
-#pragma unroll
-            for (int s = 0; s < CP_S; s++)
-                if (cp_hit_box(sp[s].x, sp[s].y, sp[s].z, sp[s].w * sp[s].w, bc, bh)) m[s >> 5] |= 1u << (s & 31);
+            bound_mask(bc, bh, m);
             bound += CP_S;
         }
 #pragma unroll
@@ -1114,7 +1225,7 @@ __device__ __noinline__ ValOut cp_validate_cull(const Team tm, const float (*seg
             while (um) {
                 const int s = 32 * w + __ffs(um) - 1;
                 um &= um - 1;
-                const float4 c = sp[s];
+                const float4 c = sph_at(s);
                 const float r2 = c.w * c.w;
                 bool any = false;
 #pragma unroll
@@ -1145,9 +1256,7 @@ __device__ __noinline__ ValOut cp_validate_cull(const Team tm, const float (*seg
         if (!tm.any(ov)) continue;
         unsigned m[(CP_S + 31) / 32 > 0 ? (CP_S + 31) / 32 : 1] = {};
         if (ov) {
-#pragma unroll
-            for (int s = 0; s < CP_S; s++)
-                if (cp_hit_box(sp[s].x, sp[s].y, sp[s].z, sp[s].w * sp[s].w, bc, bh)) m[s >> 5] |= 1u << (s & 31);
+            bound_mask(bc, bh, m);
             bound += CP_S;
         }
 #pragma unroll
@@ -1157,7 +1266,7 @@ __device__ __noinline__ ValOut cp_validate_cull(const Team tm, const float (*seg
             while (um) {
                 const int s = 32 * w + __ffs(um) - 1;
                 um &= um - 1;
-                const float4 c = sp[s];
+                const float4 c = sph_at(s);
                 bool any = false;
 #pragma unroll
                 for (int j = 0; j < CP_CHUNK; j++) any |= cp_hit_sph(c.x, c.y, c.z, c.w, cp_lds4(ch + 2 + j));
@@ -1168,15 +1277,22 @@ __device__ __noinline__ ValOut cp_validate_cull(const Team tm, const float (*seg
     }
     }
     if (!stop && CP_P > 0) {
+#if CP_SREG
+#pragma unroll
+        for (int k = 0; k < CP_P; k++) {   // compile-time pair indices: registers only
+            const float4 pa = CP_SPH(cp_pair_a(k)), pb = CP_SPH(cp_pair_b(k));
+#else
 #pragma unroll 1
         for (int k = 0; k < CP_P; k++) {
             const float4 pa = sp[cp_pair_tab[2 * k]], pb = sp[cp_pair_tab[2 * k + 1]];
+#endif
             const float rr = pa.w + pb.w;
             float dx = pa.x - pb.x, dy = pa.y - pb.y, dz = pa.z - pb.z;
             hit |= mine && fmaf(dx, dx, fmaf(dy, dy, dz * dz)) < rr * rr;
         }
         if (mine) narrow += CP_P;
     }
+#undef CP_SPH
     ValOut o;
     int key = hit ? t : CP_INTMAX, idx = t;
     tm.argmin_i(key, idx);
