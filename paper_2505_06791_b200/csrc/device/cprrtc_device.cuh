@@ -923,22 +923,33 @@ __device__ __forceinline__ cp_f2 cp_fma2(cp_f2 a, cp_f2 b, cp_f2 c) {
     asm("fma.rn.ftz.f32x2 %0, %1, %2, %3;" : "=l"(r) : "l"(a), "l"(b), "l"(c));
     return r;
 }
-// spheres (cx, cy, cz packed, squared radii r20 / r21) vs one box (centre c,
-// half extent h): cp_hit_box for both
-__device__ __forceinline__ void cp_hit_box2(cp_f2 cx, cp_f2 cy, cp_f2 cz, float r20, float r21, float4 c, float4 h,
+// spheres (cx, cy, cz packed) vs one box (centre c, half extent h):
+// cp_hit_box for both.  The clamp max(|d| - h, 0) is taken as u = t + |t| =
+// 2 max(t, 0) (t = |d| - h): two FP32-pipe adds with |.| operand modifiers
+// instead of an ALU-pipe FMNMX, and the squared sum (exactly 4x the scalar
+// one, a power-of-two scale) is compared with r4 = 4 r^2 -- the same verdict.
+__device__ __forceinline__ void cp_hit_box2(cp_f2 cx, cp_f2 cy, cp_f2 cz, float r40, float r41, float4 c, float4 h,
                                             bool& a0, bool& a1) {
     float dx0, dx1, dy0, dy1, dz0, dz1;
     cp_upk(cp_sub2(cx, cp_pk(c.x, c.x)), dx0, dx1);
     cp_upk(cp_sub2(cy, cp_pk(c.y, c.y)), dy0, dy1);
     cp_upk(cp_sub2(cz, cp_pk(c.z, c.z)), dz0, dz1);
-    const cp_f2 ex = cp_pk(fmaxf(fabsf(dx0) - h.x, 0.f), fmaxf(fabsf(dx1) - h.x, 0.f));
-    const cp_f2 ey = cp_pk(fmaxf(fabsf(dy0) - h.y, 0.f), fmaxf(fabsf(dy1) - h.y, 0.f));
-    const cp_f2 ez = cp_pk(fmaxf(fabsf(dz0) - h.z, 0.f), fmaxf(fabsf(dz1) - h.z, 0.f));
+    const float tx0 = fabsf(dx0) - h.x, tx1 = fabsf(dx1) - h.x, ty0 = fabsf(dy0) - h.y, ty1 = fabsf(dy1) - h.y;
+    const float tz0 = fabsf(dz0) - h.z, tz1 = fabsf(dz1) - h.z;
+    const cp_f2 ux = cp_pk(tx0 + fabsf(tx0), tx1 + fabsf(tx1));
+    const cp_f2 uy = cp_pk(ty0 + fabsf(ty0), ty1 + fabsf(ty1));
+    const cp_f2 uz = cp_pk(tz0 + fabsf(tz0), tz1 + fabsf(tz1));
     float s0, s1;
-    cp_upk(cp_fma2(ex, ex, cp_fma2(ey, ey, cp_mul2(ez, ez))), s0, s1);
-    a0 |= s0 < r20;
-    a1 |= s1 < r21;
+    cp_upk(cp_fma2(ux, ux, cp_fma2(uy, uy, cp_mul2(uz, uz))), s0, s1);
+    a0 |= s0 < r40;
+    a1 |= s1 < r41;
 }
+
+// Robot spheres s, s+1 packed per axis (one 64-bit register pair each), the
+// layout cp_env_pass loads: no repacking moves in the primitive loop.
+struct SPair {
+    cp_f2 x, y, z;
+};
 // spheres (packed centres, radii r) vs one obstacle sphere o: cp_hit_sph for both
 __device__ __forceinline__ void cp_hit_sph2(cp_f2 cx, cp_f2 cy, cp_f2 cz, cp_f2 r, float4 o, bool& a0, bool& a1) {
     const cp_f2 dx = cp_sub2(cx, cp_pk(o.x, o.x)), dy = cp_sub2(cy, cp_pk(o.y, o.y)),
@@ -954,8 +965,8 @@ __device__ __forceinline__ void cp_hit_sph2(cp_f2 cx, cp_f2 cy, cp_f2 cz, cp_f2 
 // so the flag-off pass carries no votes): updates first_r (smallest round with
 // a hit), rounds_done (checks per waypoint row evaluated) and stop.
 template <bool FLAG>
-__device__ __forceinline__ void cp_env_pass(const Team& tm, const float4* sp, bool mine, float margin,
-                                            const SceneSm& sc, int E, int& first_r, i64& rounds_done,
+__device__ __forceinline__ void cp_env_pass(const Team& tm, const float4* sp, const SPair* spp, bool mine,
+                                            float margin, const SceneSm& sc, int E, int& first_r, i64& rounds_done,
                                             bool& stop) {
     // Robot spheres go in pairs (s, s+1) that share every staged primitive
     // load.  first_r is the smallest sphere-major round with a hit (the
@@ -973,8 +984,9 @@ __device__ __forceinline__ void cp_env_pass(const Team& tm, const float4* sp, bo
         // +1e18 padding primitives of the staged scene
         const float4 c1 = two ? sp[s + 1] : make_float4(-3e18f, -3e18f, -3e18f, 0.f);
         const float ra = cp_rad_tab[s] + margin, rb = (two ? cp_rad_tab[s + 1] : 0.f) + margin;
-        const float r0 = ra * ra, r1 = rb * rb;
-        const cp_f2 px = cp_pk(c0.x, c1.x), py = cp_pk(c0.y, c1.y), pz = cp_pk(c0.z, c1.z), pr = cp_pk(ra, rb);
+        const float r0 = ra * ra, r1 = rb * rb, r40 = 4.f * r0, r41 = 4.f * r1;
+        const SPair pp = spp[s >> 1];
+        const cp_f2 px = pp.x, py = pp.y, pz = pp.z, pr = cp_pk(ra, rb);
         const int rb0 = s * E, rb1 = (s + 1) * E;
         const int per_chunk = two ? 2 * CP_CHUNK : CP_CHUNK;
         bool only0 = false;
@@ -984,7 +996,7 @@ __device__ __forceinline__ void cp_env_pass(const Team& tm, const float4* sp, bo
             if (!only0) {
 #pragma unroll
                 for (int j = 0; j < CP_CHUNK; j++)
-                    cp_hit_box2(px, py, pz, r0, r1, cp_lds4(sc.box_c + p0 + j), cp_lds4(sc.box_h + p0 + j), a0, a1);
+                    cp_hit_box2(px, py, pz, r40, r41, cp_lds4(sc.box_c + p0 + j), cp_lds4(sc.box_h + p0 + j), a0, a1);
                 rounds_done += per_chunk;
             } else {
 #pragma unroll
@@ -1064,6 +1076,7 @@ __device__ __noinline__ ValOut cp_validate(const Team tm, const float (*seg)[CP_
     const bool mine = t >= t_first && t < W;
     const int E = sc.nb + sc.ne;
     float4 sp[CP_S > 0 ? CP_S : 1];   // world sphere centres of my waypoint (local memory)
+    SPair spp[CP_S > 0 ? (CP_S + 1) / 2 : 1];   // the same, pair-packed for the primitive loop
     {
         float q[CP_N];
 #pragma unroll
@@ -1072,12 +1085,21 @@ __device__ __noinline__ ValOut cp_validate(const Team tm, const float (*seg)[CP_
         cp_fk<float>(q, R, P, AX, OR, SPH);
 #pragma unroll
         for (int s = 0; s < CP_S; s++) sp[s] = make_float4(SPH[3 * s], SPH[3 * s + 1], SPH[3 * s + 2], 0.f);
+        // a missing second sphere of the last pair sits far from everything,
+        // including the +1e18 padding primitives of the staged scene
+#pragma unroll
+        for (int s = 0; s < CP_S; s += 2) {
+            const bool two = s + 1 < CP_S;
+            const int u = two ? 3 * s + 3 : 3 * s;   // (in range when there is no second sphere)
+            spp[s >> 1] = SPair{cp_pk(SPH[3 * s], two ? SPH[u] : -3e18f), cp_pk(SPH[3 * s + 1], two ? SPH[u + 1] : -3e18f),
+                                cp_pk(SPH[3 * s + 2], two ? SPH[u + 2] : -3e18f)};
+        }
     }
     int first_r = CP_INTMAX;
     i64 rounds_done = 0;   // checks per waypoint row this team evaluated (team-uniform)
     bool stop = false;
-    if (flag_on) cp_env_pass<true>(tm, sp, mine, margin, sc, E, first_r, rounds_done, stop);
-    else cp_env_pass<false>(tm, sp, mine, margin, sc, E, first_r, rounds_done, stop);
+    if (flag_on) cp_env_pass<true>(tm, sp, spp, mine, margin, sc, E, first_r, rounds_done, stop);
+    else cp_env_pass<false>(tm, sp, spp, mine, margin, sc, E, first_r, rounds_done, stop);
     if (!stop && CP_P > 0) {
         const int rbase = CP_S * E;
 #pragma unroll 1
@@ -1181,7 +1203,8 @@ __device__ __noinline__ ValOut cp_validate_cull(const Team tm, const float (*seg
         for (int s = 0; s + 1 < CP_S; s += 2) {
             const float4 a = CP_SPH(s), b = CP_SPH(s + 1);
             bool h0 = false, h1 = false;
-            cp_hit_box2(cp_pk(a.x, b.x), cp_pk(a.y, b.y), cp_pk(a.z, b.z), a.w * a.w, b.w * b.w, bc, bh, h0, h1);
+            cp_hit_box2(cp_pk(a.x, b.x), cp_pk(a.y, b.y), cp_pk(a.z, b.z), 4.f * (a.w * a.w), 4.f * (b.w * b.w), bc,
+                        bh, h0, h1);
             m[s >> 5] |= (h0 ? 1u << (s & 31) : 0u) | (h1 ? 1u << ((s + 1) & 31) : 0u);
         }
         if (CP_S & 1) {
