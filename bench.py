@@ -412,7 +412,7 @@ def throughput(args, world, rank, local, line):
     for w in range(max(3, args.warmup)):
         s, g, seeds = batch_arrays(w)
         plan_many(m, sc, sp, s, g, seeds, prm, opt)
-    dev, wall, solved, kern, flops = [], [], 0, [], 0.0
+    dev, wall, solved, kern, flops, ccall = [], [], 0, [], 0.0, []
     for step in range(args.steps):
         s, g, seeds = batch_arrays(100 + step)
         barrier(world)
@@ -425,6 +425,7 @@ def throughput(args, world, rank, local, line):
         wall.append(max(b[1] for b in both))
         solved += int(r.solved.sum())
         kern.append(kms)
+        ccall.append(r.wall_ms)
         st = r.stats.astype(np.float64).sum(axis=0)
         flops += st[8] * FLOP_STAGE1_M1 + st[9] * FLOP_FK_ARM7 + st[5] * FLOP_CHECK + st[10] * FLOP_NN7
     solved_all = sum(gather(world, solved))
@@ -437,6 +438,7 @@ def throughput(args, world, rank, local, line):
                     "h2d_bytes_per_step": BATCH * (2 * 7 * 8 + 8),
                     "d2h_bytes_per_step": BATCH * (64 + 8 * 12)},
             "ms_per_step_device": float(np.mean(dev)), "ms_per_step_wall": float(np.mean(wall)),
+            "ms_per_step_c_call_rank0": float(np.mean(ccall)),
             "kernel_ms_per_step_rank0": float(np.mean(kern)), "success_rate": solved_all / total,
             "config": f"configs[4]: {BATCH} arm7 table-plane (z=0.60, tau 0.01) queries per GPU per step, W=16, "
                       "max_iterations 300 each, one persistent launch per GPU (plan_many), "

@@ -93,7 +93,7 @@ typedef struct {
     double tau_task;         /* <= 0: from the constraint */
     double tau_sm;           /* <= 0: auto, 1.5 x max initial gap */
     int max_iterations;      /* samples drawn, across all teams */
-    double time_budget_ms;   /* <= 0 or deterministic: none */
+    double time_budget_ms;   /* deterministic: ignored; <= 0: expired (TimedOut before sample 1, planner.py:450-453) */
     double connect_tolerance;/* <= 0: step_size / 10 */
     int projection_mode;     /* 0 parallel, 1 literal-gap, 2 naive */
     int flag_on;
