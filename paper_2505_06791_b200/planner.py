@@ -30,6 +30,7 @@ from __future__ import annotations
 
 import ctypes as C
 import math
+import threading
 import time
 from contextlib import contextmanager
 from collections.abc import Sequence
@@ -304,9 +305,24 @@ def _bound(problem_like, opt: DeviceOptions):
     lock, so no other caller can swap the constraint in between."""
     ctx = kernels.context(problem_like.model, opt.device)
     with ctx.lock:
-        ctx.set_scene(problem_like.scene.packed())
+        ctx.set_scene(_scene_packed(problem_like.scene))
         ctx.set_spec(None if problem_like.spec is None else problem_like.spec.packed)
         yield ctx
+
+
+_PACKED: dict = {}
+
+
+def _scene_packed(scene):
+    """scene.packed(), once per scene object: this repo's Scene caches its
+    packing, the reference's rebuilds it on every call (geometry.py:97-98),
+    which the device context would then have to re-hash to see it unchanged."""
+    hit = _PACKED.get(id(scene))
+    if hit is None or hit[0] is not scene:
+        if len(_PACKED) > 1024:
+            _PACKED.clear()
+        hit = _PACKED[id(scene)] = (scene, scene.packed())
+    return hit[1]
 
 
 @contextmanager
@@ -322,7 +338,7 @@ def _bound_many(problem_like, devices):
             seen[d] = slot + 1
             c = kernels.context(problem_like.model, d, slot)
             stack.enter_context(c.lock)
-            c.set_scene(problem_like.scene.packed())
+            c.set_scene(_scene_packed(problem_like.scene))
             c.set_spec(None if problem_like.spec is None else problem_like.spec.packed)
             c.prepare(problem_like.params.width)
             ctxs.append(c)
@@ -586,50 +602,73 @@ def _result(r, p, paths_i, srcs_i, wall, B, pc) -> PlanResult:
     return PlanResult("Solved", tuple(path), sources, stats)
 
 
-class _OneIO:
-    """Reusable host buffers and their ctypes pointers for single-query calls
-    (the latency path: no per-call array construction)."""
+class _Session:
+    """One thread's bound single-query call for one (model, scene, spec,
+    params, options): context, parameter block, the scene / constraint
+    packings and reusable host buffers with their ctypes pointers, so the
+    latency path builds no arrays and looks nothing up twice per call."""
 
-    def __init__(self, n, pc):
+    __slots__ = ("objs", "ctx", "prm", "pc", "width", "pscene", "pspec", "s", "g", "seed", "res", "paths",
+                 "srcs", "args")
+
+    def __init__(self, problem, options):
+        self.objs = (problem.model, problem.scene, problem.spec, problem.params, options)
+        self.ctx = kernels.context(problem.model, options.device)
+        self.prm = _params_struct(problem.params, options)
+        self.pc = pc = int(self.prm.path_capacity)
+        self.width = problem.params.width
+        self.pscene = _scene_packed(problem.scene)
+        self.pspec = None if problem.spec is None else problem.spec.packed
+        n = self.ctx.n
         self.s = np.empty((1, n))
         self.g = np.empty((1, n))
         self.seed = np.zeros(1, np.int64)
         self.res = (_lib.Result * 1)()
         self.paths = np.empty((1, pc, n))
         self.srcs = np.empty((1, pc), np.int32)
-        self.args = (_lib.ptr(self.s), _lib.ptr(self.g), _lib.ptr(self.seed, _lib._lp), self.res,
-                     _lib.ptr(self.paths), _lib.ptr(self.srcs, _lib._ip))
+        self.args = (self.ctx.h, C.byref(self.prm), 1, _lib.ptr(self.s), _lib.ptr(self.g),
+                     _lib.ptr(self.seed, _lib._lp), self.res, _lib.ptr(self.paths), _lib.ptr(self.srcs, _lib._ip))
 
 
-_ONE: dict = {}
+_TLS = threading.local()
+
+
+def _session(problem, options) -> _Session:
+    cache = getattr(_TLS, "sessions", None)
+    if cache is None:
+        cache = _TLS.sessions = {}
+    key = (id(problem.model), id(problem.scene), id(problem.spec), id(problem.params), id(options))
+    s = cache.get(key)
+    if s is None or s.objs[0] is not problem.model or s.objs[1] is not problem.scene \
+            or s.objs[2] is not problem.spec or s.objs[3] is not problem.params or s.objs[4] is not options:
+        if len(cache) > 256:
+            cache.clear()
+        s = cache[key] = _Session(problem, options)
+    return s
 
 
 def _plan_one(problem: PlanProblem, options: DeviceOptions, return_dense: bool) -> PlanResult:
-    prm = _params_struct(problem.params, options)
-    ctx = kernels.context(problem.model, options.device)
-    pc = int(prm.path_capacity)
-    key = (id(ctx), pc, __import__("threading").get_ident())
-    io = _ONE.get(key)
-    if io is None:
-        if len(_ONE) > 64:
-            _ONE.clear()
-        io = _ONE[key] = _OneIO(ctx.n, pc)
-    seed = int(problem.params.seed_offset)
+    ss = _session(problem, options)
+    seed = problem.params.seed_offset
     if seed < 0:
         raise ValueError("seed_offset must be >= 0")
-    io.s[0] = problem.start
-    io.g[0] = problem.goal
-    io.seed[0] = seed
-    with _bound(problem, options) as ctx:
-        ctx.prepare(problem.params.width)
+    ss.s[0] = problem.start
+    ss.g[0] = problem.goal
+    ss.seed[0] = seed
+    ctx = ss.ctx
+    with ctx.lock:   # bind + launch under one lock (planner._bound)
+        ctx.set_scene(ss.pscene)
+        ctx.set_spec(ss.pspec)
+        ctx.prepare(ss.width)
         t0 = time.perf_counter()
-        rc = ctx.L.cprrtc_plan(ctx.h, C.byref(prm), 1, *io.args)
+        rc = ctx.L.cprrtc_plan(*ss.args)
         wall = (time.perf_counter() - t0) * 1e3
-        _lib.check(rc, "plan")
-        res = _result_one(io.res[0], problem, io.paths[0], io.srcs[0], wall, pc)
+        if rc:
+            _lib.check(rc, "plan")
+        res = _result_one(ss.res[0], problem, ss.paths[0], ss.srcs[0], wall, ss.pc)
         if return_dense and res.solved:
             L = len(res.path)
-            dense, ok = _derive(ctx, prm, io.paths[0, :L], io.srcs[0, :L - 1])
+            dense, ok = _derive(ctx, ss.prm, ss.paths[0, :L], ss.srcs[0, :L - 1])
             res = replace(res, dense=dense)
     return res
 
@@ -651,7 +690,9 @@ def _out_buffers(B, pc, n):
 def plan(problem: PlanProblem, options: DeviceOptions = DeviceOptions(),
          return_dense: bool = False) -> PlanResult:
     """reference plan() (planner.py:430-485) on the device."""
-    if np.array_equal(problem.start, problem.goal):
+    # start == goal (np.array_equal semantics: -0.0 == 0.0, NaN != NaN) through
+    # Python float lists: ~10x cheaper than array_equal on the latency path
+    if problem.start.tolist() == problem.goal.tolist():
         # endpoint checks first, exactly like the reference (planner.py:435-440)
         t0 = time.perf_counter()
         code = kernels.check_config_batch(problem.model, problem.scene, problem.spec,
