@@ -216,6 +216,15 @@ CPRRTC_API int cprrtc_halton(void *ctx, int count, int64_t first_index, int64_t 
 CPRRTC_API int cprrtc_plan(void *ctx, const cprrtc_params *params, int B, const double *starts,
                 const double *goals, const int64_t *seeds, cprrtc_result *results,
                 double *paths, int32_t *sources);
+/* cprrtc_plan with the solution paths packed back to back (the batched
+ * queries of BASELINE configs[4]; same planner, same results):
+ * offsets (B+1): query i's path nodes are paths[offsets[i] .. offsets[i+1])
+ * (n doubles each) and its edge sources sources[offsets[i] ..
+ * offsets[i+1]-1); flat_capacity = rows available in paths / sources
+ * (CPRRTC_ELIMIT if the batch's paths need more; results are valid then). */
+CPRRTC_API int cprrtc_plan_flat(void *ctx, const cprrtc_params *params, int B, const double *starts,
+                                const double *goals, const int64_t *seeds, cprrtc_result *results,
+                                int64_t *offsets, double *paths, int32_t *sources, int64_t flat_capacity);
 /* cprrtc_plan's batch sharded over n_ctx contexts (typically one per GPU):
  * context k plans the contiguous slice [k*B/n_ctx, (k+1)*B/n_ctx); every shard
  * is launched before any is awaited, and the results land in the caller's

@@ -30,7 +30,7 @@ EXPORTS = (
     "cprrtc_project_config", "cprrtc_check_config", "cprrtc_validate", "cprrtc_project",
     "cprrtc_nearest", "cprrtc_halton", "cprrtc_plan", "cprrtc_derive_edges",
     "cprrtc_clearance", "cprrtc_damped_step", "cprrtc_flush_l2", "cprrtc_nearest_trees", "cprrtc_step",
-    "cprrtc_validate_broadphase", "cprrtc_plan_race", "cprrtc_plan_multi",
+    "cprrtc_validate_broadphase", "cprrtc_plan_race", "cprrtc_plan_multi", "cprrtc_plan_flat",
 )
 MAX_RACE = 8
 

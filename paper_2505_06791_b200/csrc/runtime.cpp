@@ -1507,6 +1507,40 @@ static int plan_collect(Ctx* c, int B, cprrtc_result* results, double* paths, in
     return 0;
 }
 
+// cprrtc_plan's results with the paths packed back to back (batches): one
+// pass over the mapped result block, no per-query path_capacity stride.
+int cprrtc_plan_flat(void* p, const cprrtc_params* prm, int B, const double* starts, const double* goals,
+                     const int64_t* seeds, cprrtc_result* results, int64_t* offsets, double* paths,
+                     int32_t* sources, int64_t flat_capacity) {
+    Ctx* c = C(p);
+    if (!c || !prm || B < 1 || !starts || !goals || !results || !offsets || (flat_capacity > 0 && (!paths || !sources)))
+        return fail(CPRRTC_EARG, "bad argument");
+    if (int rc = check_params(prm)) return rc;
+    if (int rc = plan_launch(c, prm, B, starts, goals, seeds, nullptr)) return rc;
+    if (int rc = plan_collect(c, B, results, nullptr, nullptr)) return rc;
+    const int n = c->n, path_cap = c->path_cap;
+    const float* hp = c->h_paths.host<float>();
+    const int* hs = c->h_src.host<int>();
+    int64_t off = 0;
+    for (int i = 0; i < B; i++) {
+        offsets[i] = off;
+        off += results[i].path_len;
+    }
+    offsets[B] = off;
+    if (off > flat_capacity) return fail(CPRRTC_ELIMIT, "flat path buffer too small");
+    for (int i = 0; i < B; i++) {
+        const int L = results[i].path_len;
+        if (L <= 0) continue;
+        const float* src = hp + (size_t)i * path_cap * n;
+        double* dst = paths + (size_t)offsets[i] * n;
+        for (int k = 0; k < L * n; k++) dst[k] = src[k];
+        const int* ss = hs + (size_t)i * path_cap;
+        int32_t* sd = sources + offsets[i];   // L - 1 edge sources, one slot of slack per query
+        for (int k = 0; k < L - 1; k++) sd[k] = ss[k];
+    }
+    return 0;
+}
+
 int cprrtc_plan(void* p, const cprrtc_params* prm, int B, const double* starts, const double* goals,
                 const int64_t* seeds, cprrtc_result* results, double* paths, int32_t* sources) {
     Ctx* c = C(p);

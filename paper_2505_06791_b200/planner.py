@@ -360,15 +360,19 @@ class BatchResult(Sequence):
     The arrays are the decoded device output: ``codes`` (B,) int (0 Solved,
     1 TimedOut, 2 IterLimit, 3 CapacityExceeded, 5 Stopped, -1 setup error),
     ``setup_codes``, ``path_len``, ``nodes`` (B, 2), ``device_ms``, ``stats``
-    (B, ST_COUNT) and the path rows (B, max path length, n) with their edge
-    sources.  Indexing gives the reference's PlanResult, built on first access
-    (a 1024-query batch costs ~5 ms of Python object construction when every
-    result is materialised, several times the launch itself)."""
+    (B, ST_COUNT), and every solved path packed back to back: query i's nodes
+    are ``rows[offsets[i]:offsets[i + 1]]`` (FP32 tree nodes as FP64; path(i)
+    puts the exact endpoints back) and its edge sources start at
+    ``sources[offsets[i]]``.  Indexing gives the reference's PlanResult, built
+    on first access (a 1024-query batch costs ~5 ms of Python object
+    construction when every result is materialised, several times the launch
+    itself)."""
 
-    def __init__(self, a, rows, sources, starts, goals, wall_ms, single):
+    def __init__(self, a, offsets, rows, sources, starts, goals, wall_ms, single):
         self.codes = a["status"].copy()
         self.setup_codes = a["setup_code"].copy()
         self.path_len = np.where(self.codes == 0, a["path_len"], 0)
+        self.offsets = offsets
         self.nodes = np.stack([a["ns"], a["ng"]], axis=1)
         self.device_ms = a["device_ms"].copy()
         self.stats = a["stats"].copy()
@@ -391,8 +395,8 @@ class BatchResult(Sequence):
 
     def path(self, i: int) -> np.ndarray:
         """(L, n) path of query i; the roots are the exact FP64 endpoints."""
-        L = int(self.path_len[i])
-        out = np.array(self.rows[i, :L])
+        o, L = int(self.offsets[i]), int(self.path_len[i])
+        out = np.array(self.rows[o:o + L])
         if L:
             out[0], out[-1] = self.starts[i], self.goals[i]
         return out
@@ -412,8 +416,8 @@ class BatchResult(Sequence):
                           int(self.nodes[i, 1]), float(self.device_ms[i]), s[8], s[9], s[10], s[11])
         code = int(self.codes[i])
         if code == 0:
-            L = int(self.path_len[i])
-            return _solved(tuple(self.path(i)), tuple(map(_SRC.__getitem__, self.sources[i, :L - 1].tolist())),
+            o, L = int(self.offsets[i]), int(self.path_len[i])
+            return _solved(tuple(self.path(i)), tuple(map(_SRC.__getitem__, self.sources[o:o + L - 1].tolist())),
                            stats)
         if code == -1:
             if self._single:
@@ -448,9 +452,8 @@ def plan_many(model, scene, spec, starts, goals, seed_offsets, params: PlanParam
     if (seeds < 0).any():
         raise ValueError("seed_offset must be >= 0")
     prm = _params_struct(params, options)
-    res = (_lib.Result * B)()
     pc = int(prm.path_capacity)
-    paths, srcs = _out_buffers(B, pc, n)
+    res, offsets, paths, srcs = _out_buffers(B, pc, n)
     devs = tuple(int(d) for d in devices) if devices is not None else ()
     if len(devs) > 1:
         with _bound_many(like, devs) as ctxs:
@@ -460,22 +463,38 @@ def plan_many(model, scene, spec, starts, goals, seed_offsets, params: PlanParam
                                                    _lib.ptr(goals), _lib.ptr(seeds, _lib._lp), res,
                                                    _lib.ptr(paths), _lib.ptr(srcs, _lib._ip)), "plan_multi")
             wall = (time.perf_counter() - t0) * 1e3
+        # the per-query (B, path_capacity, n) layout, packed like cprrtc_plan_flat's
+        a = np.frombuffer(res, dtype=_RESULT_DT)
+        L = np.where(a["status"] == 0, a["path_len"], 0)
+        offsets[0] = 0
+        np.cumsum(L, out=offsets[1:])
+        pv, sv = paths.reshape(B, pc, n), srcs.reshape(B, pc)
+        rows = np.concatenate([pv[i, :L[i]] for i in range(B)]) if L.any() else np.empty((0, n))
+        srcv = np.zeros(int(offsets[B]), np.int32)
+        for i in np.nonzero(L > 1)[0]:
+            srcv[offsets[i]:offsets[i] + L[i] - 1] = sv[i, :L[i] - 1]
+        return _batch_result(res, offsets, rows, srcv, starts, goals, wall, B, pc)
     else:
         opt = options if not devs else replace(options, device=devs[0])
         with _bound(like, opt) as ctx:
             ctx.prepare(params.width)
             t0 = time.perf_counter()
-            _lib.check(ctx.L.cprrtc_plan(ctx.h, C.byref(prm), B, _lib.ptr(starts), _lib.ptr(goals),
-                                         _lib.ptr(seeds, _lib._lp), res, _lib.ptr(paths),
-                                         _lib.ptr(srcs, _lib._ip)), "plan")
+            _lib.check(ctx.L.cprrtc_plan_flat(ctx.h, C.byref(prm), B, _lib.ptr(starts), _lib.ptr(goals),
+                                              _lib.ptr(seeds, _lib._lp), res, _lib.ptr(offsets, _lib._lp),
+                                              _lib.ptr(paths), _lib.ptr(srcs, _lib._ip), C.c_int64(B * pc)),
+                       "plan")
             wall = (time.perf_counter() - t0) * 1e3
+    tot = int(offsets[B])
+    # the packed rows and sources leave the reused output buffers (one
+    # contiguous copy each)
+    return _batch_result(res, offsets.copy(), paths[:tot].copy(), srcs[:tot].copy(), starts, goals, wall, B, pc)
+
+
+def _batch_result(res, offsets, rows, sources, starts, goals, wall, B, pc):
     a = np.frombuffer(res, dtype=_RESULT_DT)
     if (a["status"] == 4).any():
         raise RuntimeError(f"solution path longer than path_capacity={pc}")
-    lmax = int(a["path_len"][a["status"] == 0].max(initial=0))
-    # the rows and sources leave the reused output buffers (one copy)
-    return BatchResult(a, np.array(paths[:, :lmax]), np.array(srcs[:, :max(lmax - 1, 0)]), starts, goals,
-                       wall, single=(B == 1))
+    return BatchResult(a, offsets, rows, sources, starts, goals, wall, single=(B == 1))
 
 
 class _Like:
@@ -677,13 +696,17 @@ _OUT: dict = {}
 
 
 def _out_buffers(B, pc, n):
-    """Reusable host result buffers (paths are copied out per result)."""
-    key = (B, pc, n, __import__("threading").get_ident())
+    """Reusable host result buffers of a batch (the results leave them by
+    copy): the result structs, path offsets (B+1), and the packed path rows /
+    sources sized for the worst case B * path_capacity (virtual memory: only
+    the rows a batch writes are ever touched)."""
+    key = (B, pc, n, threading.get_ident())
     buf = _OUT.get(key)
     if buf is None:
         if len(_OUT) > 64:
             _OUT.clear()
-        buf = _OUT[key] = (np.empty((B, pc, n)), np.empty((B, pc), np.int32))
+        buf = _OUT[key] = ((_lib.Result * B)(), np.zeros(B + 1, np.int64), np.empty((B * pc, n)),
+                           np.empty(B * pc, np.int32))
     return buf
 
 

@@ -7,7 +7,7 @@ import bench
 from paper_2505_06791_b200.planner import DeviceOptions, PlanParams, PlanProblem, plan, prepare
 model, scene, spec, starts, goals = bench.workload()
 opt = DeviceOptions()
-gaps, walls, devs = [], [], []
+gaps, walls, devs, calls = [], [], [], []
 ctx = None
 for step in range(3):
     for j in range(25):
@@ -22,5 +22,7 @@ for step in range(3):
         w = (time.perf_counter() - t0) * 1e3
         if r.solved and step > 0:
             d = ctx.last_timing()[0]
-            walls.append(w); devs.append(d); gaps.append(w - d)
-print(f"median wall {np.median(walls):.3f} ms, median device {np.median(devs):.3f} ms, median per-query gap {np.median(gaps) * 1e3:.0f} us (p10 {np.percentile(gaps, 10) * 1e3:.0f}, p90 {np.percentile(gaps, 90) * 1e3:.0f})")
+            walls.append(w); devs.append(d); gaps.append(w - d); calls.append(r.stats.wall_ms)
+print(f"median wall {np.median(walls):.3f} ms, C call {np.median(calls):.3f} ms, device {np.median(devs):.3f} ms, "
+      f"median per-query gap {np.median(gaps) * 1e3:.0f} us (p10 {np.percentile(gaps, 10) * 1e3:.0f}, "
+      f"p90 {np.percentile(gaps, 90) * 1e3:.0f}); Python share {np.median(np.array(walls) - np.array(calls)) * 1e3:.0f} us")
