@@ -584,10 +584,10 @@ def _result_one(r, p, paths_i, srcs_i, wall, pc) -> "PlanResult":
     code = r.status
     if code == 0:
         L = r.path_len
-        path = list(paths_i[:L].copy())
-        path[0] = p.start.copy()                 # roots are the exact FP64 endpoints
-        path[-1] = p.goal.copy()
-        return _solved(tuple(path), tuple(map(_SRC.__getitem__, srcs_i[:L - 1].tolist())), stats)
+        rows = paths_i[:L].copy()                # one array; the path's nodes are its rows
+        rows[0] = p.start                        # roots are the exact FP64 endpoints
+        rows[-1] = p.goal
+        return _solved(tuple(rows), tuple(map(_SRC.__getitem__, srcs_i[:L - 1].tolist())), stats)
     if code == -1:
         raise PlanSetupError(_SETUP.get(r.setup_code, "invalid start/goal"))
     if code == 4:
@@ -623,30 +623,46 @@ def _result(r, p, paths_i, srcs_i, wall, B, pc) -> PlanResult:
 
 class _Session:
     """One thread's bound single-query call for one (model, scene, spec,
-    params, options): context, parameter block, the scene / constraint
-    packings and reusable host buffers with their ctypes pointers, so the
-    latency path builds no arrays and looks nothing up twice per call."""
+    options): context, the scene / constraint packings, the parameter block of
+    the last PlanParams seen (every query usually carries its own PlanParams,
+    differing only in seed_offset, which travels separately) and reusable host
+    buffers with their ctypes pointers, so the latency path builds no arrays
+    and looks nothing up twice per call."""
 
-    __slots__ = ("objs", "ctx", "prm", "pc", "width", "pscene", "pspec", "s", "g", "seed", "res", "paths",
-                 "srcs", "args")
+    __slots__ = ("objs", "ctx", "params", "pkey", "prm", "pc", "width", "pscene", "pspec", "s", "g", "seed",
+                 "res", "paths", "srcs", "args")
 
     def __init__(self, problem, options):
-        self.objs = (problem.model, problem.scene, problem.spec, problem.params, options)
+        self.objs = (problem.model, problem.scene, problem.spec, options)
         self.ctx = kernels.context(problem.model, options.device)
-        self.prm = _params_struct(problem.params, options)
-        self.pc = pc = int(self.prm.path_capacity)
-        self.width = problem.params.width
         self.pscene = _scene_packed(problem.scene)
         self.pspec = None if problem.spec is None else problem.spec.packed
+        self.params = self.pkey = None
+        self.pc = -1
         n = self.ctx.n
         self.s = np.empty((1, n))
         self.g = np.empty((1, n))
         self.seed = np.zeros(1, np.int64)
         self.res = (_lib.Result * 1)()
-        self.paths = np.empty((1, pc, n))
-        self.srcs = np.empty((1, pc), np.int32)
-        self.args = (self.ctx.h, C.byref(self.prm), 1, _lib.ptr(self.s), _lib.ptr(self.g),
-                     _lib.ptr(self.seed, _lib._lp), self.res, _lib.ptr(self.paths), _lib.ptr(self.srcs, _lib._ip))
+
+    def use(self, params, options):
+        """Bind params (re-deriving the parameter block only when a field
+        other than seed_offset changed)."""
+        if params is self.params:
+            return
+        key = _params_getter()(params)
+        if key != self.pkey:
+            self.prm = _make_params(params, options)
+            self.width = params.width
+            pc = int(self.prm.path_capacity)
+            if pc != self.pc:
+                self.pc = pc
+                self.paths = np.empty((1, pc, self.ctx.n))
+                self.srcs = np.empty((1, pc), np.int32)
+            self.args = (self.ctx.h, C.byref(self.prm), 1, _lib.ptr(self.s), _lib.ptr(self.g),
+                         _lib.ptr(self.seed, _lib._lp), self.res, _lib.ptr(self.paths), _lib.ptr(self.srcs, _lib._ip))
+            self.pkey = key
+        self.params = params
 
 
 _TLS = threading.local()
@@ -656,13 +672,14 @@ def _session(problem, options) -> _Session:
     cache = getattr(_TLS, "sessions", None)
     if cache is None:
         cache = _TLS.sessions = {}
-    key = (id(problem.model), id(problem.scene), id(problem.spec), id(problem.params), id(options))
+    key = (id(problem.model), id(problem.scene), id(problem.spec), id(options))
     s = cache.get(key)
     if s is None or s.objs[0] is not problem.model or s.objs[1] is not problem.scene \
-            or s.objs[2] is not problem.spec or s.objs[3] is not problem.params or s.objs[4] is not options:
+            or s.objs[2] is not problem.spec or s.objs[3] is not options:
         if len(cache) > 256:
             cache.clear()
         s = cache[key] = _Session(problem, options)
+    s.use(problem.params, options)
     return s
 
 
