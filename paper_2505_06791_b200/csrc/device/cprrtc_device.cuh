@@ -26,12 +26,6 @@
 #endif
 
 #define CP_M ((CP_KIND == 0 ? 1 : 2) + (CP_ORIENT ? 3 : 0))
-#ifndef CP_ESTRIN
-#define CP_ESTRIN 1   // shorter dependency chains in the FP32 stage 1
-#endif
-#ifndef CP_DAMPED_ADJ
-#define CP_DAMPED_ADJ 0   // m = 4 damped solve by adjugate (one reciprocal) instead of 2x2 blocks
-#endif
 #define CP_NP ((CP_N % 2) ? CP_N : (CP_N + 1))   // odd row pitch: no bank conflicts
 #define CP_CHUNK 8
 #define CP_VOTE 4                    // lockstep CC: early-exit vote every CP_VOTE chunks
@@ -175,13 +169,6 @@ template <> __device__ __forceinline__ float cp_rotscale<float>(float s2, float 
     const bool sw = vn > rw;
     const float x = sw ? rw * ivn : vn * irw;
     const float u = x * x;
-#if CP_ESTRIN
-    // Estrin's scheme: depth 4 instead of Horner's 8 on the stage-1 chain
-    const float u2 = u * u, u4 = u2 * u2;
-    const float e0 = fmaf(-0.33333075046539307f, u, 1.0f), e1 = fmaf(-0.14203891158103943f, u, 0.19992651045322418f);
-    const float e2 = fmaf(-0.07506226748228073f, u, 0.1064186692237854f), e3 = fmaf(-0.016082055866718292f, u, 0.042713798582553864f);
-    const float p = fmaf(fmaf(fmaf(0.0028531861025840044f, u4, e3), u2, e2), u4, fmaf(e1, u2, e0));
-#else
     float p = 0.0028531861025840044f;
     p = fmaf(p, u, -0.016082055866718292f);
     p = fmaf(p, u, 0.042713798582553864f);
@@ -191,7 +178,6 @@ template <> __device__ __forceinline__ float cp_rotscale<float>(float s2, float 
     p = fmaf(p, u, 0.19992651045322418f);
     p = fmaf(p, u, -0.33333075046539307f);
     p = fmaf(p, u, 1.0f);
-#endif
     return sw ? 2.f * fmaf(-x, p, 1.5707963267948966f) * ivn : 2.f * p * irw;
 }
 
@@ -237,13 +223,6 @@ __device__ __forceinline__ void cp_orient_rotvec<float>(const Con<float>& c, con
     const bool sw = vn > ac;
     const float x = sw ? ac * ivn : vn * iac;
     const float u = x * x;
-#if CP_ESTRIN
-    // Estrin's scheme: depth 4 instead of Horner's 8 on the stage-1 chain
-    const float u2 = u * u, u4 = u2 * u2;
-    const float e0 = fmaf(-0.33333075046539307f, u, 1.0f), e1 = fmaf(-0.14203891158103943f, u, 0.19992651045322418f);
-    const float e2 = fmaf(-0.07506226748228073f, u, 0.1064186692237854f), e3 = fmaf(-0.016082055866718292f, u, 0.042713798582553864f);
-    const float p = fmaf(fmaf(fmaf(0.0028531861025840044f, u4, e3), u2, e2), u4, fmaf(e1, u2, e0));
-#else
     float p = 0.0028531861025840044f;
     p = fmaf(p, u, -0.016082055866718292f);
     p = fmaf(p, u, 0.042713798582553864f);
@@ -253,7 +232,6 @@ __device__ __forceinline__ void cp_orient_rotvec<float>(const Con<float>& c, con
     p = fmaf(p, u, 0.19992651045322418f);
     p = fmaf(p, u, -0.33333075046539307f);
     p = fmaf(p, u, 1.0f);
-#endif
     const float at = x * p;                                   // atan(x)
     const float half = sw ? 1.5707963267948966f - at : at;   // atan2(vn, |cth|)
     const float th = cth >= 0.f ? half : 3.14159265358979f - half;
@@ -321,14 +299,6 @@ template <class T> __device__ __forceinline__ T cp_so3_c2(T t2) {
 template <> __device__ __forceinline__ float cp_so3_c2<float>(float t2) {
     // minimax polynomial in t2 over [0, pi^2] (every rotation-vector angle),
     // max relative error 8e-8 in FP32: branch-free, no cancellation
-#if CP_ESTRIN
-    const float u2 = t2 * t2, u4 = u2 * u2;
-    const float e0 = fmaf(0.00138888880610466f, t2, 0.0833333358168602f);
-    const float e1 = fmaf(8.264817665804003e-07f, t2, 3.306901635369286e-05f);
-    const float e2 = fmaf(4.946845155728852e-10f, t2, 2.0997001470846044e-08f);
-    const float e3 = fmaf(-1.5192574032586031e-13f, t2, 1.8825586922677218e-11f);
-    return fmaf(fmaf(fmaf(3.002027066604379e-14f, u4, e3), u2, e2), u4, fmaf(e1, u2, e0));
-#else
     float p = 3.002027066604379e-14f;
     p = fmaf(p, t2, -1.5192574032586031e-13f);
     p = fmaf(p, t2, 1.8825586922677218e-11f);
@@ -338,7 +308,6 @@ template <> __device__ __forceinline__ float cp_so3_c2<float>(float t2) {
     p = fmaf(p, t2, 3.306901635369286e-05f);
     p = fmaf(p, t2, 0.00138888880610466f);
     return fmaf(p, t2, 0.0833333358168602f);
-#endif
 }
 
 // inverse left Jacobian of SO(3) (pure.py:348-366)
@@ -542,59 +511,13 @@ __device__ __forceinline__ bool cp_damped_f4(const float (*J)[CP_N], const float
     for (int i = 0; i < 4; i++)
 #pragma unroll
         for (int j = 0; j <= i; j++) {
-#if CP_ESTRIN
-            // even / odd k in two chains: depth ceil(n/2) + 1 instead of n
-            float acc0 = 0.f, acc1 = 0.f;
-#pragma unroll
-            for (int k = 0; k < CP_N; k += 2) {
-                acc0 = fmaf(J[i][k], J[j][k], acc0);
-                if (k + 1 < CP_N) acc1 = fmaf(J[i][k + 1], J[j][k + 1], acc1);
-            }
-            const float acc = acc0 + acc1;
-#else
             float acc = 0.f;
 #pragma unroll
             for (int k = 0; k < CP_N; k++) acc = fmaf(J[i][k], J[j][k], acc);
-#endif
             a[i][j] = a[j][i] = acc;
         }
     const float l2 = lam * lam;
     a[0][0] += l2; a[1][1] += l2; a[2][2] += l2; a[3][3] += l2;
-#if CP_DAMPED_ADJ
-    // adjugate / determinant from 2x2 minors (Laplace expansion by the
-    // complementary rows 0-1 / 2-3): one reciprocal on the chain instead of
-    // two, the unscaled solve adj(A) e overlapping it.  SPD test = the
-    // leading principal minors a00, s0, det3, det all positive (Sylvester),
-    // the condition the block elimination and the reference's Cholesky test.
-    {
-        const float a00 = a[0][0], a01 = a[0][1], a02 = a[0][2], a03 = a[0][3], a11 = a[1][1], a12 = a[1][2];
-        const float a13 = a[1][3], a22 = a[2][2], a23 = a[2][3], a33 = a[3][3];
-        const float s0 = fmaf(a00, a11, -a01 * a01), s1 = fmaf(a00, a12, -a01 * a02), s2 = fmaf(a00, a13, -a01 * a03);
-        const float s3 = fmaf(a01, a12, -a11 * a02), s4 = fmaf(a01, a13, -a11 * a03), s5 = fmaf(a02, a13, -a12 * a03);
-        const float c5 = fmaf(a22, a33, -a23 * a23), c4 = fmaf(a12, a33, -a13 * a23), c3 = fmaf(a12, a23, -a13 * a22);
-        const float c2 = fmaf(a02, a33, -a03 * a23), c1 = fmaf(a02, a23, -a03 * a22), c0 = fmaf(a02, a13, -a03 * a12);
-        const float det = (fmaf(s0, c5, -s1 * c4) + fmaf(s2, c3, s3 * c2)) + fmaf(-s4, c1, s5 * c0);
-        const float det3 = fmaf(a02, s3, fmaf(-a12, s1, a22 * s0));
-        const float idet = __fdividef(1.f, det);
-        const float e0 = e[0], e1 = e[1], e2 = e[2], e3 = e[3];
-        const float z0 = fmaf(fmaf(a11, c5, fmaf(-a12, c4, a13 * c3)), e0, fmaf(fmaf(-a01, c5, fmaf(a02, c4, -a03 * c3)), e1,
-                         fmaf(fmaf(a13, s5, fmaf(-a23, s4, a33 * s3)), e2, fmaf(-a12, s5, fmaf(a22, s4, -a23 * s3)) * e3)));
-        const float z1 = fmaf(fmaf(-a01, c5, fmaf(a12, c2, -a13 * c1)), e0, fmaf(fmaf(a00, c5, fmaf(-a02, c2, a03 * c1)), e1,
-                         fmaf(fmaf(-a03, s5, fmaf(a23, s2, -a33 * s1)), e2, fmaf(a02, s5, fmaf(-a22, s2, a23 * s1)) * e3)));
-        const float z2 = fmaf(fmaf(a01, c4, fmaf(-a11, c2, a13 * c0)), e0, fmaf(fmaf(-a00, c4, fmaf(a01, c2, -a03 * c0)), e1,
-                         fmaf(fmaf(a03, s4, fmaf(-a13, s2, a33 * s0)), e2, fmaf(-a02, s4, fmaf(a12, s2, -a23 * s0)) * e3)));
-        const float z3 = fmaf(fmaf(-a01, c3, fmaf(a11, c1, -a12 * c0)), e0, fmaf(fmaf(a00, c3, fmaf(-a01, c1, a02 * c0)), e1,
-                         fmaf(fmaf(-a03, s3, fmaf(a13, s1, -a23 * s0)), e2, fmaf(a02, s3, fmaf(-a12, s1, a22 * s0)) * e3)));
-        const float y0 = z0 * idet, y1 = z1 * idet, y2 = z2 * idet, y3 = z3 * idet;
-        const bool ok = a00 > 0.f && s0 > 0.f && det3 > 0.f && det > 0.f;
-#pragma unroll
-        for (int k = 0; k < CP_N; k++) {
-            const float g = fmaf(J[0][k], y0, fmaf(J[1][k], y1, fmaf(J[2][k], y2, J[3][k] * y3)));
-            step[k] = ok ? g : 0.f;
-        }
-        return ok;
-    }
-#endif
     // P^-1
     const float dp = fmaf(a[0][0], a[1][1], -a[0][1] * a[0][1]);
     const float idp = __fdividef(1.f, dp);
@@ -2237,15 +2160,51 @@ __device__ __forceinline__ int cp_scene_f4(const SceneSm& g) {
                   : 2 * cp_pad8(g.nb) + cp_pad8(g.ne);
 }
 
+// One contiguous global -> shared copy by the Tensor Memory Accelerator: a
+// single thread issues 1D bulk copies (cp.async.bulk, <= 32 KB each) that
+// complete on a shared-memory mbarrier carrying the byte count; every thread
+// waits on the barrier's phase (no per-thread loads, no CTA barrier after).
+// Up to three blocks (dst[i] <- src[i], bytes[i], multiples of 16) on one barrier.
+__device__ __forceinline__ void cp_bulk_to_smem(float4* const* dst, const float4* const* src, const unsigned* bytes,
+                                                int nblk) {
+    __shared__ __align__(8) unsigned long long bar;
+    const unsigned b = cp_smem_addr(&bar);
+    if (threadIdx.x == 0) {
+        asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(b) : "memory");
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        unsigned total = 0;
+        for (int k = 0; k < nblk; k++) total += bytes[k];
+        asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(b), "r"(total) : "memory");
+        for (int k = 0; k < nblk; k++) {
+            const unsigned d = cp_smem_addr(dst[k]);
+            for (unsigned off = 0; off < bytes[k]; off += 32768u) {
+                const unsigned n = bytes[k] - off < 32768u ? bytes[k] - off : 32768u;
+                asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+                             ::"r"(d + off), "l"(reinterpret_cast<const char*>(src[k]) + off), "r"(n), "r"(b)
+                             : "memory");
+            }
+        }
+    }
+    cp_mb_wait(&bar, 0);
+}
+
 // Stage the scene into shared memory.  Reference order: padded to whole
 // CP_CHUNKs with primitives 1e18 m away (never hit), so the check loop has no
-// bounds test.  Clustered: one contiguous copy (the host padded the chunks).
+// bounds test.  Clustered: one contiguous block (the host padded the chunks),
+// copied by TMA bulk copies.
 __device__ __forceinline__ SceneSm cp_stage_scene(const SceneSm& g, float4* sm) {
     SceneSm s = g;
     if (g.cull) {
         const int tot = cp_scene_f4(g);
-        for (int i = threadIdx.x; i < tot; i += blockDim.x) sm[i] = g.cl[i];
-        __syncthreads();
+        if (tot > 0) {
+            float4* d[1] = {sm};
+            const float4* sr[1] = {g.cl};
+            const unsigned n[1] = {(unsigned)tot * 16u};
+            cp_bulk_to_smem(d, sr, n, 1);
+        }
         s.cl = sm;
         return s;
     }
@@ -2255,11 +2214,16 @@ __device__ __forceinline__ SceneSm cp_stage_scene(const SceneSm& g, float4* sm) 
     float4* sp = sm + 2 * nbp;
     const float4 far = make_float4(1e18f, 1e18f, 1e18f, 0.f);
     const float4 zero = make_float4(0.f, 0.f, 0.f, 0.f);
-    for (int i = threadIdx.x; i < nbp; i += blockDim.x) {
-        bc[i] = i < g.nb ? g.box_c[i] : far;
-        bh[i] = i < g.nb ? g.box_h[i] : zero;
+    // the primitives by TMA bulk copies, the chunk padding by the threads
+    // (disjoint ranges), then one CTA barrier for the padding stores
+    for (int i = g.nb + threadIdx.x; i < nbp; i += blockDim.x) { bc[i] = far; bh[i] = zero; }
+    for (int i = g.ne + threadIdx.x; i < nep; i += blockDim.x) sp[i] = far;
+    {
+        float4* d[3] = {bc, bh, sp};
+        const float4* sr[3] = {g.box_c, g.box_h, g.sph};
+        const unsigned n[3] = {(unsigned)g.nb * 16u, (unsigned)g.nb * 16u, (unsigned)g.ne * 16u};
+        if (g.nb + g.ne > 0) cp_bulk_to_smem(d, sr, n, 3);
     }
-    for (int i = threadIdx.x; i < nep; i += blockDim.x) sp[i] = i < g.ne ? g.sph[i] : far;
     __syncthreads();
     s.box_c = bc; s.box_h = bh; s.sph = sp;
     return s;

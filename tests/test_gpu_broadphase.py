@@ -83,8 +83,10 @@ def test_broadphase_matches_lockstep(K, oracle, robot, scene):
 
 
 def test_broadphase_planner_paths(oracle):
-    """Planning through the 999-box shelf with the broad phase forced on:
-    solved paths re-validate in FP64 (dense motions collision-free)."""
+    """Planning through the 999-box shelf in both check orders (the clustered
+    broad phase and the reference's lockstep order): each must solve, over
+    three seeds, and every path re-validates in FP64 (dense motions
+    collision-free, on the manifold)."""
     from test_gpu_planner import _check_path
     from paper_2505_06791_b200.planner import DeviceOptions, PlanParams, PlanProblem, plan
     p = next(x for x in fx.plans() if x["id"] == "shelf_plane55_800")
@@ -92,10 +94,10 @@ def test_broadphase_planner_paths(oracle):
     sc = fx.scene("shelf_x111")
     kw = dict(p["params"])
     kw["max_iterations"] = 200_000
-    prob = PlanProblem(m, sc, sp, np.array(p["start"]), np.array(p["goal"]), PlanParams(**kw))
     for bp in (1, 0):
-        res = plan(prob, DeviceOptions(cc_broadphase=bp))
-        if res.solved:
+        for seed in range(3):
+            kw["seed_offset"] = seed * 10_000
+            prob = PlanProblem(m, sc, sp, np.array(p["start"]), np.array(p["goal"]), PlanParams(**kw))
+            res = plan(prob, DeviceOptions(cc_broadphase=bp))
+            assert res.solved, (bp, seed, res.status)
             _check_path(oracle, prob, res)
-    res = plan(prob, DeviceOptions(cc_broadphase=1))
-    assert res.solved, res.status
