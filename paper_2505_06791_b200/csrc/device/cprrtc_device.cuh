@@ -26,6 +26,14 @@
 #endif
 
 #define CP_M ((CP_KIND == 0 ? 1 : 2) + (CP_ORIENT ? 3 : 0))
+// packed box test clamp: 1 = FMNMX on the ALU pipe (vs r^2), 0 = t + |t| on
+// the FP32 pipe (squared sum 4x, vs 4 r^2).  r2 A/B on the 999-box CC kernel:
+// 2.18 vs 2.10 T checks/s (with the sphere pairs pre-packed, the FP32 pipe is
+// the tighter one, so the clamp goes to the ALU)
+#ifndef CP_CC_CLAMP_ALU
+#define CP_CC_CLAMP_ALU 1
+#endif
+#define CP_CC_RSCALE (CP_CC_CLAMP_ALU ? 1.f : 4.f)
 #define CP_NP ((CP_N % 2) ? CP_N : (CP_N + 1))   // odd row pitch: no bank conflicts
 #define CP_CHUNK 8
 #define CP_VOTE 4                    // lockstep CC: early-exit vote every CP_VOTE chunks
@@ -927,10 +935,11 @@ __device__ __forceinline__ bool cp_hit_sph(float cx, float cy, float cz, float r
 // scalar one (DESIGN.md section 3 has the instruction counts).
 //
 // spheres (cx, cy, cz packed) vs one box (centre c, half extent h):
-// cp_hit_box for both.  The clamp max(|d| - h, 0) is taken as u = t + |t| =
-// 2 max(t, 0) (t = |d| - h): two FP32-pipe adds with |.| operand modifiers
-// instead of an ALU-pipe FMNMX, and the squared sum (exactly 4x the scalar
-// one, a power-of-two scale) is compared with r4 = 4 r^2 -- the same verdict.
+// cp_hit_box for both.  The clamp max(|d| - h, 0) is an FMNMX (ALU pipe) or,
+// with CP_CC_CLAMP_ALU 0, u = t + |t| = 2 max(t, 0) (t = |d| - h: FP32-pipe
+// adds with |.| operand modifiers) whose squared sum, exactly 4x the scalar
+// one (a power-of-two scale), is compared with 4 r^2 -- the same verdict
+// either way; r40 / r41 are the radii squared times CP_CC_RSCALE.
 __device__ __forceinline__ void cp_hit_box2(cp_f2 cx, cp_f2 cy, cp_f2 cz, float r40, float r41, float4 c, float4 h,
                                             bool& a0, bool& a1) {
     float dx0, dx1, dy0, dy1, dz0, dz1;
@@ -939,9 +948,14 @@ __device__ __forceinline__ void cp_hit_box2(cp_f2 cx, cp_f2 cy, cp_f2 cz, float 
     cp_upk(cp_sub2(cz, cp_pk(c.z, c.z)), dz0, dz1);
     const float tx0 = fabsf(dx0) - h.x, tx1 = fabsf(dx1) - h.x, ty0 = fabsf(dy0) - h.y, ty1 = fabsf(dy1) - h.y;
     const float tz0 = fabsf(dz0) - h.z, tz1 = fabsf(dz1) - h.z;
-    const cp_f2 ux = cp_pk(tx0 + fabsf(tx0), tx1 + fabsf(tx1));
-    const cp_f2 uy = cp_pk(ty0 + fabsf(ty0), ty1 + fabsf(ty1));
-    const cp_f2 uz = cp_pk(tz0 + fabsf(tz0), tz1 + fabsf(tz1));
+#if CP_CC_CLAMP_ALU
+    auto u2 = [](float t) { return fmaxf(t, 0.f); };      // FMNMX (ALU pipe); compare with r^2
+#else
+    auto u2 = [](float t) { return t + fabsf(t); };        // 2 max(t, 0) on the FP32 pipe; compare with 4 r^2
+#endif
+    const cp_f2 ux = cp_pk(u2(tx0), u2(tx1));
+    const cp_f2 uy = cp_pk(u2(ty0), u2(ty1));
+    const cp_f2 uz = cp_pk(u2(tz0), u2(tz1));
     float s0, s1;
     cp_upk(cp_fma2(ux, ux, cp_fma2(uy, uy, cp_mul2(uz, uz))), s0, s1);
     a0 |= s0 < r40;
@@ -987,7 +1001,7 @@ __device__ __forceinline__ void cp_env_pass(const Team& tm, const float4* sp, co
         // +1e18 padding primitives of the staged scene
         const float4 c1 = two ? sp[s + 1] : make_float4(-3e18f, -3e18f, -3e18f, 0.f);
         const float ra = cp_rad_tab[s] + margin, rb = (two ? cp_rad_tab[s + 1] : 0.f) + margin;
-        const float r0 = ra * ra, r1 = rb * rb, r40 = 4.f * r0, r41 = 4.f * r1;
+        const float r0 = ra * ra, r1 = rb * rb, r40 = CP_CC_RSCALE * r0, r41 = CP_CC_RSCALE * r1;
         const SPair pp = spp[s >> 1];
         const cp_f2 px = pp.x, py = pp.y, pz = pp.z, pr = cp_pk(ra, rb);
         const int rb0 = s * E, rb1 = (s + 1) * E;
@@ -1206,8 +1220,8 @@ __device__ __noinline__ ValOut cp_validate_cull(const Team tm, const float (*seg
         for (int s = 0; s + 1 < CP_S; s += 2) {
             const float4 a = CP_SPH(s), b = CP_SPH(s + 1);
             bool h0 = false, h1 = false;
-            cp_hit_box2(cp_pk(a.x, b.x), cp_pk(a.y, b.y), cp_pk(a.z, b.z), 4.f * (a.w * a.w), 4.f * (b.w * b.w), bc,
-                        bh, h0, h1);
+            cp_hit_box2(cp_pk(a.x, b.x), cp_pk(a.y, b.y), cp_pk(a.z, b.z), CP_CC_RSCALE * (a.w * a.w),
+                        CP_CC_RSCALE * (b.w * b.w), bc, bh, h0, h1);
             m[s >> 5] |= (h0 ? 1u << (s & 31) : 0u) | (h1 ? 1u << ((s + 1) & 31) : 0u);
         }
         if (CP_S & 1) {
