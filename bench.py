@@ -197,6 +197,10 @@ def dist_setup():
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    if os.environ.get("CPRRTC_BENCH_ONE_GPU") == "1":
+        # test mode only (exercises the N > 1 code path on a one-GPU box):
+        # every rank plans on cuda:0; such a run is not a scaling measurement
+        local = 0
     if world > 1:
         import torch.distributed as dist
         dist.init_process_group("gloo")
@@ -230,7 +234,7 @@ def _relaunch(args):
     """--gpus N > 1 outside torchrun: one rank per GPU under
     torch.distributed.run (the driver's own launch form)."""
     have = _visible_gpus()
-    if have < args.gpus:
+    if have < args.gpus and os.environ.get("CPRRTC_BENCH_ONE_GPU") != "1":
         sys.exit(f"bench.py: --gpus {args.gpus} but only {have} CUDA device(s) are visible")
     import socket
     with socket.socket() as s:
@@ -850,13 +854,16 @@ def main():
     args = ap.parse_args()
     if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
         _relaunch(args)
+    if os.environ.get("CPRRTC_BENCH_ONE_GPU") == "1":
+        print("bench.py: CPRRTC_BENCH_ONE_GPU=1 -- every rank on cuda:0 (code-path test, not a measurement)",
+              file=sys.stderr)
     world, rank, local = dist_setup()
     if world != args.gpus:
         sys.exit(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={world}")
     if args.impl == "reference":
         line = run_reference(args, world, rank)
     else:
-        if world > 1 and _visible_gpus() <= local:
+        if world > 1 and _visible_gpus() <= local and os.environ.get("CPRRTC_BENCH_ONE_GPU") != "1":
             sys.exit(f"bench.py: rank {rank} needs cuda:{local}, {_visible_gpus()} device(s) visible")
         line = run_b200(args, world, rank, local)
     if rank == 0 and line is not None:

@@ -101,3 +101,23 @@ def test_two_ranks_plan_their_shards():
         assert [e[0] for e in everyone] == [0, 1]
         for _, solved, bad, dev_ms in everyone:
             assert solved >= 60 and bad == 0 and dev_ms > 0
+
+
+@pytest.mark.gpu
+def test_bench_two_ranks_one_gpu(tmp_path):
+    """bench.py --gpus 2 end to end (relaunch under torch.distributed.run,
+    gloo control plane, per-rank shards, max-over-ranks timing), both ranks on
+    cuda:0 via the CPRRTC_BENCH_ONE_GPU test mode."""
+    import json
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = dict(os.environ, CPRRTC_BENCH_ONE_GPU="1")
+    p = subprocess.run([sys.executable, os.path.join(root, "bench.py"), "--gpus", "2", "--steps", "1", "--warmup",
+                        "3", "--queries", "4", "--no-extras", "--no-cpu", "--records-dir", str(tmp_path)],
+                       capture_output=True, text=True, timeout=900, env=env, cwd=root)
+    assert p.returncode == 0, p.stderr[-3000:]
+    line = json.loads(p.stdout.strip().splitlines()[-1])
+    assert line["n_gpus"] == 2 and line["queries"] == 8
+    assert line["throughput"]["value"] > 0 and line["throughput"]["success_rate"] > 0.95
+    assert "2 GPU(s)" in line["throughput"]["config"]
