@@ -656,75 +656,6 @@ __device__ __noinline__ float cp_err_norm(const float* q) {
 // (B200): a plain load cost ~300 cycles per iteration of ~1500 (ptxas turned
 // its value into a predicate right after issue, stalling on the round trip),
 // and a same-iteration cp.async.wait_all was hoisted the same way.
-#ifndef CP_PIPE
-#define CP_PIPE 1
-#endif
-// The constrained, untraced iterations of Alg. 1, software-pipelined: stage-1
-// part A of iteration k+1 is evaluated at xn (lane t's update of iteration k)
-// right after part B of iteration k, without waiting for the team vote.  A
-// lane whose row does not freeze this iteration gets exactly xn as its next
-// row, so A(xn) is its next stage-1 part A; a row that freezes is inactive
-// from then on and its speculative A is discarded (the loop is branch-free,
-// every lane evaluates anyway).  Only part B (the smoothing term / validity,
-// which needs row t-1) waits for the vote, and it is a few dozen
-// instructions: the vote, the prefix scan, the row selects and the shuffle of
-// row t-1 overlap part A instead of sitting between two stage-1 evaluations.
-// The values computed are those of cp_alg1_loop<true, false>; the final
-// iteration's speculative part A is wasted work.
-__device__ __forceinline__ void cp_alg1_loop_pipe(const Team tm, int W, const ProjArgs& pa, float tau_sm, float* xc,
-                                                  int& prog, int& iters, bool& ok, bool& aborted, unsigned& s1,
-                                                  const int* stop_flag, int* pslot) {
-    const int t = (int)tm.lane;
-    const bool row = t < W;
-    const unsigned full = (W >= 32) ? 0xffffffffu : ((1u << W) - 1u);
-    const bool poll = stop_flag && pslot && t == 0;
-    const unsigned long long sbase = (unsigned long long)stop_flag & ~15ull;
-    const unsigned slot = pslot ? (unsigned)__cvta_generic_to_shared(pslot) : 0u;
-    const unsigned soff = (unsigned)((unsigned long long)stop_flag - sbase);
-    unsigned par = poll ? (unsigned)pslot[8] : 0u;
-    Stage1A a;
-    cp_stage1a(pa, xc, a);
-    for (int it = 1; it <= pa.max_iters; it++) {
-        const bool act = row && t > prog;
-        const unsigned put = slot + 16u * (par & 1u), get = slot + 16u * ((par + 1u) & 1u) + soff;
-        par ^= 1u;
-        asm volatile("{ .reg .pred p; setp.ne.u32 p, %2, 0; @p cp.async.cg.shared.global [%0], [%1], 16; "
-                     "cp.async.commit_group; }" ::"r"(put), "l"(sbase), "r"((unsigned)poll));
-        float xp[CP_N], xn[CP_N];
-#pragma unroll
-        for (int k = 0; k < CP_N; k++) xp[k] = __shfl_up_sync(tm.mask, xc[k], 1, CP_G);
-        const bool valid = act && cp_stage1b(pa, a, xc, xp, tau_sm, xn);
-        s1 += act ? 1u : 0u;
-        Stage1A an;
-        cp_stage1a(pa, xn, an);   // next iteration's part A, speculatively at xn
-        int sf;
-        asm volatile("{ .reg .pred p; setp.ne.u32 p, %2, 0; cp.async.wait_group 1; mov.u32 %0, 0; "
-                     "@p ld.shared.b32 %0, [%1]; }" : "=r"(sf) : "r"(get), "r"((unsigned)(poll && it > 1)));
-        const unsigned vm = tm.ballot(valid || sf != 0) & full;
-        const unsigned hi = vm & ~((2u << prog) - 1u);              // literal-gap
-        const int np1 = hi ? 31 - __clz(hi) : prog;
-        const int run = __ffs(~(vm >> (prog + 1))) - 1;               // contiguous prefix
-        const int np0 = min(prog + (run < 0 ? 32 : run), W - 1);
-        const int np = pa.mode == 1 ? np1 : np0;
-        if (np == W - 1) {
-            ok = true;
-            iters = it;
-            prog = np;
-            break;
-        }
-        if (vm & 1u) {   // the query is over: abandon
-            aborted = true;
-            break;
-        }
-        const bool upd = row && t > np;
-#pragma unroll
-        for (int k = 0; k < CP_N; k++) xc[k] = upd ? xn[k] : xc[k];
-        a = an;   // exact for every row that stays active (upd); frozen rows never use it
-        prog = np;
-    }
-    if (poll) pslot[8] = (int)par;
-}
-
 template <bool UNC, bool TRACE>
 __device__ __forceinline__ void cp_alg1_loop(const Team tm, int W, const ProjArgs& pa, float tau_sm,
                                              float* xc, int& prog, int& iters, bool& ok, bool& aborted,
@@ -917,7 +848,6 @@ __device__ __noinline__ ProjRes cp_project_body(const Team tm, float (*seg)[CP_N
             else cp_alg1_loop<true, false>(tm, W, pa, tau_sm, xc, prog, iters, ok, aborted, s1, stop_flag, poll_slot, nullptr, nullptr);
         } else {
             if (trace) cp_alg1_loop<false, true>(tm, W, pa, tau_sm, xc, prog, iters, ok, aborted, s1, stop_flag, poll_slot, trace, trace_prog);
-            else if (CP_PIPE) cp_alg1_loop_pipe(tm, W, pa, tau_sm, xc, prog, iters, ok, aborted, s1, stop_flag, poll_slot);
             else cp_alg1_loop<false, false>(tm, W, pa, tau_sm, xc, prog, iters, ok, aborted, s1, stop_flag, poll_slot, nullptr, nullptr);
         }
         tm.sync();
