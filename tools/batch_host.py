@@ -31,6 +31,10 @@ for step in range(20):
     rows.append((wall, r.wall_ms, tot, kern))
 a = np.array(rows)
 print("median ms: wall %.3f  C call %.3f  device %.3f  plan kernel %.3f" % tuple(np.median(a, axis=0)))
+q = r.device_ms
+print("per-query device ms (last batch): p10 %.3f  median %.3f  p90 %.3f  p99 %.3f  max %.3f; solved %d / %d; "
+      "samples per query median %d" % (np.percentile(q, 10), np.median(q), np.percentile(q, 90), np.percentile(q, 99),
+                                       q.max(), int(r.solved.sum()), len(q), int(np.median(r.stats[:, 0]))))
 s, g, seeds = bench.batch_arrays(7)
 cProfile.run("for _ in range(20): plan_many(m, sc, sp, s, g, seeds, prm)", "/tmp/bh.prof")
 pstats.Stats("/tmp/bh.prof").sort_stats("tottime").print_stats(12)
