@@ -78,8 +78,9 @@ def _revalidate_rate(M, probs, results):
 
 
 def test_reference_revalidate_path_on_gpu_paths(M):
-    """Every GPU path of configs[1] (100 upright pairs) and configs[0]
-    (rand10) through the reference's FP64 revalidate_path."""
+    """Every GPU path of configs[1] (100 upright pairs), configs[0] (rand10),
+    configs[3] (arm8_dense, line) and configs[2] (999-box shelf) through the
+    reference's FP64 revalidate_path."""
     from paper_2505_06791_b200.planner import PlanParams, PlanProblem, plan_batch
     m, sc, sp = fx.robot("arm7"), fx.scene("table"), fx.spec("upright")
     prs = fx.pairs()
@@ -96,11 +97,35 @@ def test_reference_revalidate_path_on_gpu_paths(M):
                                           seed_offset=i * 10_000)) for i in range(3)]
     res0 = [plan_batch([p])[0] for p in probs0]
     ok0, n0, bad0 = _revalidate_rate(M, probs0, res0)
+    # configs[3] (arm8_dense: 36 spheres, 96 self pairs, line constraint) and
+    # configs[2] (the shelf densified to 999 boxes: arm7 / arm8 reaches and the
+    # plane sweep), a few seeds each
+    probs3, res3 = [], []
+    m8, sp8 = fx.robot("arm8_dense"), fx.spec("table_line_8")
+    for i in np.nonzero(fx.dense8_feasible())[0]:
+        p = PlanProblem(m8, sc, sp8, prs["dense8_line_start"][i], prs["dense8_line_goal"][i],
+                        PlanParams(width=16, max_iterations=200_000, time_budget_ms=3000.0, seed_offset=int(i) * 10_000))
+        probs3.append(p)
+        res3.append(plan_batch([p])[0])
+    ok3, n3, bad3 = _revalidate_rate(M, probs3, res3)
+    shelf = fx.scene("shelf_x111")
+    probs2, res2 = [], []
+    for key, rob, spn in (("shelf_arm7", "arm7", None), ("shelf_arm8", "arm8", None), ("shelf_sweep", "arm7", "plane55")):
+        for i in range(len(prs[f"{key}_seed"])):
+            for seed in range(2):
+                p = PlanProblem(fx.robot(rob), shelf, None if spn is None else fx.spec(spn), prs[f"{key}_start"][i],
+                                prs[f"{key}_goal"][i], PlanParams(width=16, max_iterations=200_000,
+                                                                  time_budget_ms=3000.0, seed_offset=seed * 10_000))
+                probs2.append(p)
+                res2.append(plan_batch([p])[0])
+    ok2, n2, bad2 = _revalidate_rate(M, probs2, res2)
     print(f"\nreference FP64 revalidate_path: configs[1] {ok1}/{n1} = {ok1 / max(1, n1):.3f} "
-          f"(failed {bad1}), configs[0] {ok0}/{n0} = {ok0 / max(1, n0):.3f} (failed {bad0})")
-    assert n1 >= 80 and n0 >= 28
+          f"(failed {bad1}), configs[0] {ok0}/{n0} = {ok0 / max(1, n0):.3f} (failed {bad0}), "
+          f"configs[3] {ok3}/{n3} (failed {bad3}), configs[2] 999 boxes {ok2}/{n2} (failed {bad2})")
+    assert n1 >= 80 and n0 >= 28 and n3 == len(probs3) and n2 == len(probs2)
     assert ok0 == n0                     # unconstrained: FP64 re-derivation is interpolation + CC
     assert ok1 >= 0.98 * n1, (ok1, n1)     # measured on B200 (r2): 86/86
+    assert ok3 >= 0.9 * n3 and ok2 >= 0.9 * n2, (ok3, n3, ok2, n2)   # measured (r2): 9/9, 8/8
 
 
 def test_selector_patch_acceptance_criteria():
