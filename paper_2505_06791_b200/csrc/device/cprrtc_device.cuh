@@ -1661,28 +1661,15 @@ __device__ __forceinline__ int cp_append(const Team& tm, const PlanArgs& A, Quer
         if (tm.lane == 0) { atomicExch(&Q.overflow, 1); atomicExch(&Q.stop, 1); }
         return -1;
     }
-    // publication order: the parent, then coordinate 0, which lane 0 stores
-    // itself with release semantics (ordered after its parent store).  A node counts as present only once every
-    // coordinate is non-NaN, so whoever sees it (NN scan, connect, extraction
-    // after its own fence) also sees its parent -- the reset kernel never
-    // clears parents[], so a stale parent would otherwise be readable.
-#ifndef CP_APPEND_ORDER
-#define CP_APPEND_ORDER 2   // 2: coordinate 0 by st.release; 1: __threadfence; 0: unordered (A/B only)
-#endif
+    // Plain stores, no ordering between them: coordinates are published by
+    // being non-NaN (a reader skips a node until every coordinate is), the
+    // parent by being >= 0 -- the reset kernel returns every used slot to NaN /
+    // -1 after each run, and the path extraction waits for a parent it reads
+    // as -1 (the store of a node it can see is in flight), so no reader can
+    // take a previous run's parent and no writer pays a fence.
     float* row = cp_tree(A, qi, k) + idx;
-    if (tm.lane == 0) {
-        cp_par(A, qi, k)[idx] = par;
-#if CP_APPEND_ORDER == 2
-        asm volatile("st.release.gpu.global.f32 [%0], %1;" :: "l"(row), "f"(q[0]) : "memory");
-#else
-#if CP_APPEND_ORDER == 1
-        __threadfence();
-#endif
-        row[0] = q[0];
-#endif
-    } else if ((int)tm.lane < CP_N) {
-        row[(size_t)tm.lane * A.cap] = q[tm.lane];
-    }
+    if (tm.lane == 0) cp_par(A, qi, k)[idx] = par;
+    if ((int)tm.lane < CP_N) row[(size_t)tm.lane * A.cap] = q[tm.lane];
     tm.sync();
     return idx;
 }
@@ -2288,19 +2275,29 @@ __device__ __noinline__ void cp_extract_path(const Team tm, const PlanArgs& A, i
     // the two parent chains are walked concurrently: lane 0 the start tree
     // into ch[0..), lane 1 the goal tree into ch[path_cap - 1] downwards
     const int m0 = cp_ldvol(&Q.meet[0]), m1 = cp_ldvol(&Q.meet[1]);
-    __threadfence();   // pairs with cp_append's fence: chain nodes seen => their parents seen
+    // a chain node is visible, so its parent store is issued: a -1 (the reset
+    // value) means it has not landed yet -- read again until it has
+    auto parent_of = [](const int* pp, int i) {
+        int p = cp_ldvol(pp + i);
+        while (p < 0) p = cp_ldvol(pp + i);
+        return p;
+    };
     int cnt = 0;
     if (lane == 0) {
-        for (int i = m0;; i = __ldcg(ps + i)) {   // start chain, meet first
+        for (int i = m0;;) {   // start chain, meet first
             if (cnt < path_cap) ch[cnt] = i;
             cnt++;
-            if (__ldcg(ps + i) == i) break;
+            const int p = parent_of(ps, i);
+            if (p == i) break;
+            i = p;
         }
     } else if (lane == 1) {
-        for (int i = m1;; i = __ldcg(pg + i)) {   // goal chain, meet first, stored from the end
+        for (int i = m1;;) {   // goal chain, meet first, stored from the end
             if (cnt < path_cap) ch[path_cap - 1 - cnt] = (1 << 30) | i;
             cnt++;
-            if (__ldcg(pg + i) == i) break;
+            const int p = parent_of(pg, i);
+            if (p == i) break;
+            i = p;
         }
     }
     ca = tm.bcast(cnt, 0);
@@ -2605,16 +2602,18 @@ extern "C" __global__ void __launch_bounds__(64) cp_check_kernel(const __grid_co
 
 // Reset the node slots used by the previous run to NaN (publication marker),
 // and the stop / setup words for the next run's concurrent endpoint checks.
-extern "C" __global__ void cp_reset_kernel(QueryState* qs, float* trees, int cap, int nq) {
+extern "C" __global__ void cp_reset_kernel(QueryState* qs, float* trees, int* parents, int cap, int nq) {
     for (int qk = blockIdx.y; qk < 2 * nq; qk += gridDim.y) {
         const int qi = qk >> 1, k = qk & 1;
         const int h = min(qs[qi].hwm[k], cap);
         if (k == 0 && blockIdx.x == 0 && threadIdx.x == 0) { qs[qi].stop = 0; qs[qi].setup_code = 0; }
         float* base = trees + (size_t)qk * CP_N * cap;
+        int* pb = parents + (size_t)qk * cap;
         const float nan = __int_as_float(0x7fffffff);
-        for (int d = 0; d < CP_N; d++)
-            for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < h; i += gridDim.x * blockDim.x)
-                base[(size_t)d * cap + i] = nan;
+        for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < h; i += gridDim.x * blockDim.x) {
+            pb[i] = -1;
+            for (int d = 0; d < CP_N; d++) base[(size_t)d * cap + i] = nan;
+        }
     }
 }
 

@@ -1211,6 +1211,7 @@ static int ensure_plan_buffers(Ctx* c, int nq, int cap, int path_cap) {
             if (g.exec) cudaGraphExecDestroy(g.exec);
         c->graphs.clear();
         CUDA_TRY(cudaMemsetAsync(c->trees.p, 0xff, tree_bytes, c->stream));   // NaN = unpublished
+        CUDA_TRY(cudaMemsetAsync(c->parents.p, 0xff, (size_t)nq * 2 * cap * sizeof(int), c->stream));   // -1
         CUDA_TRY(cudaMemsetAsync(c->qs.p, 0, (size_t)nq * sizeof(QueryState), c->stream));
         c->nq_alloc = nq;
         c->cap_alloc = cap;
@@ -1438,8 +1439,9 @@ static int plan_launch(Ctx* c, const cprrtc_params* prm, int B, const double* st
             // host waits on ev[3] only, so this overlaps the host's result handling)
             QueryState* qs = c->qs.as<QueryState>();
             float* tr = c->trees.as<float>();
+            int* pa = c->parents.as<int>();
             int capv = cap, nq = B;
-            void* args[] = {&qs, &tr, &capv, &nq};
+            void* args[] = {&qs, &tr, &pa, &capv, &nq};
             rc = rc ? rc : launch(c, m, "cp_reset_kernel", 8, (unsigned)std::min(2 * B, 65535), 256, 0, args);
         }
         cudaGraph_t graph = nullptr;
@@ -1693,6 +1695,7 @@ int cprrtc_step(void* p, const cprrtc_params* prm, int op, int N, const double* 
         for (int k = 0; k < n; k++) soa[(size_t)k * cap + i] = (float)nodes[(size_t)i * n + k];
     CUDA_TRY(cudaMemcpyAsync(c->trees.p, soa.data(), soa.size() * 4, cudaMemcpyHostToDevice, c->stream));
     CUDA_TRY(cudaMemcpyAsync(c->parents.p, parents, (size_t)N * 4, cudaMemcpyHostToDevice, c->stream));
+    CUDA_TRY(cudaMemsetAsync(c->parents.as<int>() + N, 0xff, (size_t)(cap - N) * 4, c->stream));   // -1: unpublished
     QueryState Q;
     CUDA_TRY(cudaMemcpyAsync(&Q, c->qs.p, sizeof Q, cudaMemcpyDeviceToHost, c->stream));
     CUDA_TRY(cudaStreamSynchronize(c->stream));
