@@ -1185,6 +1185,9 @@ __device__ __forceinline__ unsigned cp_team_or(const Team& tm, unsigned v) {
 // index), else a local array (dynamically indexed: the 36-sphere arm).
 #define CP_SREG_MAX 16
 #define CP_SREG (CP_S > 0 && CP_S <= CP_SREG_MAX)
+#ifndef CP_NARROW_PAIRS
+#define CP_NARROW_PAIRS 1   // register path: narrow phase by packed sphere pairs (else bit loop + select chain)
+#endif
 
 __device__ __noinline__ ValOut cp_validate_cull(const Team tm, const float (*seg)[CP_NP], int W, int t_first,
                                                 bool flag_on, float margin, const SceneSm sc) {
@@ -1279,6 +1282,27 @@ __device__ __noinline__ ValOut cp_validate_cull(const Team tm, const float (*seg
             bound_mask(bc, bh, m);
             bound += CP_S;
         }
+#if CP_SREG && CP_NARROW_PAIRS
+        {   // sphere pairs with a reaching member test the 8 boxes packed (no
+            // select chain for a runtime sphere index, no per-sphere loop)
+            const unsigned um = cp_team_or(tm, m[0]);
+#pragma unroll
+            for (int s = 0; s < CP_S; s += 2) {
+                if ((um >> s) & 3u) {
+                    const float4 a = CP_SPH(s), b = CP_SPH(s + 1 < CP_S ? s + 1 : s);
+                    const cp_f2 px = cp_pk(a.x, b.x), py = cp_pk(a.y, b.y), pz = cp_pk(a.z, b.z);
+                    const float ra = CP_CC_RSCALE * (a.w * a.w), rb = CP_CC_RSCALE * (b.w * b.w);
+                    bool h0 = false, h1 = false;
+#pragma unroll
+                    for (int j = 0; j < CP_CHUNK; j++)
+                        cp_hit_box2(px, py, pz, ra, rb, cp_lds4(ch + 2 + j), cp_lds4(ch + 2 + CP_CHUNK + j), h0, h1);
+                    const unsigned mine = (m[0] >> s) & (s + 1 < CP_S ? 3u : 1u);
+                    hit |= ((mine & 1u) && h0) || ((mine & 2u) && h1);
+                    narrow += CP_CHUNK * __popc(mine);
+                }
+            }
+        }
+#else
 #pragma unroll
         for (int w = 0; w < (CP_S + 31) / 32; w++) {
             unsigned um = cp_team_or(tm, m[w]);
@@ -1295,6 +1319,7 @@ __device__ __noinline__ ValOut cp_validate_cull(const Team tm, const float (*seg
                 if ((m[w] >> (s & 31)) & 1u) { hit |= any; narrow += CP_CHUNK; }
             }
         }
+#endif
         if (flag_on && tm.any(hit)) stop = true;   // the shared collision flag
     }
     }
@@ -1320,6 +1345,24 @@ __device__ __noinline__ ValOut cp_validate_cull(const Team tm, const float (*seg
             bound_mask(bc, bh, m);
             bound += CP_S;
         }
+#if CP_SREG && CP_NARROW_PAIRS
+        {
+            const unsigned um = cp_team_or(tm, m[0]);
+#pragma unroll
+            for (int s = 0; s < CP_S; s += 2) {
+                if ((um >> s) & 3u) {
+                    const float4 a = CP_SPH(s), b = CP_SPH(s + 1 < CP_S ? s + 1 : s);
+                    const cp_f2 px = cp_pk(a.x, b.x), py = cp_pk(a.y, b.y), pz = cp_pk(a.z, b.z), pr = cp_pk(a.w, b.w);
+                    bool h0 = false, h1 = false;
+#pragma unroll
+                    for (int j = 0; j < CP_CHUNK; j++) cp_hit_sph2(px, py, pz, pr, cp_lds4(ch + 2 + j), h0, h1);
+                    const unsigned mine = (m[0] >> s) & (s + 1 < CP_S ? 3u : 1u);
+                    hit |= ((mine & 1u) && h0) || ((mine & 2u) && h1);
+                    narrow += CP_CHUNK * __popc(mine);
+                }
+            }
+        }
+#else
 #pragma unroll
         for (int w = 0; w < (CP_S + 31) / 32; w++) {
             unsigned um = cp_team_or(tm, m[w]);
@@ -1334,6 +1377,7 @@ __device__ __noinline__ ValOut cp_validate_cull(const Team tm, const float (*seg
                 if ((m[w] >> (s & 31)) & 1u) { hit |= any; narrow += CP_CHUNK; }
             }
         }
+#endif
         if (flag_on && tm.any(hit)) stop = true;
     }
     }
