@@ -32,6 +32,7 @@ import ctypes as C
 import math
 import threading
 import time
+import weakref
 from contextlib import contextmanager
 from collections.abc import Sequence
 from dataclasses import dataclass, field, replace
@@ -369,13 +370,15 @@ class BatchResult(Sequence):
     itself)."""
 
     def __init__(self, a, offsets, rows, sources, starts, goals, wall_ms, single):
-        self.codes = a["status"].copy()
-        self.setup_codes = a["setup_code"].copy()
+        # a / offsets / rows / sources are views of a result arena this object
+        # holds (planner._arena): the arena is reused only once it is dropped
+        self.codes = a["status"]
+        self.setup_codes = a["setup_code"]
         self.path_len = np.where(self.codes == 0, a["path_len"], 0)
         self.offsets = offsets
         self.nodes = np.stack([a["ns"], a["ng"]], axis=1)
-        self.device_ms = a["device_ms"].copy()
-        self.stats = a["stats"].copy()
+        self.device_ms = a["device_ms"]
+        self.stats = a["stats"]
         self.rows, self.sources = rows, sources
         self.starts, self.goals = starts, goals
         self.wall_ms = wall_ms
@@ -453,7 +456,8 @@ def plan_many(model, scene, spec, starts, goals, seed_offsets, params: PlanParam
         raise ValueError("seed_offset must be >= 0")
     prm = _params_struct(params, options)
     pc = int(prm.path_capacity)
-    res, offsets, paths, srcs = _out_buffers(B, pc, n)
+    arena = _arena(B, pc, n)
+    res, offsets, paths, srcs = arena.res, arena.offsets, arena.paths, arena.srcs
     devs = tuple(int(d) for d in devices) if devices is not None else ()
     if len(devs) > 1:
         with _bound_many(like, devs) as ctxs:
@@ -473,7 +477,7 @@ def plan_many(model, scene, spec, starts, goals, seed_offsets, params: PlanParam
         srcv = np.zeros(int(offsets[B]), np.int32)
         for i in np.nonzero(L > 1)[0]:
             srcv[offsets[i]:offsets[i] + L[i] - 1] = sv[i, :L[i] - 1]
-        return _batch_result(res, offsets, rows, srcv, starts, goals, wall, B, pc)
+        return _batch_result(arena, res, offsets.copy(), rows, srcv, starts, goals, wall, B, pc)
     else:
         opt = options if not devs else replace(options, device=devs[0])
         with _bound(like, opt) as ctx:
@@ -485,16 +489,19 @@ def plan_many(model, scene, spec, starts, goals, seed_offsets, params: PlanParam
                        "plan")
             wall = (time.perf_counter() - t0) * 1e3
     tot = int(offsets[B])
-    # the packed rows and sources leave the reused output buffers (one
-    # contiguous copy each)
-    return _batch_result(res, offsets.copy(), paths[:tot].copy(), srcs[:tot].copy(), starts, goals, wall, B, pc)
+    # no copies: the result keeps views of the arena the device results were
+    # written to, and owns it until dropped
+    return _batch_result(arena, res, offsets, paths[:tot], srcs[:tot], starts, goals, wall, B, pc)
 
 
-def _batch_result(res, offsets, rows, sources, starts, goals, wall, B, pc):
+def _batch_result(arena, res, offsets, rows, sources, starts, goals, wall, B, pc):
     a = np.frombuffer(res, dtype=_RESULT_DT)
     if (a["status"] == 4).any():
         raise RuntimeError(f"solution path longer than path_capacity={pc}")
-    return BatchResult(a, offsets, rows, sources, starts, goals, wall, single=(B == 1))
+    out = BatchResult(a, offsets, rows, sources, starts, goals, wall, single=(B == 1))
+    out._arena = arena
+    arena.owner = weakref.ref(out)
+    return out
 
 
 class _Like:
@@ -709,22 +716,37 @@ def _plan_one(problem: PlanProblem, options: DeviceOptions, return_dense: bool) 
     return res
 
 
-_OUT: dict = {}
+class _Arena:
+    """Host result buffers of one batch launch: the result structs, path
+    offsets (B+1), and the packed path rows / sources sized for the worst case
+    B * path_capacity (virtual memory: only the rows a batch writes are ever
+    touched).  The BatchResult built on it keeps views and owns it; a later
+    call reuses it only after that result is gone (no copy-out, no fresh
+    page faults per call)."""
+
+    __slots__ = ("res", "offsets", "paths", "srcs", "owner")
+
+    def __init__(self, B, pc, n):
+        self.res = (_lib.Result * B)()
+        self.offsets = np.zeros(B + 1, np.int64)
+        self.paths = np.empty((B * pc, n))
+        self.srcs = np.empty(B * pc, np.int32)
+        self.owner = None
 
 
-def _out_buffers(B, pc, n):
-    """Reusable host result buffers of a batch (the results leave them by
-    copy): the result structs, path offsets (B+1), and the packed path rows /
-    sources sized for the worst case B * path_capacity (virtual memory: only
-    the rows a batch writes are ever touched)."""
-    key = (B, pc, n, threading.get_ident())
-    buf = _OUT.get(key)
-    if buf is None:
-        if len(_OUT) > 64:
-            _OUT.clear()
-        buf = _OUT[key] = ((_lib.Result * B)(), np.zeros(B + 1, np.int64), np.empty((B * pc, n)),
-                           np.empty(B * pc, np.int32))
-    return buf
+def _arena(B, pc, n) -> _Arena:
+    pools = getattr(_TLS, "arenas", None)
+    if pools is None:
+        pools = _TLS.arenas = {}
+    pool = pools.setdefault((B, pc, n), [])
+    for a in pool:
+        if a.owner is None or a.owner() is None:
+            a.owner = None
+            return a
+    a = _Arena(B, pc, n)
+    if len(pool) < 4:
+        pool.append(a)
+    return a
 
 
 def plan(problem: PlanProblem, options: DeviceOptions = DeviceOptions(),
