@@ -225,6 +225,18 @@ CPRRTC_API int cprrtc_plan(void *ctx, const cprrtc_params *params, int B, const 
 CPRRTC_API int cprrtc_plan_flat(void *ctx, const cprrtc_params *params, int B, const double *starts,
                                 const double *goals, const int64_t *seeds, cprrtc_result *results,
                                 int64_t *offsets, double *paths, int32_t *sources, int64_t flat_capacity);
+/* cprrtc_plan_flat in two halves: submit launches the batch and returns at
+ * once (the inputs are staged before it returns); wait collects it into the
+ * packed layout of cprrtc_plan_flat.  One batch in flight per context;
+ * alternating two contexts on a device overlaps a batch's slowest queries
+ * with the next batch (BASELINE configs[4] as a stream of batches). */
+CPRRTC_API int cprrtc_plan_submit(void *ctx, const cprrtc_params *params, int B, const double *starts,
+                                  const double *goals, const int64_t *seeds);
+CPRRTC_API int cprrtc_plan_wait(void *ctx, int B, cprrtc_result *results, int64_t *offsets, double *paths,
+                                int32_t *sources, int64_t flat_capacity);
+/* device time (CUDA events) from the start of ctx_from's last submitted batch
+ * to the end of ctx_to's (same device): a pipelined stream of batches */
+CPRRTC_API int cprrtc_elapsed_ms(void *ctx_from, void *ctx_to, double *ms);
 /* cprrtc_plan's batch sharded over n_ctx contexts (typically one per GPU):
  * context k plans the contiguous slice [k*B/n_ctx, (k+1)*B/n_ctx); every shard
  * is launched before any is awaited, and the results land in the caller's

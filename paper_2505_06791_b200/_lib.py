@@ -31,6 +31,7 @@ EXPORTS = (
     "cprrtc_nearest", "cprrtc_halton", "cprrtc_plan", "cprrtc_derive_edges",
     "cprrtc_clearance", "cprrtc_damped_step", "cprrtc_flush_l2", "cprrtc_nearest_trees", "cprrtc_step",
     "cprrtc_validate_broadphase", "cprrtc_plan_race", "cprrtc_plan_multi", "cprrtc_plan_flat",
+    "cprrtc_plan_submit", "cprrtc_plan_wait", "cprrtc_elapsed_ms",
 )
 MAX_RACE = 8
 

@@ -345,6 +345,7 @@ struct Ctx {
     bool plan_ev = true;           // ev[1..2] bracket the plan kernel in the current graph
     double last_query_ms = 0.0;    // longest query device time of the last plan call
     bool timing_pending = false;   // last_*_ms still to be read from ev[0..3] (last plan call)
+    int inflight = 0;              // B of a batch submitted and not yet waited for (cprrtc_plan_submit)
     int64_t launches = 0;
 };
 
@@ -1295,6 +1296,7 @@ struct RaceLink {
 // on the context's stream; plan_collect waits and reads the results.
 static int plan_launch(Ctx* c, const cprrtc_params* prm, int B, const double* starts, const double* goals,
                        const int64_t* seeds, const RaceLink* race) {
+    if (c->inflight) return fail(CPRRTC_EARG, "the context has a submitted batch not yet waited for");
     if (int rc = set_device(c)) return rc;
     Module* m;
     if (int rc = cur_module(c, prm->width, 0, &m)) return rc;
@@ -1509,16 +1511,29 @@ static int plan_collect(Ctx* c, int B, cprrtc_result* results, double* paths, in
     return 0;
 }
 
-// cprrtc_plan's results with the paths packed back to back (batches): one
-// pass over the mapped result block, no per-query path_capacity stride.
-int cprrtc_plan_flat(void* p, const cprrtc_params* prm, int B, const double* starts, const double* goals,
-                     const int64_t* seeds, cprrtc_result* results, int64_t* offsets, double* paths,
-                     int32_t* sources, int64_t flat_capacity) {
+// Batches without waiting: cprrtc_plan_submit launches the per-call sequence
+// and returns; cprrtc_plan_wait collects it with the paths packed back to back
+// (one pass over the mapped result block, no per-query path_capacity stride).
+// A context holds one batch in flight; alternating contexts on one device
+// overlap a batch's tail (its slowest queries) with the next batch's start.
+int cprrtc_plan_submit(void* p, const cprrtc_params* prm, int B, const double* starts, const double* goals,
+                       const int64_t* seeds) {
     Ctx* c = C(p);
-    if (!c || !prm || B < 1 || !starts || !goals || !results || !offsets || (flat_capacity > 0 && (!paths || !sources)))
-        return fail(CPRRTC_EARG, "bad argument");
+    if (!c || !prm || B < 1 || !starts || !goals) return fail(CPRRTC_EARG, "bad argument");
+    if (c->inflight) return fail(CPRRTC_EARG, "the context already has a batch in flight");
     if (int rc = check_params(prm)) return rc;
     if (int rc = plan_launch(c, prm, B, starts, goals, seeds, nullptr)) return rc;
+    c->inflight = B;
+    return 0;
+}
+
+int cprrtc_plan_wait(void* p, int B, cprrtc_result* results, int64_t* offsets, double* paths, int32_t* sources,
+                     int64_t flat_capacity) {
+    Ctx* c = C(p);
+    if (!c || B < 1 || !results || !offsets || (flat_capacity > 0 && (!paths || !sources)))
+        return fail(CPRRTC_EARG, "bad argument");
+    if (c->inflight != B) return fail(CPRRTC_EARG, "no batch of that size in flight on this context");
+    c->inflight = 0;
     if (int rc = plan_collect(c, B, results, nullptr, nullptr)) return rc;
     const int n = c->n, path_cap = c->path_cap;
     const float* hp = c->h_paths.host<float>();
@@ -1540,6 +1555,25 @@ int cprrtc_plan_flat(void* p, const cprrtc_params* prm, int B, const double* sta
         int32_t* sd = sources + offsets[i];   // L - 1 edge sources, one slot of slack per query
         for (int k = 0; k < L - 1; k++) sd[k] = ss[k];
     }
+    return 0;
+}
+
+int cprrtc_plan_flat(void* p, const cprrtc_params* prm, int B, const double* starts, const double* goals,
+                     const int64_t* seeds, cprrtc_result* results, int64_t* offsets, double* paths,
+                     int32_t* sources, int64_t flat_capacity) {
+    if (!results || !offsets || (flat_capacity > 0 && (!paths || !sources))) return fail(CPRRTC_EARG, "bad argument");
+    if (int rc = cprrtc_plan_submit(p, prm, B, starts, goals, seeds)) return rc;
+    return cprrtc_plan_wait(p, B, results, offsets, paths, sources, flat_capacity);
+}
+
+int cprrtc_elapsed_ms(void* from, void* to, double* ms) {
+    Ctx* a = C(from);
+    Ctx* b = C(to);
+    if (!a || !b || !ms || a->device != b->device) return fail(CPRRTC_EARG, "bad argument");
+    float t = 0.f;
+    cudaError_t e = cudaEventElapsedTime(&t, a->ev[0], b->ev[3]);
+    if (e != cudaSuccess) return fail(CPRRTC_ECUDA, std::string("cudaEventElapsedTime: ") + cudaGetErrorString(e));
+    *ms = t;
     return 0;
 }
 

@@ -50,7 +50,7 @@ __all__ = [
     "Tree", "PlanParams", "PlanProblem", "PlanResult", "PlanStats", "PlanContext",
     "ExtendOutcome", "ConnectOutcome", "DeviceOptions", "nearest", "steer", "plan",
     "plan_batch", "extract_path", "derive_edge", "derive_path", "revalidate_path", "dense_path", "extend",
-    "connect", "prepare", "plan_race", "plan_many", "BatchResult",
+    "connect", "prepare", "plan_race", "plan_many", "BatchResult", "PlanStream",
 ]
 
 
@@ -502,6 +502,87 @@ def _batch_result(arena, res, offsets, rows, sources, starts, goals, wall, B, pc
     out._arena = arena
     arena.owner = weakref.ref(out)
     return out
+
+
+class PlanStream:
+    """A stream of batches on one device (BASELINE configs[4] served
+    continuously): ``submit`` launches a batch and returns at once, ``result``
+    collects it as a BatchResult.  ``depth`` contexts take turns, so up to
+    ``depth`` batches are in flight and a batch's slowest queries overlap the
+    next batch's start (a persistent launch ends with its last query; its
+    finished teams free their SMs for the next launch).  Results come back in
+    submission order; each is exactly the batch plan_many would return."""
+
+    _instances = 0
+
+    def __init__(self, model, scene, spec, params: PlanParams = PlanParams(),
+                 options: DeviceOptions = DeviceOptions(), depth: int = 2):
+        if not 1 <= depth <= 8:
+            raise ValueError("depth must be in 1..8")
+        self._like = _Like(model, scene, spec, params)
+        self._prm = _make_params(params, options)
+        self._pc = int(self._prm.path_capacity)
+        PlanStream._instances += 1      # private contexts for every stream
+        base = 1000 + 8 * PlanStream._instances
+        self._ctxs = [kernels.context(model, options.device, slot=base + k) for k in range(depth)]
+        for c in self._ctxs:
+            with c.lock:
+                c.set_scene(_scene_packed(scene))
+                c.set_spec(None if spec is None else spec.packed)
+                c.prepare(params.width)
+        self._n = model.n
+        self._next = 0
+        self._inflight: dict = {}   # ticket -> (ctx, B, starts, goals, arena, t0): submitted, not collected
+        self._ready: dict = {}      # ticket -> BatchResult: collected, not yet handed out
+
+    def submit(self, starts, goals, seed_offsets) -> int:
+        """Launch one batch; returns its ticket.  Blocks only when the context
+        whose turn it is still holds the batch submitted ``depth`` tickets
+        earlier (that one is collected first and kept for ``result``)."""
+        starts = np.ascontiguousarray(starts, dtype=np.float64)
+        goals = np.ascontiguousarray(goals, dtype=np.float64)
+        seeds = np.ascontiguousarray(seed_offsets, dtype=np.int64)
+        B = starts.shape[0]
+        if B == 0 or starts.shape != (B, self._n) or goals.shape != (B, self._n) or seeds.shape != (B,):
+            raise ValueError(f"starts / goals must be (B, {self._n}) and seed_offsets (B,), B >= 1")
+        if (seeds < 0).any():
+            raise ValueError("seed_offset must be >= 0")
+        t = self._next
+        prev = t - len(self._ctxs)
+        if prev in self._inflight:
+            self._ready[prev] = self._collect(prev)
+        ctx = self._ctxs[t % len(self._ctxs)]
+        arena = _arena(B, self._pc, self._n)
+        arena.owner = lambda: ctx   # reserved until its BatchResult takes it over
+        t0 = time.perf_counter()
+        with ctx.lock:
+            rc = ctx.L.cprrtc_plan_submit(ctx.h, C.byref(self._prm), B, _lib.ptr(starts), _lib.ptr(goals),
+                                          _lib.ptr(seeds, _lib._lp))
+        if rc:
+            arena.owner = None
+            _lib.check(rc, "plan_submit")
+        self._inflight[t] = (ctx, B, starts, goals, arena, t0)
+        self._next += 1
+        return t
+
+    def _collect(self, ticket):
+        ctx, B, starts, goals, arena, t0 = self._inflight.pop(ticket)
+        with ctx.lock:
+            _lib.check(ctx.L.cprrtc_plan_wait(ctx.h, B, arena.res, _lib.ptr(arena.offsets, _lib._lp),
+                                              _lib.ptr(arena.paths), _lib.ptr(arena.srcs, _lib._ip),
+                                              C.c_int64(B * self._pc)), "plan_wait")
+        wall = (time.perf_counter() - t0) * 1e3
+        tot = int(arena.offsets[B])
+        return _batch_result(arena, arena.res, arena.offsets, arena.paths[:tot], arena.srcs[:tot], starts, goals,
+                             wall, B, self._pc)
+
+    def result(self, ticket: int) -> "BatchResult":
+        """The BatchResult of ``ticket`` (waits for it if still in flight)."""
+        if ticket in self._ready:
+            return self._ready.pop(ticket)
+        if ticket in self._inflight:
+            return self._collect(ticket)
+        raise KeyError(f"unknown or already collected ticket {ticket}")
 
 
 class _Like:

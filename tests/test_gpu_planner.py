@@ -310,3 +310,43 @@ print('ok')
     out = subprocess.run([sys.executable, "-c", code], cwd=root, env=env, capture_output=True, text=True,
                          timeout=600)
     assert out.returncode == 0 and "ok" in out.stdout, out.stderr[-2000:]
+
+
+def test_plan_stream_batches(oracle):
+    """PlanStream: batches submitted back to back (two in flight), results in
+    ticket order, sound paths, the same success as a plain plan_many; a
+    context never holds two batches (the C layer refuses)."""
+    import ctypes as C
+
+    import bench
+    from paper_2505_06791_b200 import _lib
+    from paper_2505_06791_b200.planner import PlanParams, PlanProblem, PlanStream, plan_many
+    m, sc, sp = fx.robot("arm7"), fx.scene("table"), fx.spec("table_plane")
+    prm = PlanParams(width=16, max_iterations=300)
+    stream = PlanStream(m, sc, sp, prm, depth=2)
+    tickets = [stream.submit(*bench.batch_arrays(k)) for k in range(5)]   # the 3rd submit collects the 1st
+    res = [stream.result(t) for t in tickets]
+    with pytest.raises(KeyError):
+        stream.result(tickets[0])
+    ref = plan_many(m, sc, sp, *bench.batch_arrays(0), prm)
+    assert abs(int(res[0].solved.sum()) - int(ref.solved.sum())) <= 5
+    for k, r in enumerate(res):
+        s, g, seeds = bench.batch_arrays(k)
+        assert len(r) == 1024 and r.solved.mean() > 0.97
+        for i in np.nonzero(r.solved)[0][:3]:
+            prob = PlanProblem(m, sc, sp, s[i], g[i],
+                               PlanParams(width=16, max_iterations=300, seed_offset=int(seeds[i])))
+            _check_path(oracle, prob, r[int(i)])
+    ctx = stream._ctxs[0]
+    s, g, seeds = bench.batch_arrays(9)
+    assert ctx.L.cprrtc_plan_submit(ctx.h, C.byref(stream._prm), 1024, _lib.ptr(s), _lib.ptr(g),
+                                    _lib.ptr(seeds, _lib._lp)) == 0
+    rc = ctx.L.cprrtc_plan_submit(ctx.h, C.byref(stream._prm), 1024, _lib.ptr(s), _lib.ptr(g),
+                                  _lib.ptr(seeds, _lib._lp))
+    assert rc == -1                      # one batch in flight per context
+    arena_res = (_lib.Result * 1024)()
+    off = np.zeros(1025, np.int64)
+    paths = np.empty((1024 * 1024, 7))
+    srcs = np.empty(1024 * 1024, np.int32)
+    assert ctx.L.cprrtc_plan_wait(ctx.h, 1024, arena_res, _lib.ptr(off, _lib._lp), _lib.ptr(paths),
+                                  _lib.ptr(srcs, _lib._ip), C.c_int64(1024 * 1024)) == 0
