@@ -27,6 +27,11 @@ sp2 = fx.spec("table_plane")
 probs = [PlanProblem(m, sc, sp2, prs["table_plane_start"][i], prs["table_plane_goal"][i],
                      PlanParams(width=16, max_iterations=300, seed_offset=i)) for i in range(16)]
 print("batch", sum(x.solved for x in plan_batch(probs)))
+from paper_2505_06791_b200.planner import PlanStream
+st = PlanStream(m, sc, sp2, PlanParams(width=16, max_iterations=300), depth=2)
+S = np.stack([p.start for p in probs]); G = np.stack([p.goal for p in probs])
+tk = [st.submit(S, G, np.arange(16) * 10_000 + k) for k in range(3)]
+print("stream", [int(st.result(t).solved.sum()) for t in tk])
 shelf = fx.scene("shelf_x11")
 qs = kernels.halton_batch(m, 128, 1, 3)
 t = np.linspace(0, 1, 16)[None, :, None]
