@@ -1359,7 +1359,11 @@ static int plan_launch(Ctx* c, const cprrtc_params* prm, int B, const double* st
     // arm8 0.28 -> 0.23 ms, arm7 equal)
     // (r1 re-sweep after the fast start, tools/team_sweep.sh: 160-222 pairs
     // ~2 % under 256 on upright Panda, but the shelf and configs[3] medians
-    // 4-5 % over; 256 kept)
+    // 4-5 % over; 256 kept.  r2 re-sweep on the r2 code, every config,
+    // tools/team_sweep_all.py: 128 / 148 / 160 / 192 / 256 pairs -> upright
+    // 0.144 / 0.142 / 0.145 / 0.144 / 0.148-0.151 ms, 999-box shelf 0.199 /
+    // 0.209 / 0.187 / 0.180 / 0.190, configs[3] 0.200 / 0.207 / 0.205 / 0.202 /
+    // 0.205-0.208, configs[0] equal: 192 pairs)
     static const bool pair_off = getenv("CPRRTC_PAIR") && atoi(getenv("CPRRTC_PAIR")) == 0;
     const bool pair = solo && !pair_off;
     const int tpw = solo ? 1 : 32 / m->G;         // teams per warp
@@ -1370,7 +1374,7 @@ static int plan_launch(Ctx* c, const cprrtc_params* prm, int B, const double* st
     // median -- or (batches) every resident team; never more than a quarter of the
     // sample budget so that at least ~4 waves of extensions build on each other
     // (samples are the reference's iterations)
-    long long want_teams = prm->teams > 0 ? prm->teams : (B == 1 ? (pair ? 256 : 512) : (long long)resident);
+    long long want_teams = prm->teams > 0 ? prm->teams : (B == 1 ? (pair ? 192 : 512) : (long long)resident);
     long long budget_teams = (long long)B * prm->max_iterations / 4;
     if (budget_teams < tpw) budget_teams = tpw;
     if (want_teams > budget_teams) want_teams = budget_teams;
