@@ -1369,12 +1369,16 @@ static int plan_launch(Ctx* c, const cprrtc_params* prm, int B, const double* st
     const int tpw = solo ? 1 : 32 / m->G;         // teams per warp
     const int max_tpc = solo ? kThreads / 32 : kThreads / m->G;   // teams per full CTA
     const int resident = m->plan_occ * c->sms * max_tpc;
-    // concurrency: the requested team count, else (single query) 512 teams --
-    // r1 sweep on upright Panda: 256/512/1024/2368 teams -> 0.91/0.95/1.04/1.25 ms
-    // median -- or (batches) every resident team; never more than a quarter of the
-    // sample budget so that at least ~4 waves of extensions build on each other
-    // (samples are the reference's iterations)
-    long long want_teams = prm->teams > 0 ? prm->teams : (B == 1 ? (pair ? 192 : 512) : (long long)resident);
+    // concurrency: the requested team count, else (single query) 192 pair
+    // teams / 512 one-warp teams, or (batches) B + B/8 teams but at least half
+    // the resident ones -- r2 sweep, 1024-query batches (tools/batch_teams.py):
+    // 592 / 740 / 1036 / 1184 / 1480 / 2368 (every resident) teams -> 0.98 /
+    // 0.99 / 1.08 / 1.13 / 1.09 / 0.94 M queries/s: past ~one team per query the
+    // extra teams mostly duplicate work the first solution throws away; never
+    // more than a quarter of the sample budget so that at least ~4 waves of
+    // extensions build on each other (samples are the reference's iterations)
+    long long want_teams = prm->teams > 0 ? prm->teams
+                           : (B == 1 ? (pair ? 192 : 512) : std::max((long long)B + B / 8, (long long)resident / 2));
     long long budget_teams = (long long)B * prm->max_iterations / 4;
     if (budget_teams < tpw) budget_teams = tpw;
     if (want_teams > budget_teams) want_teams = budget_teams;

@@ -126,7 +126,8 @@ class DeviceOptions:
     """B200 knobs (no reference counterpart)."""
 
     device: int = 0
-    teams: int = 0               # concurrent extension teams; 0 = one CTA per SM
+    teams: int = 0               # concurrent extension teams; 0 = automatic (single query: 192 two-warp
+                                 # teams; batches: B + B/8, at least half the resident teams)
     cc_margin: float = 1e-5      # planner robot-sphere inflation (m)
     tree_capacity: int = 0       # nodes per tree; 0 = derived from the params
     path_capacity: int = 1024
@@ -521,6 +522,7 @@ class PlanStream:
             raise ValueError("depth must be in 1..8")
         self._like = _Like(model, scene, spec, params)
         self._prm = _make_params(params, options)
+        self._auto_teams = options.teams == 0
         self._pc = int(self._prm.path_capacity)
         PlanStream._instances += 1      # private contexts for every stream
         base = 1000 + 8 * PlanStream._instances
@@ -552,6 +554,12 @@ class PlanStream:
         if prev in self._inflight:
             self._ready[prev] = self._collect(prev)
         ctx = self._ctxs[t % len(self._ctxs)]
+        if self._auto_teams:
+            # two launches share the GPU: ~0.7 teams per query each (r2 sweep,
+            # tools/batch_teams.py, 1024-query batches: 444 / 592 / 740 / 1036 /
+            # 1184 / 2368 teams -> 1.10 / 1.20 / 1.29 / 1.19 / 1.02 / 0.99 M
+            # queries/s end to end)
+            self._prm.teams = max(64, (7 * B // 10) & ~1)
         arena = _arena(B, self._pc, self._n)
         arena.owner = lambda: ctx   # reserved until its BatchResult takes it over
         t0 = time.perf_counter()
