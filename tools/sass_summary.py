@@ -21,7 +21,7 @@ if len(sys.argv) > 1:
     MODS = [(a[i], int(a[i + 1]), int(a[i + 2]), int(a[i + 3]), int(a[i + 4])) for i in range(0, len(a), 5)]
 KEEP = {"cp_plan_kernel", "cp_validate_kernel", "cp_validate_cull_kernel", "cp_nearest_kernel", "cp_project_kernel",
         "cp_dense_kernel", "cp_check_kernel"}
-CLASSES = ["FFMA", "FFMA2", "FADD", "FADD2", "FMUL", "FMUL2", "FMNMX", "FSETP", "MUFU", "LDL", "STL", "LDS",
+CLASSES = ["FFMA", "FFMA2", "FADD", "FADD2", "FMUL", "FMUL2", "FMNMX", "FMNMX3", "FSETP", "MUFU", "LDL", "STL", "LDS",
            "LDG", "STG", "SHFL", "BAR", "CALL"]
 
 for name, G, kind, orient, parity in MODS:
