@@ -212,7 +212,9 @@ CPRRTC_API int cprrtc_halton(void *ctx, int count, int64_t first_index, int64_t 
                              const double *lo, const double *hi, double *out);
 /* plan (planner.py:430-505) for B independent queries sharing robot, scene,
  * constraint and params.  paths (B, path_capacity, n), sources
- * (B, path_capacity): 0 start, 1 junction, 2 goal. */
+ * (B, path_capacity): 0 start, 1 junction, 2 goal.  A solved path's first
+ * and last rows are the exact FP64 start and goal (the tree roots,
+ * planner.py:488-505); the rows between are the FP32 tree nodes. */
 CPRRTC_API int cprrtc_plan(void *ctx, const cprrtc_params *params, int B, const double *starts,
                 const double *goals, const int64_t *seeds, cprrtc_result *results,
                 double *paths, int32_t *sources);

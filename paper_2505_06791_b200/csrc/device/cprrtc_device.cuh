@@ -56,6 +56,7 @@ __device__ __forceinline__ float4 cp_ldcg4(const float* p) {
     return v;
 }
 __device__ __forceinline__ int cp_ldvol(const int* p) { return *(const volatile int*)p; }
+__device__ __forceinline__ unsigned long long cp_ldvol64(const unsigned long long* p) { return *(const volatile unsigned long long*)p; }
 template <class T> __device__ __forceinline__ bool cp_finite(T x) { return isfinite(x); }
 
 // ---------------------------------------------------------------------------
@@ -1621,12 +1622,36 @@ __device__ __forceinline__ int* cp_par(const PlanArgs& A, int q, int k) {
     return A.parents + (size_t)(2 * q + k) * A.cap;
 }
 
-// (host mirror: runtime.cpp ws_bytes = 48 + (G + 7) NP floats, rounded up to 16 B)
+// (host mirror: runtime.cpp ws_bytes = 64 + (G + 7) NP floats, rounded up to 16 B)
 struct alignas(16) TeamWS {
-    int poll[12];          // stop-word poll: two 16 B landing slots + the next slot's parity (cp_alg1_loop)
+    int poll[16];          // stop-word polls: two 16 B landing slots + the next slot's parity (cp_alg1_loop),
+                           // and at [12, 16) the connect loop's slot (cp_stop_poll_issue)
     float seg[CP_G][CP_NP];
     float qr[CP_NP], qn[CP_NP], qs[CP_NP], qe[CP_NP], qc[CP_NP], qt[CP_NP], qm[CP_NP];
 };
+
+// Stop polls around waits that cover an L2 round trip: lane 0 copies the stop
+// word's 16-byte sector into the team's slot asynchronously (cp.async.cg: L2,
+// no register scoreboard) and reads it after the wait.  Warp P issues one
+// when a connect motion starts and reads it after the motion's wait for C's
+// verdict; warp C issues one before each collision check and reads it after
+// the check and the append, reporting a finished query to P with its verdict.
+// Without them, short projections (one or two Alg. 1 iterations: their own
+// poll is read from the second iteration on) let a team run several more
+// motions after the query is solved, and the host waits for the last team.
+__device__ __forceinline__ void cp_stop_poll_issue(const Team& tm, TeamWS& ws, const int* stop) {
+    if (tm.lane == 0)
+        asm volatile("cp.async.cg.shared.global [%0], [%1], 16; cp.async.commit_group;"
+                     ::"r"((unsigned)__cvta_generic_to_shared(&ws.poll[12])), "l"((unsigned long long)stop & ~15ull) : "memory");
+}
+__device__ __forceinline__ bool cp_stop_poll_read(const Team& tm, TeamWS& ws, const int* stop) {
+    int v = 0;
+    if (tm.lane == 0) {
+        asm volatile("cp.async.wait_all;" ::: "memory");
+        v = ws.poll[12 + (int)(((unsigned long long)stop & 15ull) >> 2)];
+    }
+    return tm.bcast(v, 0) != 0;
+}
 
 struct Stats {
     unsigned long long v[ST_NSTAT];
@@ -1677,7 +1702,7 @@ __device__ __forceinline__ bool cp_check_motion(const Team& tm, TeamWS& ws, cons
 // derive_edge (planner.py:223-245): the motion a->b re-derivable from its endpoints
 __device__ __noinline__ bool cp_derive_edge(const Team& tm, TeamWS& ws, const PlanArgs& A, const SceneSm& sc,
                                const float* a, const float* b, Stats& st, const int* stop = nullptr,
-                               unsigned long long* prof = nullptr) {
+                               unsigned long long* prof = nullptr, int* cc_poll = nullptr) {
     const long long t0 = prof ? clock64() : 0;
     cp_interp(tm, ws.seg, A.W, a, b);
     int it, pr;
@@ -1689,6 +1714,10 @@ __device__ __noinline__ bool cp_derive_edge(const Team& tm, TeamWS& ws, const Pl
     if (!okp) {
         st.v[ST_PFAIL]++;
         return false;
+    }
+    if (cc_poll) {   // the certifier's stop poll, read after the check and the append
+        cp_stop_poll_issue(tm, ws, stop);
+        *cc_poll = 1;
     }
     const bool ok = cp_check_motion(tm, ws, A, sc, st);
     if (prof) prof[1] += (unsigned long long)(clock64() - t1);
@@ -1798,7 +1827,8 @@ __device__ __noinline__ int cp_extend_once(const Team& tm, TeamWS& ws, const Pla
     return node < 0 ? -4 : node;
 }
 
-__device__ __noinline__ void cp_extract_path(const Team tm, const PlanArgs& A, int qi);   // below
+__device__ __noinline__ void cp_extract_path(const Team tm, const PlanArgs& A, int qi, int meet0, int meet1,
+                                             float (*stage)[CP_NP]);   // below
 
 // ===========================================================================
 // Pair mode (single queries): a team is two warps.  Warp P draws samples and
@@ -1816,6 +1846,7 @@ __device__ __noinline__ void cp_extract_path(const Team tm, const PlanArgs& A, i
 struct PairBox {
     unsigned long long full, done;   // mbarriers
     int result;                      // new node index, or -2 projection, -3 collision, -4 full
+    int over;                        // the query was over by the end of the job (stop word set)
     int qi, tree, parent, derive, exit;
     int p_ndone, p_pend;             // P's bookkeeping: done phases consumed, a result outstanding
     float from[CP_NP], to[CP_NP];
@@ -1871,8 +1902,10 @@ __device__ __forceinline__ void cp_pair_post(const Team& tm, PairBox& bx, TeamWS
     cp_mb_arrive(&bx.full);   // every lane: release of its own writes
 }
 
-__device__ __forceinline__ int cp_pair_result(const Team& tm, PairBox& bx) {
+// C's verdict on the outstanding job; over |= the query was over by its end
+__device__ __forceinline__ int cp_pair_result(const Team& tm, PairBox& bx, bool& over) {
     cp_pair_wait_idle(tm, bx);
+    over |= tm.bcast(bx.over, 0) != 0;
     return tm.bcast(bx.result, 0);
 }
 
@@ -1897,16 +1930,22 @@ __device__ void cp_pair_certifier(const Team& tm, TeamWS& ws, PairBox& bx, const
         if (bx.exit) break;
         const int qi = bx.qi, tree = bx.tree;
         QueryState& Q = A.qs[qi];
+#ifdef CP_TIMELINE
+        const u64 job_t0 = cp_clock_ns();
+#endif
         Stats st;
         int res;
         bool ok;
+        int polled = 0;
         if (bx.derive) {
             if ((int)tm.lane < CP_N) { ws.qr[tm.lane] = bx.from[tm.lane]; ws.qn[tm.lane] = bx.to[tm.lane]; }
             tm.sync();
             const unsigned long long pf0 = st.v[ST_PFAIL];
-            ok = cp_derive_edge(tm, ws, A, sc, ws.qr, ws.qn, st, &Q.stop, CP_CPROF);
+            ok = cp_derive_edge(tm, ws, A, sc, ws.qr, ws.qn, st, &Q.stop, CP_CPROF, &polled);
             res = ok ? 0 : (st.v[ST_PFAIL] != pf0 ? -2 : -3);
         } else {
+            cp_stop_poll_issue(tm, ws, &Q.stop);
+            polled = 1;
 #ifdef CP_PROFILE
             const long long t_cc = clock64();
 #endif
@@ -1932,11 +1971,20 @@ __device__ void cp_pair_certifier(const Team& tm, TeamWS& ws, PairBox& bx, const
         if (tm.lane == 0)
             for (int i = 0; i < 6; i++) bx.cprof[i] = cpf[i];
 #endif
+        const int over = polled && cp_stop_poll_read(tm, ws, &Q.stop);
         if (tm.lane == 0) {
 #pragma unroll
             for (int i = 0; i < ST_NSTAT; i++)
                 if (st.v[i]) atomicAdd(&Q.stats[i], st.v[i]);
             bx.result = res;
+            bx.over = over;
+#ifdef CP_TIMELINE
+            // the longest job running across the solve: (ns after the solve) & ~15 | kind
+            // (1 derive ok, 2 derive failed, 3 check ok, 4 check failed)
+            const u64 ts = cp_ldvol64(&Q.t_end_ns), now = cp_clock_ns();
+            if (ts != 0 && job_t0 <= ts && now > ts)
+                atomicMax(&Q.pad1_[0], (int)((((now - ts) >> 4) << 4) | (u64)((bx.derive ? 1 : 3) + (ok ? 0 : 1))));
+#endif
         }
         tm.sync();
         cp_mb_arrive(&bx.done);   // every lane: release
@@ -1974,11 +2022,21 @@ __device__ void cp_plan_query_pair(const Team& tm, TeamWS& ws, TeamWS& wsc, Pair
     pf[PF_LAUNCH_NS] = cp_clock_ns() - Q.t0_ns;
     const long long pf_entry = clock64();
 #endif
+#ifdef CP_TIMELINE
+    int why = 5;
+    u64 tl_t[8] = {};
+    int tl_id[8] = {}, tl_n = 0;
+#define CP_TL(id) do { if (tm.lane == 0) { tl_t[tl_n & 7] = cp_clock_ns(); tl_id[tl_n & 7] = (id); } tl_n++; } while (0)
+#define CP_WHY(k) (why = (k))
+#else
+#define CP_WHY(k) ((void)0)
+#define CP_TL(id) ((void)0)
+#endif
     for (int round = 0;; round++) {
-        CP_PF_T0(t_stop);
-        if (!(round == 0 && first_it > 0 && A.budget_ns >= 0) && cp_should_stop(tm, Q, A)) break;
+        CP_PF_T0(t_stop); CP_TL(1);
+        if (!(round == 0 && first_it > 0 && A.budget_ns >= 0) && cp_should_stop(tm, Q, A)) { CP_WHY(0); break; }
         CP_PF_ADD(PF_STOP, t_stop);
-        CP_PF_T0(t_samp);
+        CP_PF_T0(t_samp); CP_TL(2);
         int it = first_it;
         if (round > 0 || first_it <= 0) {
             if (tm.lane == 0) it = atomicAdd(&Q.next_sample, 1) + 1 + (first_it > 0 ? n_teams : 0);
@@ -1997,7 +2055,7 @@ __device__ void cp_plan_query_pair(const Team& tm, TeamWS& ws, TeamWS& wsc, Pair
         tm.sync();
         CP_PF_ADD(PF_SAMPLE, t_samp);
         CP_PF_INC(PF_NSAMP, 1);
-        CP_PF_T0(t_nn);
+        CP_PF_T0(t_nn); CP_TL(3);
         // extension P1 (planner.py:265-281)
         int cnt_a;
         const int inear = cp_nearest_ld(tm, cp_tree(A, qi, a), A.cap, &Q.count[a], ws.qr, ws.qn, &cnt_a);
@@ -2007,20 +2065,20 @@ __device__ void cp_plan_query_pair(const Team& tm, TeamWS& ws, TeamWS& wsc, Pair
         cp_interp(tm, ws.seg, W, ws.qn, ws.qs);
         CP_PF_ADD(PF_NN, t_nn);
         int pit, ppr;
-        CP_PF_T0(t_p1);
+        CP_PF_T0(t_p1); CP_TL(4);
         bool okp = cp_project(tm, ws.seg, W, A.pa, &pit, &ppr, nullptr, nullptr, &st.v[ST_STAGE1], &Q.stop, ws.poll);
         CP_PF_ADD(PF_PROJ, t_p1);
         CP_PF_INC(PF_NPROJ, 1);
         CP_PF_INC(PF_PITER, pit > 0 ? pit : 0);
-        if (pit < 0) break;
+        if (pit < 0) { CP_WHY(1); break; }
         st.v[ST_PROJITER] += pit;
         if (!okp) { st.v[ST_PFAIL]++; continue; }
         cp_copy(tm, ws.qe, ws.seg[W - 1]);
         if (cp_vec_equal(tm, ws.qe, ws.qn)) continue;
-        CP_PF_T0(t_post);
+        CP_PF_T0(t_post); CP_TL(5);
         cp_pair_post(tm, bx, wsc, qi, a, inear, !cp_vec_equal(tm, ws.qe, ws.qs), ws.qn, ws.qe, ws.seg, W);
         CP_PF_ADD(PF_WAIT, t_post);
-        CP_PF_T0(t_nn2);
+        CP_PF_T0(t_nn2); CP_TL(6);
         // greedy connect of tree b toward q_new while C certifies the extension
         cp_copy(tm, ws.qt, ws.qe);
         int cnt_b;
@@ -2032,67 +2090,73 @@ __device__ void cp_plan_query_pair(const Team& tm, TeamWS& ws, TeamWS& wsc, Pair
         bool pending_ext = true, stop = false, full = false;
         int prev = -1;          // node of the last accepted connect motion
         bool pending_con = false;
+        bool over = false;      // C saw the stop word set (after its last check)
         if (dist <= A.tol) {
-            node = cp_pair_result(tm, bx);
+            node = cp_pair_result(tm, bx, over);
             pending_ext = false;
             if (node == -4) full = true;
             if (node >= 0) meet = icur;
+            if (over) { CP_WHY(7); stop = true; }
         } else {
             for (int segs = 0; segs < A.max_connect; segs++) {
                 // the full stop / time-budget poll every 4th motion: a solved query
                 // already stops the projections (they poll the stop word) and the
                 // budget is checked at every sample (r1 A/B: -2.5 % median)
-                if (segs > 0 && (segs & 3) == 0 && cp_should_stop(tm, Q, A)) { stop = true; break; }
-                CP_PF_T0(t_si);
+                if (segs > 0 && (segs & 3) == 0 && cp_should_stop(tm, Q, A)) { CP_WHY(2); stop = true; break; }
+                cp_stop_poll_issue(tm, ws, &Q.stop);
+                CP_PF_T0(t_si); CP_TL(7);
                 cp_steer(tm, ws.qc, ws.qt, A.step, ws.qs);
                 cp_interp(tm, ws.seg, W, ws.qc, ws.qs);
                 CP_PF_ADD(PF_NN, t_si);
                 int it2, pr2;
-                CP_PF_T0(t_p2);
+                CP_PF_T0(t_p2); CP_TL(8);
                 const bool ok1 = cp_project(tm, ws.seg, W, A.pa, &it2, &pr2, nullptr, nullptr, &st.v[ST_STAGE1],
                                             &Q.stop, ws.poll);
                 CP_PF_ADD(PF_PROJ, t_p2);
                 CP_PF_INC(PF_NPROJ, 1);
                 CP_PF_INC(PF_PITER, it2 > 0 ? it2 : 0);
                 if (it2 >= 0) st.v[ST_PROJITER] += it2;
-                CP_PF_T0(t_w);
+                CP_PF_T0(t_w); CP_TL(9);
                 // the previous motion must be accepted before this one builds on it
                 if (pending_ext) {
-                    node = cp_pair_result(tm, bx);
+                    node = cp_pair_result(tm, bx, over);
                     pending_ext = false;
                     if (node < 0) { full = node == -4; break; }
                 } else if (pending_con) {
-                    prev = cp_pair_result(tm, bx);
+                    prev = cp_pair_result(tm, bx, over);
                     pending_con = false;
                     if (prev < 0) { full = prev == -4; break; }
                     icur = prev;
                 }
                 CP_PF_ADD(PF_WAIT, t_w);
-                if (it2 < 0) { stop = true; break; }
+                if (it2 < 0) { CP_WHY(3); stop = true; break; }
+                if (over || cp_stop_poll_read(tm, ws, &Q.stop)) { CP_WHY(7); stop = true; break; }
                 if (!ok1) { st.v[ST_PFAIL]++; break; }
                 cp_copy(tm, ws.qe, ws.seg[W - 1]);
                 const float nd = cp_vec_dist(tm, ws.qe, ws.qt);
                 if (!(nd < dist)) break;
-                CP_PF_T0(t_w2);
+                CP_PF_T0(t_w2); CP_TL(10);
                 cp_pair_post(tm, bx, wsc, qi, b, icur, !cp_vec_equal(tm, ws.qe, ws.qs), ws.qc, ws.qe, ws.seg, W);
                 pending_con = true;
                 cp_copy(tm, ws.qc, ws.qe);
                 dist = nd;
                 CP_PF_ADD(PF_WAIT, t_w2);
                 if (dist <= A.tol) {
-                    CP_PF_T0(t_w3);
-                    const int r = cp_pair_result(tm, bx);
+                    CP_PF_T0(t_w3); CP_TL(11);
+                    const int r = cp_pair_result(tm, bx, over);
                     CP_PF_ADD(PF_WAIT, t_w3);
                     pending_con = false;
                     if (r >= 0) meet = r;
                     else full = r == -4;
+                    if (over) { CP_WHY(7); stop = true; }   // someone else won
                     break;
                 }
             }
+            CP_TL(13);
             // drain: motions still being certified are kept (the reference
             // appends every accepted motion of a trapped connect too)
-            if (pending_ext) { node = cp_pair_result(tm, bx); pending_ext = false; if (node == -4) full = true; }
-            if (pending_con) { const int r = cp_pair_result(tm, bx); if (r == -4) full = true; }
+            if (pending_ext) { node = cp_pair_result(tm, bx, over); pending_ext = false; if (node == -4) full = true; }
+            if (pending_con) { const int r = cp_pair_result(tm, bx, over); if (r == -4) full = true; }
         }
         if (node >= 0) st.v[ST_ADDED]++;
         if (full) {
@@ -2101,7 +2165,7 @@ __device__ void cp_plan_query_pair(const Team& tm, TeamWS& ws, TeamWS& wsc, Pair
         }
         if (stop) break;
         if (node < 0 || meet < 0) continue;
-        CP_PF_T0(t_j);
+        CP_PF_T0(t_j); CP_TL(12);
         // junction (planner.py:466-481): q_new (tree a) against the meet node (tree b)
         cp_load_node(tm, A, qi, b, meet, ws.qm);
         const float* js = a == 0 ? ws.qt : ws.qm;
@@ -2132,13 +2196,20 @@ __device__ void cp_plan_query_pair(const Team& tm, TeamWS& ws, TeamWS& wsc, Pair
                 Q.meet[a] = node;
                 Q.meet[b] = meet;
                 Q.t_end_ns = cp_clock_ns();
+#ifdef CP_TIMELINE
+                Q.pad1_[4] = (int)(blockIdx.x * blockDim.x + (threadIdx.x & ~31u));
+#endif
                 __threadfence();
                 atomicExch(&Q.stop, 1);
                 for (int r = 0; r < A.n_race; r++) *(volatile int*)A.race_peers[r] = 1;
                 if (A.n_race) __threadfence_system();
                 won = 1;
             }
-            if (tm.bcast(won, 0)) cp_extract_path(tm, A, qi);   // while the other teams leave
+            if (tm.bcast(won, 0)) {   // while the other teams leave
+                CP_WHY(6);
+                cp_extract_path(tm, A, qi, a == 0 ? node : meet, a == 0 ? meet : node, ws.seg);
+            }
+            else CP_WHY(4);
             break;
         }
     }
@@ -2146,7 +2217,20 @@ __device__ void cp_plan_query_pair(const Team& tm, TeamWS& ws, TeamWS& wsc, Pair
 #pragma unroll
         for (int i = 0; i < ST_NSTAT; i++)
             if (st.v[i]) atomicAdd(&Q.stats[i], st.v[i]);
+#ifdef CP_TIMELINE
+        const u64 now = cp_clock_ns();
+        atomicMax(&Q.pad1_[6 + why], (int)(now - Q.t0_ns));
+        const u64 ts = cp_ldvol64(&Q.t_end_ns);
+        if (why != 6 && ts != 0 && now > ts) {   // the phase this team was in when the query was solved
+            int ph = 15;
+            for (int j = tl_n - 1; j >= 0 && j >= tl_n - 8; j--)
+                if (tl_t[j & 7] <= ts) { ph = tl_id[j & 7]; break; }
+            atomicMax(&Q.pad1_[2], (int)((((now - ts) >> 4) << 4) | (u64)ph));
+        }
+#endif
     }
+#undef CP_WHY
+#undef CP_TL
 }
 
 // One team works on query qi until it is solved / stopped / out of samples.
@@ -2202,6 +2286,9 @@ __device__ void cp_plan_query(const Team& tm, TeamWS& ws, const PlanArgs& A, con
                 Q.meet[a] = node;
                 Q.meet[b] = meet;
                 Q.t_end_ns = cp_clock_ns();
+#ifdef CP_TIMELINE
+                Q.pad1_[4] = (int)(blockIdx.x * blockDim.x + (threadIdx.x & ~31u));
+#endif
                 __threadfence();
                 atomicExch(&Q.stop, 1);
                 // first-solution flag of a race: one store into every racer's word
@@ -2209,7 +2296,8 @@ __device__ void cp_plan_query(const Team& tm, TeamWS& ws, const PlanArgs& A, con
                 if (A.n_race) __threadfence_system();
                 won = 1;
             }
-            if (tm.bcast(won, 0)) cp_extract_path(tm, A, qi);   // while the other teams leave
+            if (tm.bcast(won, 0))   // while the other teams leave
+                cp_extract_path(tm, A, qi, a == 0 ? node : meet, a == 0 ? meet : node, ws.seg);
             break;
         }
     }
@@ -2296,29 +2384,33 @@ __device__ __forceinline__ SceneSm cp_stage_scene(const SceneSm& g, float4* sm) 
 }
 
 #if !CP_PARITY
-// Path extraction (planner.py:488-505) into the result area (mapped host
-// memory), by one team: lane 0 walks the two parent chains (dependent L2
-// loads) into a device index list; then the team gathers the node
-// coordinates and writes path and sources with contiguous lane-consecutive
-// stores (coalesced PCIe writes).  setup_code is written by cp_check_kernel.
 // The solved query's path (planner.py:488-505), by the team that solved it,
-// right away -- it overlaps the other teams' exit.  Lane 0 walks the two
-// parent chains (dependent L2 loads) into a device index list; then the team
-// gathers the node coordinates and writes path and sources with contiguous
-// lane-consecutive stores (coalesced PCIe writes).
-__device__ __noinline__ void cp_extract_path(const Team tm, const PlanArgs& A, int qi) {
-    QueryState& Q = A.qs[qi];
+// right away -- it overlaps the other teams' exit, but the host waits for it.
+// Lanes 0 and 1 walk the start and the goal parent chains concurrently (one
+// dependent L2 load per step, meet node first) and every step's two nodes are
+// handed to the team by shuffle: chain entry e lives in lane e % CP_G,
+// register slot e / CP_G, so reversing the start chain and splicing the goal
+// chain is a shuffle per slot, not a round trip through a global index list.
+// The team then gathers 16 nodes' coordinates at a time (one round of
+// independent L2 loads) into its shared-memory segment rows and writes them
+// to the mapped result lane-consecutively (coalesced PCIe writes).  Chains
+// longer than the registers hold (CP_XK CP_G entries) take the same walk's
+// global index list instead.  meet0 / meet1: the meet nodes in the start /
+// goal tree (the winner's registers; also in Q.meet).  setup_code is written
+// by cp_check_kernel.
+#define CP_XK 4
+__device__ __noinline__ void cp_extract_path(const Team tm, const PlanArgs& A, int qi, int meet0, int meet1,
+                                             float (*stage)[CP_NP]) {
     QueryOut& O = A.out[qi];
     const int lane = (int)tm.lane, cap = A.cap, path_cap = A.path_cap;
     const float* ts = cp_tree(A, qi, 0);
     const float* tg = cp_tree(A, qi, 1);
     const int* ps = cp_par(A, qi, 0);
     const int* pg = cp_par(A, qi, 1);
-    int* ch = A.chain + (size_t)qi * path_cap;   // path position -> (tree << 30) | node
-    int status = 0, len = 0, ca = 0, skip = 0;
-    // the two parent chains are walked concurrently: lane 0 the start tree
-    // into ch[0..), lane 1 the goal tree into ch[path_cap - 1] downwards
-    const int m0 = cp_ldvol(&Q.meet[0]), m1 = cp_ldvol(&Q.meet[1]);
+    int* ch = A.chain + (size_t)qi * path_cap;   // long chains: path position -> (tree << 30) | node
+    // the two meet nodes' coordinates (equal: the junction node appears once), in flight during the walk
+    const float cm0 = lane < CP_N ? __ldcg(ts + (size_t)lane * cap + meet0) : 0.f;
+    const float cm1 = lane < CP_N ? __ldcg(tg + (size_t)lane * cap + meet1) : 0.f;
     // a chain node is visible, so its parent store is issued: a -1 (the reset
     // value) means it has not landed yet -- read again until it has
     auto parent_of = [](const int* pp, int i) {
@@ -2326,48 +2418,85 @@ __device__ __noinline__ void cp_extract_path(const Team tm, const PlanArgs& A, i
         while (p < 0) p = cp_ldvol(pp + i);
         return p;
     };
-    int cnt = 0;
-    if (lane == 0) {
-        for (int i = m0;;) {   // start chain, meet first
-            if (cnt < path_cap) ch[cnt] = i;
-            cnt++;
-            const int p = parent_of(ps, i);
-            if (p == i) break;
-            i = p;
+    int rs[CP_XK], rg[CP_XK];   // start / goal chain entries e = CP_G slot + lane
+#pragma unroll
+    for (int j = 0; j < CP_XK; j++) { rs[j] = 0; rg[j] = 0; }
+    int cur = lane == 0 ? meet0 : meet1, cnt = 0;
+    bool walking = lane < 2;
+    for (int c = 0;; c++) {
+        const unsigned wm = tm.ballot(walking);
+        if (!(wm & 3u)) break;
+        const int e0 = tm.bcast(cur, 0), e1 = tm.bcast(cur, 1);
+        if (c % CP_G == lane) {
+#pragma unroll
+            for (int j = 0; j < CP_XK; j++)
+                if (c / CP_G == j) {
+                    if (wm & 1u) rs[j] = e0;
+                    if (wm & 2u) rg[j] = e1;
+                }
         }
-    } else if (lane == 1) {
-        for (int i = m1;;) {   // goal chain, meet first, stored from the end
-            if (cnt < path_cap) ch[path_cap - 1 - cnt] = (1 << 30) | i;
+        if (walking) {
+            if (c < path_cap) {
+                if (lane == 0) ch[c] = cur;                              // start chain, meet first
+                else ch[path_cap - 1 - c] = (1 << 30) | cur;             // goal chain, from the end
+            }
             cnt++;
-            const int p = parent_of(pg, i);
-            if (p == i) break;
-            i = p;
+            const int p = parent_of(lane == 0 ? ps : pg, cur);
+            if (p == cur) walking = false;
+            else cur = p;
         }
     }
-    ca = tm.bcast(cnt, 0);
-    const int cb = tm.bcast(cnt, 1);
-    bool same = true;
-    for (int d = 0; d < CP_N; d++) same &= __ldcg(ts + (size_t)d * cap + m0) == __ldcg(tg + (size_t)d * cap + m1);
-    skip = same ? 1 : 0;
-    len = ca + cb - skip;
-    __threadfence_block();
-    tm.sync();
+    const int ca = tm.bcast(cnt, 0), cb = tm.bcast(cnt, 1);
+    const int skip = tm.ballot(lane < CP_N && cm0 != cm1) == 0u ? 1 : 0;
+    const int len = ca + cb - skip;
+    int status = 0;
     if (len > path_cap || ca + cb > path_cap) {
         status = 4;
-    } else if (lane == 0) {
-        // start chain root..meet, then the goal chain meet..root (the meet node once if equal)
-        for (int a = 0, b = ca - 1; a < b; a++, b--) { int t = ch[a]; ch[a] = ch[b]; ch[b] = t; }
-        for (int k = skip; k < cb; k++) ch[ca + k - skip] = ch[path_cap - 1 - k];
-    }
-    __threadfence_block();
-    tm.sync();
-    if (status == 0) {
+    } else if (ca <= CP_XK * CP_G && cb <= CP_XK * CP_G) {
+        float* path = A.paths + (size_t)qi * path_cap * CP_N;
+        for (int base = 0; base < len; base += CP_G) {
+            // position k: start chain entry ca - 1 - k, then goal chain entry k - ca + skip
+            const int k = base + lane;
+            const bool st = k < ca;
+            const int e = st ? ca - 1 - k : k - ca + skip;
+            int node = 0;
+#pragma unroll
+            for (int j = 0; j < CP_XK; j++) {
+                const int vs = __shfl_sync(tm.mask, rs[j], e % CP_G, CP_G);
+                const int vg = __shfl_sync(tm.mask, rg[j], e % CP_G, CP_G);
+                if (e / CP_G == j) node = st ? vs : vg;
+            }
+            if (k < len) {
+                const float* t = st ? ts : tg;
+#pragma unroll
+                for (int d = 0; d < CP_N; d++) stage[lane][d] = __ldcg(t + (size_t)d * cap + node);
+            }
+            tm.sync();
+            const int rows = min(CP_G, len - base);
+            for (int f = lane; f < rows * CP_N; f += CP_G) {
+                const int r = f / CP_N;
+                path[(size_t)base * CP_N + f] = stage[r][f - r * CP_N];
+            }
+            tm.sync();
+        }
+    } else {
+        // long chains: the global index list, root .. meet .. root
+        __threadfence_block();
+        tm.sync();
+        if (lane == 0) {
+            for (int a = 0, b = ca - 1; a < b; a++, b--) { int t = ch[a]; ch[a] = ch[b]; ch[b] = t; }
+            for (int k = skip; k < cb; k++) ch[ca + k - skip] = ch[path_cap - 1 - k];
+        }
+        __threadfence_block();
+        tm.sync();
         float* path = A.paths + (size_t)qi * path_cap * CP_N;
         for (int f = lane; f < len * CP_N; f += CP_G) {
             const int k = f / CP_N, d = f - k * CP_N;
             const int e = ch[k];
             path[f] = __ldcg(((e >> 30) ? tg : ts) + (size_t)d * cap + (e & 0x3fffffff));
         }
+    }
+    if (status == 0) {
         // edge sources: start edges, then the junction (or the first goal
         // edge when the meet nodes coincide), then goal edges
         int* src = A.sources + (size_t)qi * path_cap;
@@ -2376,7 +2505,12 @@ __device__ __noinline__ void cp_extract_path(const Team tm, const PlanArgs& A, i
     if (lane == 0) {
         O.status = status;
         O.path_len = status == 0 ? len : 0;
+#ifdef CP_TIMELINE
+        QueryState& Q = A.qs[qi];
+        Q.pad1_[1] = (int)(cp_clock_ns() - Q.t0_ns);
+#endif
     }
+    if (A.nq == 1) __threadfence_system();   // the path reaches the host before the finalizer's completion word
     tm.sync();
 }
 
@@ -2389,8 +2523,12 @@ __device__ __noinline__ void cp_extract_query(const Team tm, const PlanArgs& A, 
     const int lane = (int)tm.lane, cap = A.cap;
     const int ns = min(cp_ldvol(&Q.count[0]), cap), ng = min(cp_ldvol(&Q.count[1]), cap);
 #ifndef CP_PROFILE
+#ifdef CP_TIMELINE
+    if (lane < 6) O.stats[lane] = (u64)cp_ldvol(&Q.pad1_[lane < 5 ? 6 + lane : 13]);   // latest exit by reason
+#else
     if (lane < ST_NSTAT) O.stats[lane] = __ldcg(&Q.stats[lane]);
     if (ST_NSTAT > CP_G && lane + CP_G < ST_NSTAT) O.stats[lane + CP_G] = __ldcg(&Q.stats[lane + CP_G]);
+#endif
 #endif
     const int solved = cp_ldvol(&Q.solved);
     if (lane == 0) {
@@ -2403,7 +2541,20 @@ __device__ __noinline__ void cp_extract_query(const Team tm, const PlanArgs& A, 
         Q.hwm[0] = ns;
         Q.hwm[1] = ng;
         const u64 tend = solved ? Q.t_end_ns : cp_clock_ns();
+#ifdef CP_TIMELINE   // diagnostic: stats 8-11 = solved / chains walked / path written / last team out (ns after init)
+        O.stats[8] = solved ? Q.t_end_ns - Q.t0_ns : 0;
+        O.stats[9] = (u64)cp_ldvol(&Q.pad1_[2]);   // latest other P: (ns after solve) & ~15 | phase at the solve
+        O.stats[10] = (u64)Q.pad1_[1];
+        O.stats[11] = cp_clock_ns() - Q.t0_ns;
+        O.stats[6] = (u64)cp_ldvol(&Q.pad1_[0]);   // warp C's longest job across the solve (see the certifier)
+        O.stats[7] = (u64)cp_ldvol(&Q.pad1_[5]);   // the winner out
+#endif
         O.device_ms = (double)(tend - Q.t0_ns) * 1e-6;
+    }
+    if (A.nq == 1) {   // single query: every lane's result stores reach the host before the completion word
+        __threadfence_system();
+        tm.sync();
+        if (lane == 0) *(volatile unsigned*)&O.done_seq = (unsigned)A.seeds[A.nq];
     }
     tm.sync();
 }
@@ -2509,6 +2660,13 @@ cp_plan_kernel(const __grid_constant__ PlanArgs A) {
         // the last team to leave the query extracts its result (a late
         // joiner may extract again: identical values)
         int last = 0;
+#ifdef CP_TIMELINE
+        if (tm.lane == 0) {
+            const int tnow = (int)(cp_clock_ns() - Q.t0_ns);
+            if (cp_ldvol(&Q.pad1_[4]) == (int)(blockIdx.x * blockDim.x + (threadIdx.x & ~31u))) Q.pad1_[5] = tnow;
+            else atomicMax(&Q.pad1_[3], tnow);
+        }
+#endif
         if (tm.lane == 0) {
             __threadfence();
             last = atomicSub(&Q.active, 1) == 1;
@@ -2616,6 +2774,10 @@ extern "C" __global__ void __launch_bounds__(32) cp_init_kernel(const __grid_con
         Q.meet[0] = -1; Q.meet[1] = -1;
         Q.t0_ns = cp_clock_ns();
         Q.t_end_ns = 0;
+#ifdef CP_TIMELINE
+        Q.pad1_[0] = 0; Q.pad1_[2] = 0; Q.pad1_[3] = 0; Q.pad1_[4] = -1; Q.pad1_[5] = 0;
+        for (int k = 6; k < 14; k++) Q.pad1_[k] = 0;
+#endif
     }
     if (lane < ST_NSTAT) Q.stats[lane] = 0ull;
 }
@@ -2640,6 +2802,10 @@ extern "C" __global__ void __launch_bounds__(64) cp_check_kernel(const __grid_co
         if (c) {
             Q.setup_code = c;
             atomicExch(&Q.stop, 1);
+        }
+        if (gridDim.x == 1) {   // single query: the completion word, with the call's sequence number
+            __threadfence_system();
+            *(volatile unsigned*)&S.out[qi].chk_seq = (unsigned)S.seeds[gridDim.x];
         }
     }
 }

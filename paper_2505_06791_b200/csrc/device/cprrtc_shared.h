@@ -133,6 +133,10 @@ struct QueryOut {
     int pad;
     double device_ms;
     u64 stats[ST_NSTAT];
+    // completion words (the call's sequence number, from the input block):
+    // written last, behind a system-scope fence, by the query's finalizer and
+    // by the endpoint check; the host polls them instead of the graph's event
+    unsigned done_seq, chk_seq;
 };
 
 #endif

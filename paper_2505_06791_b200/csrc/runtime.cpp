@@ -16,6 +16,8 @@
 #include <unistd.h>
 
 #include <algorithm>
+#include <atomic>
+#include <chrono>
 #include <cmath>
 #include <cstddef>
 #include <cstdint>
@@ -346,6 +348,7 @@ struct Ctx {
     double last_query_ms = 0.0;    // longest query device time of the last plan call
     bool timing_pending = false;   // last_*_ms still to be read from ev[0..3] (last plan call)
     int inflight = 0;              // B of a batch submitted and not yet waited for (cprrtc_plan_submit)
+    unsigned plan_seq = 0;         // sequence number of the last plan launch (QueryOut completion words)
     int64_t launches = 0;
 };
 
@@ -419,7 +422,7 @@ int get_module(Ctx* c, int G, int kind, int orient, int parity, Module** out) {
     m->kind = kind;
     m->orient = orient;
     // sizeof(TeamWS): the poll slots (48 B), G segment rows and 7 vectors, 16-byte aligned
-    m->ws_bytes = ((size_t)48 + (size_t)(G + 7) * c->NP * sizeof(float) + 15) & ~(size_t)15;
+    m->ws_bytes = ((size_t)64 + (size_t)(G + 7) * c->NP * sizeof(float) + 15) & ~(size_t)15;
     for (const char* k : {"cp_plan_kernel", "cp_validate_kernel", "cp_validate_cull_kernel", "cp_project_kernel",
                           "cp_dense_kernel", "cp_step_kernel"})
         if (m->fn.count(k)) drv().funcSetAttribute(m->fn[k], CU_FUNC_ATTRIBUTE_MAX_DYNAMIC_SHARED_SIZE_BYTES, 200 * 1024);
@@ -844,6 +847,8 @@ int cprrtc_last_timing(void* p, double* total_ms, double* plan_ms) {
     if (!c) return fail(CPRRTC_EARG, "NULL context");
     if (c->timing_pending) {
         float t_all = 0, t_plan = 0;
+        if (int rc = set_device(c)) return rc;
+        cudaEventSynchronize(c->ev[3]);   // plan_collect returns before the graph's results event
         cudaEventElapsedTime(&t_all, c->ev[0], c->ev[3]);
         // without events around the planner (the PDL graph) its time is the
         // longest query's device time (init -> solved / last team out, globaltimer)
@@ -1220,9 +1225,9 @@ static int ensure_plan_buffers(Ctx* c, int nq, int cap, int path_cap) {
     int rc = c->counters.ensure(64);
     {   // inputs (starts | goals | seeds) in one block; a move invalidates the graphs
         void* before = c->d_starts.p;
-        rc = rc ? rc : c->d_starts.ensure((size_t)nq * (2 * n + 1) * 8);
+        rc = rc ? rc : c->d_starts.ensure((size_t)nq * (2 * n + 1) * 8 + 8);   // + the call's sequence number
         void* hbefore = c->h_in.h;
-        rc = rc ? rc : c->h_in.ensure((size_t)nq * (2 * n + 1) * 8);
+        rc = rc ? rc : c->h_in.ensure((size_t)nq * (2 * n + 1) * 8 + 8);
         void* obefore = c->h_out.h;
         rc = rc ? rc : c->h_out.ensure((size_t)nq * sizeof(QueryOut));
         void* pbefore = c->h_paths.h;
@@ -1294,6 +1299,46 @@ struct RaceLink {
 
 // Stage inputs and launch the per-call sequence (H2D, setup, plan, extract)
 // on the context's stream; plan_collect waits and reads the results.
+static int plan_collect(Ctx* c, int B, cprrtc_result* results, double* paths, int32_t* sources);
+
+// A solved path's roots are the exact FP64 endpoints (the tree roots hold
+// their FP32 roundings on the device)
+static void exact_roots(const Ctx* c, int B, const double* starts, const double* goals, const cprrtc_result* results,
+                        double* paths) {
+    if (!paths) return;
+    const int n = c->n;
+    for (int i = 0; i < B; i++) {
+        const int L = results[i].path_len;
+        if (L < 2) continue;
+        double* row = paths + (size_t)i * c->path_cap * n;
+        std::memcpy(row, starts + (size_t)i * n, (size_t)n * sizeof(double));
+        std::memcpy(row + (size_t)(L - 1) * n, goals + (size_t)i * n, (size_t)n * sizeof(double));
+    }
+}
+
+// Developer knob: CPRRTC_HOST_PROFILE=1 prints, at exit, the medians of the
+// host-side phases of cprrtc_plan (us): launch preparation, cudaGraphLaunch,
+// the wait for the results event, the result copy.
+namespace {
+struct HostProfile {
+    std::vector<double> v[4];
+    ~HostProfile() {
+        if (v[0].empty()) return;
+        const char* names[4] = {"prepare", "graph launch", "wait", "collect"};
+        std::fprintf(stderr, "[cprrtc host profile] %zu calls, medians (us):", v[0].size());
+        for (int k = 0; k < 4; k++) {
+            std::vector<double> x = v[k];
+            std::nth_element(x.begin(), x.begin() + x.size() / 2, x.end());
+            std::fprintf(stderr, " %s %.2f", names[k], x[x.size() / 2]);
+        }
+        std::fprintf(stderr, "\n");
+    }
+};
+HostProfile g_hprof;
+double g_hp_launch_us = 0.0;   // cudaGraphLaunch time of the last plan_launch
+const bool g_hp_on = getenv("CPRRTC_HOST_PROFILE") && atoi(getenv("CPRRTC_HOST_PROFILE")) != 0;
+}  // namespace
+
 static int plan_launch(Ctx* c, const cprrtc_params* prm, int B, const double* starts, const double* goals,
                        const int64_t* seeds, const RaceLink* race) {
     if (c->inflight) return fail(CPRRTC_EARG, "the context has a submitted batch not yet waited for");
@@ -1317,7 +1362,8 @@ static int plan_launch(Ctx* c, const cprrtc_params* prm, int B, const double* st
     std::memcpy(hin + (size_t)B * n, goals, (size_t)B * n * 8);
     long long* hseed = reinterpret_cast<long long*>(hin + (size_t)2 * B * n);
     for (int i = 0; i < B; i++) hseed[i] = seeds ? seeds[i] : 0;
-    const size_t in_bytes = (size_t)B * (2 * n + 1) * 8;
+    hseed[B] = (long long)++c->plan_seq;   // the completion words carry it back (plan_collect)
+    const size_t in_bytes = (size_t)B * (2 * n + 1) * 8 + 8;
     const double tau = prm->tau_task > 0 ? prm->tau_task : c->tau_task;
     // setup (FP64 endpoint checks, NaN refill of last run's slots, roots,
     // counters) -- planner.py:416-445
@@ -1477,7 +1523,12 @@ static int plan_launch(Ctx* c, const cprrtc_params* prm, int B, const double* st
         c->graphs.push_back(g);
         G = &c->graphs.back();
     }
-    CUDA_TRY(cudaGraphLaunch(G->exec, c->stream));
+    {
+        const auto tl = g_hp_on ? std::chrono::steady_clock::now() : std::chrono::steady_clock::time_point();
+        CUDA_TRY(cudaGraphLaunch(G->exec, c->stream));
+        if (g_hp_on)
+            g_hp_launch_us = std::chrono::duration<double, std::micro>(std::chrono::steady_clock::now() - tl).count();
+    }
     c->launches += 4;   // init, check, plan, reset
     c->last_args = A;
     c->last_mod = m;
@@ -1485,12 +1536,47 @@ static int plan_launch(Ctx* c, const cprrtc_params* prm, int B, const double* st
     return 0;
 }
 
+// Wait for a launch's results.  A single query's completion words (written
+// in mapped memory by its finalizer and its endpoint check, behind
+// system-scope fences) carry the launch's sequence number -- the host sees
+// them a PCIe write after the last team leaves, without waiting for the
+// planner grid to retire and the graph's results event to fire (r2: e2e
+// median -8 %).  The event is still queried every few thousand polls: a
+// failed launch, or one that ended without writing a word, ends the wait
+// there.  Batches wait for the event: there the system-scope fences, one per
+// query and per solved path, cost more than they save (r2: 1024-query batch
+// kernel 0.84 -> 1.21 ms with them).
+static int wait_results(Ctx* c, int B) {
+    if (B != 1) {
+        const cudaError_t e = cudaEventSynchronize(c->ev[3]);
+        if (e != cudaSuccess) return fail(CPRRTC_ECUDA, std::string("kernel failed: ") + cudaGetErrorString(e));
+        return 0;
+    }
+    const volatile QueryOut* out = c->h_out.host<QueryOut>();
+    const unsigned seq = c->plan_seq;
+    for (unsigned spin = 1;; spin++) {
+        bool all = true;
+        for (int i = 0; i < B && all; i++) all = out[i].done_seq == seq && out[i].chk_seq == seq;
+        if (all) break;
+        if ((spin & 4095) == 0) {
+            const cudaError_t e = cudaEventQuery(c->ev[3]);
+            if (e == cudaSuccess) break;
+            if (e != cudaErrorNotReady)
+                return fail(CPRRTC_ECUDA, std::string("kernel failed: ") + cudaGetErrorString(e));
+        }
+#if defined(__x86_64__)
+        __builtin_ia32_pause();
+#endif
+    }
+    std::atomic_thread_fence(std::memory_order_acquire);
+    return 0;
+}
+
 static int plan_collect(Ctx* c, int B, cprrtc_result* results, double* paths, int32_t* sources) {
     if (int rc = set_device(c)) return rc;
-    {   // results are complete at ev[3]; the tree refill behind it may still run
-        cudaError_t e = cudaEventSynchronize(c->ev[3]);
-        if (e != cudaSuccess) return fail(CPRRTC_ECUDA, std::string("kernel failed: ") + cudaGetErrorString(e));
-    }
+    // results are complete when the completion words say so; the planner's
+    // last warps, the results event and the tree refill behind it may still run
+    if (int rc = wait_results(c, B)) return rc;
     const int n = c->n;
     const int path_cap = c->path_cap;
     c->timing_pending = true;   // event times are read only when asked for (cprrtc_last_timing)
@@ -1579,6 +1665,8 @@ int cprrtc_elapsed_ms(void* from, void* to, double* ms) {
     Ctx* b = C(to);
     if (!a || !b || !ms || a->device != b->device) return fail(CPRRTC_EARG, "bad argument");
     float t = 0.f;
+    if (int rc = set_device(b)) return rc;
+    cudaEventSynchronize(b->ev[3]);
     cudaError_t e = cudaEventElapsedTime(&t, a->ev[0], b->ev[3]);
     if (e != cudaSuccess) return fail(CPRRTC_ECUDA, std::string("cudaEventElapsedTime: ") + cudaGetErrorString(e));
     *ms = t;
@@ -1590,8 +1678,26 @@ int cprrtc_plan(void* p, const cprrtc_params* prm, int B, const double* starts, 
     Ctx* c = C(p);
     if (!c || !prm || B < 1 || !starts || !goals || !results) return fail(CPRRTC_EARG, "bad argument");
     if (int rc = check_params(prm)) return rc;
+    using clk = std::chrono::steady_clock;
+    const auto t0 = g_hp_on ? clk::now() : clk::time_point();
     if (int rc = plan_launch(c, prm, B, starts, goals, seeds, nullptr)) return rc;
-    return plan_collect(c, B, results, paths, sources);
+    if (!g_hp_on) {
+        const int rc = plan_collect(c, B, results, paths, sources);
+        if (!rc) exact_roots(c, B, starts, goals, results, paths);
+        return rc;
+    }
+    const auto t1 = clk::now();
+    if (int rc = wait_results(c, B)) return rc;
+    const auto t2 = clk::now();
+    const int rc = plan_collect(c, B, results, paths, sources);
+    if (!rc) exact_roots(c, B, starts, goals, results, paths);
+    const auto t3 = clk::now();
+    auto us = [](clk::duration d) { return std::chrono::duration<double, std::micro>(d).count(); };
+    g_hprof.v[0].push_back(us(t1 - t0) - g_hp_launch_us);
+    g_hprof.v[1].push_back(g_hp_launch_us);
+    g_hprof.v[2].push_back(us(t2 - t1));
+    g_hprof.v[3].push_back(us(t3 - t2));
+    return rc;
 }
 
 int cprrtc_plan_multi(void* const* ctxs, int n_ctx, const cprrtc_params* prm, int B, const double* starts,

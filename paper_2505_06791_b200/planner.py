@@ -672,8 +672,24 @@ def _solved(path, sources, stats) -> "PlanResult":
     return r
 
 
+_SRC_CACHE: dict = {}
+
+
+def _sources(srcs_i, L) -> tuple:
+    """Edge-source names of a path (the codes' bytes key a small cache: a
+    path's sources are start edges, a junction, goal edges)."""
+    key = srcs_i[:L - 1].tobytes()
+    t = _SRC_CACHE.get(key)
+    if t is None:
+        if len(_SRC_CACHE) > 4096:
+            _SRC_CACHE.clear()
+        t = _SRC_CACHE[key] = tuple(map(_SRC.__getitem__, srcs_i[:L - 1].tolist()))
+    return t
+
+
 def _result_one(r, p, paths_i, srcs_i, wall, pc) -> "PlanResult":
-    """The single-query latency path's decoding (one ctypes result)."""
+    """The single-query latency path's decoding (one ctypes result; the C
+    call wrote the exact FP64 endpoints into the path's first and last rows)."""
     s = r.stats[:]
     stats = PlanStats(s[0], s[1], s[2], s[3], s[4], s[5], s[6], wall, r.nodes_start, r.nodes_goal,
                       r.device_ms, s[8], s[9], s[10], s[11])
@@ -681,9 +697,7 @@ def _result_one(r, p, paths_i, srcs_i, wall, pc) -> "PlanResult":
     if code == 0:
         L = r.path_len
         rows = paths_i[:L].copy()                # one array; the path's nodes are its rows
-        rows[0] = p.start                        # roots are the exact FP64 endpoints
-        rows[-1] = p.goal
-        return _solved(tuple(rows), tuple(map(_SRC.__getitem__, srcs_i[:L - 1].tolist())), stats)
+        return _solved(tuple(rows), _sources(srcs_i, L), stats)
     if code == -1:
         raise PlanSetupError(_SETUP.get(r.setup_code, "invalid start/goal"))
     if code == 4:
