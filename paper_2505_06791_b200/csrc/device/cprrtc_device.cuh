@@ -2425,7 +2425,7 @@ __device__ __noinline__ void cp_extract_path(const Team tm, const PlanArgs& A, i
     bool walking = lane < 2;
     for (int c = 0;; c++) {
         const unsigned wm = tm.ballot(walking);
-        if (!(wm & 3u)) break;
+        if (!(wm & 3u) || c > cap) break;   // (a chain is never longer than its tree)
         const int e0 = tm.bcast(cur, 0), e1 = tm.bcast(cur, 1);
         if (c % CP_G == lane) {
 #pragma unroll
