@@ -2199,7 +2199,8 @@ __device__ void cp_plan_query_pair(const Team& tm, TeamWS& ws, TeamWS& wsc, Pair
 #ifdef CP_TIMELINE
                 Q.pad1_[4] = (int)(blockIdx.x * blockDim.x + (threadIdx.x & ~31u));
 #endif
-                __threadfence();
+                // no fence: the stop word is only a signal to leave (the
+                // finalizer reads meet / t_end after the active-count handshake)
                 atomicExch(&Q.stop, 1);
                 for (int r = 0; r < A.n_race; r++) *(volatile int*)A.race_peers[r] = 1;
                 if (A.n_race) __threadfence_system();
@@ -2289,7 +2290,8 @@ __device__ void cp_plan_query(const Team& tm, TeamWS& ws, const PlanArgs& A, con
 #ifdef CP_TIMELINE
                 Q.pad1_[4] = (int)(blockIdx.x * blockDim.x + (threadIdx.x & ~31u));
 #endif
-                __threadfence();
+                // no fence: the stop word is only a signal to leave (the
+                // finalizer reads meet / t_end after the active-count handshake)
                 atomicExch(&Q.stop, 1);
                 // first-solution flag of a race: one store into every racer's word
                 for (int r = 0; r < A.n_race; r++) *(volatile int*)A.race_peers[r] = 1;
