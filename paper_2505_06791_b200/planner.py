@@ -30,6 +30,7 @@ from __future__ import annotations
 
 import ctypes as C
 import math
+import os
 import threading
 import time
 import weakref
@@ -740,7 +741,7 @@ class _Session:
     and looks nothing up twice per call."""
 
     __slots__ = ("objs", "ctx", "params", "pkey", "prm", "pc", "width", "pscene", "pspec", "s", "g", "seed",
-                 "res", "paths", "srcs", "args")
+                 "res", "paths", "srcs", "args", "fast")
 
     def __init__(self, problem, options):
         self.objs = (problem.model, problem.scene, problem.spec, options)
@@ -771,6 +772,9 @@ class _Session:
                 self.srcs = np.empty((1, pc), np.int32)
             self.args = (self.ctx.h, C.byref(self.prm), 1, _lib.ptr(self.s), _lib.ptr(self.g),
                          _lib.ptr(self.seed, _lib._lp), self.res, _lib.ptr(self.paths), _lib.ptr(self.srcs, _lib._ip))
+            # the _cprrtc_fast arguments around (start, goal, seed): the same buffers by address
+            self.fast = (self.ctx.h.value, C.addressof(self.prm), C.addressof(self.res), self.paths.ctypes.data,
+                         self.srcs.ctypes.data, self.ctx.n)
             self.pkey = key
         self.params = params
 
@@ -793,25 +797,69 @@ def _session(problem, options) -> _Session:
     return s
 
 
+_FAST_UNSET = object()
+_FAST = _FAST_UNSET
+
+
+def _fast():
+    """The CPython fast path of the single-query call (csrc/pyfast.c), or
+    None (not built, or CPRRTC_NO_FAST=1): then plan() goes through ctypes."""
+    global _FAST
+    if _FAST is _FAST_UNSET:
+        f = None
+        if os.environ.get("CPRRTC_NO_FAST", "0") in ("", "0"):
+            try:
+                from . import _cprrtc_fast as f
+                f.setup(C.cast(_lib.load().cprrtc_plan, C.c_void_p).value, _SRC)
+            except ImportError:
+                f = None
+        _FAST = f
+    return _FAST
+
+
+def _result_fast(out, pc) -> "PlanResult":
+    """PlanResult of a _cprrtc_fast.plan_one tuple (0, status, setup_code,
+    stats in PlanStats order, path rows, sources)."""
+    code = out[1]
+    stats = PlanStats(*out[3])
+    if code == 0:
+        return _solved(out[4], out[5], stats)
+    if code == -1:
+        raise PlanSetupError(_SETUP.get(out[2], "invalid start/goal"))
+    if code == 4:
+        raise RuntimeError(f"solution path longer than path_capacity={pc}")
+    return PlanResult(_STATUS.get(code, "IterLimit"), None, None, stats)
+
+
 def _plan_one(problem: PlanProblem, options: DeviceOptions, return_dense: bool) -> PlanResult:
     ss = _session(problem, options)
     seed = problem.params.seed_offset
     if seed < 0:
         raise ValueError("seed_offset must be >= 0")
-    ss.s[0] = problem.start
-    ss.g[0] = problem.goal
-    ss.seed[0] = seed
     ctx = ss.ctx
+    fast = _FAST if _FAST is not _FAST_UNSET else _fast()
     with ctx.lock:   # bind + launch under one lock (planner._bound)
         ctx.set_scene(ss.pscene)
         ctx.set_spec(ss.pspec)
         ctx.prepare(ss.width)
-        t0 = time.perf_counter()
-        rc = ctx.L.cprrtc_plan(*ss.args)
-        wall = (time.perf_counter() - t0) * 1e3
-        if rc:
-            _lib.check(rc, "plan")
-        res = _result_one(ss.res[0], problem, ss.paths[0], ss.srcs[0], wall, ss.pc)
+        out = None
+        if fast is not None:
+            h, prm, res, paths, srcs, n = ss.fast
+            out = fast.plan_one(h, prm, problem.start, problem.goal, seed, res, paths, srcs, n)
+        if out is not None:
+            if out[0]:
+                _lib.check(out[0], "plan")
+            res = _result_fast(out, ss.pc)
+        else:   # ctypes (no fast module, or inputs it does not take: not float64 C-contiguous)
+            ss.s[0] = problem.start
+            ss.g[0] = problem.goal
+            ss.seed[0] = seed
+            t0 = time.perf_counter()
+            rc = ctx.L.cprrtc_plan(*ss.args)
+            wall = (time.perf_counter() - t0) * 1e3
+            if rc:
+                _lib.check(rc, "plan")
+            res = _result_one(ss.res[0], problem, ss.paths[0], ss.srcs[0], wall, ss.pc)
         if return_dense and res.solved:
             L = len(res.path)
             dense, ok = _derive(ctx, ss.prm, ss.paths[0, :L], ss.srcs[0, :L - 1])

@@ -75,3 +75,18 @@ def test_shared_struct_layout_matches_ctypes():
     from paper_2505_06791_b200 import _lib
     assert C.sizeof(_lib.Result) == 4 * 5 + 4 + 8 + 8 * 12
     assert C.sizeof(_lib.Params) > 0
+
+
+def test_fast_path_module_loads():
+    """The CPython fast path of the single-query plan() (csrc/pyfast.c) is
+    built in-tree, binds to the ctypes library's cprrtc_plan, and declines
+    (returns None) arguments it does not take instead of calling."""
+    from paper_2505_06791_b200 import planner
+    f = planner._fast()
+    assert f is not None and f.__name__.endswith("_cprrtc_fast")
+    z = np.zeros(7)
+    assert f.plan_one(0, 0, z, z, 0, 0, 0, 0, 7) is None                   # NULL context: no call
+    assert f.plan_one(1, 1, np.zeros(14)[::2], z, 0, 1, 1, 1, 7) is None    # strided start
+    assert f.plan_one(1, 1, z.astype(np.float32), z, 0, 1, 1, 1, 7) is None
+    with pytest.raises(TypeError):
+        f.plan_one(0, 0, z)

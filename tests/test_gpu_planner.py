@@ -350,3 +350,27 @@ def test_plan_stream_batches(oracle):
     srcs = np.empty(1024 * 1024, np.int32)
     assert ctx.L.cprrtc_plan_wait(ctx.h, 1024, arena_res, _lib.ptr(off, _lib._lp), _lib.ptr(paths),
                                   _lib.ptr(srcs, _lib._ip), C.c_int64(1024 * 1024)) == 0
+
+
+def test_fast_and_ctypes_single_query_paths(oracle):
+    """plan() goes through the CPython fast path (csrc/pyfast.c) when the
+    inputs are float64 C-contiguous and through ctypes otherwise; both give
+    the same result types (a tuple of float64 rows with the exact FP64
+    endpoints, the reference's edge-source names, PlanStats) and sound paths."""
+    from paper_2505_06791_b200 import planner
+    from paper_2505_06791_b200.planner import PlanParams, PlanProblem, plan
+    assert planner._fast() is not None
+    m, sc, sp = fx.robot("arm7"), fx.scene("table"), fx.spec("upright")
+    prs = fx.pairs()
+    k = int(np.nonzero(fx.upright_feasible())[0][0])
+    s, g = prs["upright_start"][k], prs["upright_goal"][k]
+    strided = np.repeat(s, 2)[::2]                      # a non-contiguous view: the ctypes path
+    assert not strided.flags.c_contiguous
+    for start in (np.ascontiguousarray(s), strided):
+        prob = PlanProblem(m, sc, sp, start, g, PlanParams(width=16, max_iterations=10**6, seed_offset=k))
+        r = plan(prob)
+        assert r.solved, r.status
+        assert isinstance(r.path, tuple) and all(q.dtype == np.float64 and q.shape == (m.n,) for q in r.path)
+        assert set(r.edge_sources) <= {"start", "junction", "goal"}
+        assert r.stats.wall_ms > 0 and r.stats.device_ms > 0 and r.stats.nodes_start >= 1
+        _check_path(oracle, prob, r)
