@@ -2117,6 +2117,8 @@ __device__ void cp_plan_query_pair(const Team& tm, TeamWS& ws, TeamWS& wsc, Pair
                 CP_PF_INC(PF_PITER, it2 > 0 ? it2 : 0);
                 if (it2 >= 0) st.v[ST_PROJITER] += it2;
                 CP_PF_T0(t_w); CP_TL(9);
+                // abandoned (the query is over): leave without C's verdict on the previous motion
+                if (it2 < 0) { CP_WHY(3); stop = true; break; }
                 // the previous motion must be accepted before this one builds on it
                 if (pending_ext) {
                     node = cp_pair_result(tm, bx, over);
@@ -2129,7 +2131,6 @@ __device__ void cp_plan_query_pair(const Team& tm, TeamWS& ws, TeamWS& wsc, Pair
                     icur = prev;
                 }
                 CP_PF_ADD(PF_WAIT, t_w);
-                if (it2 < 0) { CP_WHY(3); stop = true; break; }
                 if (over || cp_stop_poll_read(tm, ws, &Q.stop)) { CP_WHY(7); stop = true; break; }
                 if (!ok1) { st.v[ST_PFAIL]++; break; }
                 cp_copy(tm, ws.qe, ws.seg[W - 1]);
@@ -2154,9 +2155,14 @@ __device__ void cp_plan_query_pair(const Team& tm, TeamWS& ws, TeamWS& wsc, Pair
             }
             CP_TL(13);
             // drain: motions still being certified are kept (the reference
-            // appends every accepted motion of a trapped connect too)
-            if (pending_ext) { node = cp_pair_result(tm, bx, over); pending_ext = false; if (node == -4) full = true; }
-            if (pending_con) { const int r = cp_pair_result(tm, bx, over); if (r == -4) full = true; }
+            // appends every accepted motion of a trapped connect too) -- unless
+            // the query is over: then the team leaves at once and C finishes
+            // its job on its own (its append, if any, stays inside the slots
+            // the reset refills: cp_reset_kernel covers the final count)
+            if (!stop) {
+                if (pending_ext) { node = cp_pair_result(tm, bx, over); pending_ext = false; if (node == -4) full = true; }
+                if (pending_con) { const int r = cp_pair_result(tm, bx, over); if (r == -4) full = true; }
+            }
         }
         if (node >= 0) st.v[ST_ADDED]++;
         if (full) {
@@ -2817,7 +2823,9 @@ extern "C" __global__ void __launch_bounds__(64) cp_check_kernel(const __grid_co
 extern "C" __global__ void cp_reset_kernel(QueryState* qs, float* trees, int* parents, int cap, int nq) {
     for (int qk = blockIdx.y; qk < 2 * nq; qk += gridDim.y) {
         const int qi = qk >> 1, k = qk & 1;
-        const int h = min(qs[qi].hwm[k], cap);
+        // every slot appended, including by a certifier still finishing its
+        // job after the query's finalizer ran (count is final: the planner grid is done)
+        const int h = min(max(qs[qi].hwm[k], qs[qi].count[k]), cap);
         if (k == 0 && blockIdx.x == 0 && threadIdx.x == 0) { qs[qi].stop = 0; qs[qi].setup_code = 0; }
         float* base = trees + (size_t)qk * CP_N * cap;
         int* pb = parents + (size_t)qk * cap;
