@@ -1909,6 +1909,38 @@ __device__ __forceinline__ int cp_pair_result(const Team& tm, PairBox& bx, bool&
     return tm.bcast(bx.result, 0);
 }
 
+__device__ int cp_check_config_d(const SetupArgs& S, const double* q, int lane, int nl, unsigned mask);   // below
+
+// The single query's FP64 endpoint checks (planner.py:416-427), on the
+// certifier warps of the first two teams before their first job (P's first
+// projection takes far longer): team 0 checks the start, team 1 the goal
+// (team 0 both if it is alone).  A bad endpoint stops the query at once; the
+// second check to finish combines the codes as cp_check_kernel does, writes
+// setup_code to the results and then the check's completion word.
+__device__ __noinline__ void cp_pair_endpoint_checks(const Team& tm, const PlanArgs& A, int gteam, int n_teams) {
+    const SetupArgs& S = A.chk;
+    QueryState& Q = A.qs[0];
+    for (int w = gteam; w < 2; w += n_teams) {
+        const double* q = w == 0 ? S.starts : S.goals;
+        const int code = cp_check_config_d(S, q, (int)tm.lane, CP_G, tm.mask);
+        if (tm.lane == 0) {
+            Q.chk_code[w] = code;
+            if (code) atomicExch(&Q.stop, 1);
+            __threadfence();
+            if (atomicAdd(&Q.chk_cnt, 1) == 1) {   // both verdicts are in
+                const int c0 = cp_ldvol(&Q.chk_code[0]), c1 = cp_ldvol(&Q.chk_code[1]);
+                const int c = c0 ? c0 : (c1 ? 3 + c1 : 0);
+                QueryOut& O = A.out[0];
+                O.setup_code = c;
+                if (c) Q.setup_code = c;
+                __threadfence_system();
+                *(volatile unsigned*)&O.chk_seq = (unsigned)A.seeds[1];   // the call's sequence number
+            }
+        }
+        tm.sync();
+    }
+}
+
 // warp C: certify jobs until P posts the exit job
 __device__ void cp_pair_certifier(const Team& tm, TeamWS& ws, PairBox& bx, const PlanArgs& A, const SceneSm& sc) {
 #ifdef CP_PROFILE
@@ -2558,6 +2590,7 @@ __device__ __noinline__ void cp_extract_query(const Team tm, const PlanArgs& A, 
         O.stats[7] = (u64)cp_ldvol(&Q.pad1_[5]);   // the winner out
 #endif
         O.device_ms = (double)(tend - Q.t0_ns) * 1e-6;
+        O.total_ms = (double)(cp_clock_ns() - Q.t0_ns) * 1e-6;
     }
     if (A.nq == 1) {   // single query: every lane's result stores reach the host before the completion word
         __threadfence_system();
@@ -2620,6 +2653,7 @@ cp_plan_kernel(const __grid_constant__ PlanArgs A) {
         const int w = threadIdx.x >> 5;
         bx = cp_pair_box(&wsa[(w & ~1) * (32 / CP_G) + 1]);
         if (w & 1) {
+            if (A.chk_in_kernel && gteam < 2) cp_pair_endpoint_checks(tm, A, gteam, n_teams);
             cp_pair_certifier(tm, ws, *bx, A, sc);
             asm volatile("cp.async.wait_all;" ::: "memory");   // the last stop-word poll has landed
             return;
@@ -2694,8 +2728,8 @@ cp_plan_kernel(const __grid_constant__ PlanArgs A) {
 // FP64 endpoint test of one configuration (planner.py:416-427
 // _check_endpoint): limits, manifold, collision; one warp.
 
-__device__ int cp_check_config_d(const SetupArgs& S, const double* q, int lane) {
-    // 1 limits, 2 manifold, 3 collision, 0 ok  (evaluated by all 32 lanes)
+__device__ int cp_check_config_d(const SetupArgs& S, const double* q, int lane, int nl, unsigned mask) {
+    // 1 limits, 2 manifold, 3 collision, 0 ok  (evaluated by the nl lanes of mask)
     bool lim = false;
 #pragma unroll
     for (int k = 0; k < CP_N; k++) lim |= (q[k] < cp_lo(k) || q[k] > cp_hi(k));
@@ -2714,7 +2748,7 @@ __device__ int cp_check_config_d(const SetupArgs& S, const double* q, int lane) 
     bool hit = false;
     const int E = S.nb + S.ne;
     const int total = CP_S * E + CP_P;
-    for (int c = lane; c < total; c += 32) {
+    for (int c = lane; c < total; c += nl) {
         double cl;
         if (c < CP_S * E) {
             int si = c / E, pi = c - si * E;
@@ -2750,7 +2784,7 @@ __device__ int cp_check_config_d(const SetupArgs& S, const double* q, int lane) 
         }
         hit |= cl < 0.0;
     }
-    return __any_sync(0xffffffffu, hit) ? 3 : 0;
+    return __any_sync(mask, hit) ? 3 : 0;
 }
 
 #if !CP_PARITY
@@ -2779,6 +2813,7 @@ extern "C" __global__ void __launch_bounds__(32) cp_init_kernel(const __grid_con
         Q.next_sample = 0;
         Q.solved = 0; Q.timed_out = 0; Q.overflow = 0; Q.exhausted = 0; Q.race_stopped = 0;
         Q.active = 0;
+        Q.chk_cnt = 0;
         Q.meet[0] = -1; Q.meet[1] = -1;
         Q.t0_ns = cp_clock_ns();
         Q.t_end_ns = 0;
@@ -2801,7 +2836,7 @@ extern "C" __global__ void __launch_bounds__(64) cp_check_kernel(const __grid_co
     QueryState& Q = S.qs[qi];
     __shared__ int codes[2];
     const double* q = (w == 0 ? S.starts : S.goals) + (size_t)qi * CP_N;
-    int code = cp_check_config_d(S, q, lane);
+    int code = cp_check_config_d(S, q, lane, 32, 0xffffffffu);
     if (lane == 0) codes[w] = code;
     __syncthreads();
     if (threadIdx.x == 0) {
@@ -2955,7 +2990,7 @@ extern "C" __global__ void cp_project_config_kernel(int B, Con<double> cd, doubl
 extern "C" __global__ void cp_check_config_kernel(int B, const __grid_constant__ SetupArgs S, const double* q, int* code) {
     int i = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
     if (i >= B) return;
-    int c = cp_check_config_d(S, q + (size_t)i * CP_N, threadIdx.x & 31);
+    int c = cp_check_config_d(S, q + (size_t)i * CP_N, threadIdx.x & 31, 32, 0xffffffffu);
     if ((threadIdx.x & 31) == 0) code[i] = c;
 }
 

@@ -68,10 +68,31 @@ struct alignas(128) QueryState {
     int count[2];          // tree node counters (atomic append)
     int next_sample;       // Halton index counter (= reference iteration)
     int active;            // teams inside the query (the last one out extracts)
-    int pad2_[28];
+    int chk_code[2];       // in-kernel endpoint checks (single query): start / goal verdicts
+    int chk_cnt;           // endpoint checks done
+    int pad2_[25];
     // line 2: stats (one atomicAdd per team and counter)
     u64 stats[ST_NSTAT];
     u64 pad3_[16 - ST_NSTAT];
+};
+
+struct SetupArgs {
+    QueryState* qs;
+    const double* starts;   // (nq, CP_N)
+    const double* goals;
+    const i64* seeds;
+    float* trees;
+    int* parents;
+    int cap;
+    Con<double> con;
+    double tau_task;
+    const double* box_min;  // (nb,3) FP64 scene for the exact endpoint test
+    const double* box_max;
+    const double* sph_c;
+    const double* sph_r;
+    int nb, ne;
+    int* counters;          // planner queue counters, zeroed by block 0 (may be null)
+    struct QueryOut* out;   // endpoint-check codes go straight to the results
 };
 
 struct PlanArgs {
@@ -103,25 +124,10 @@ struct PlanArgs {
     int path_cap;
     int pair;              // 1: two-warp teams (single queries; warp P projects, warp C certifies)
     const i64* seeds;      // (nq) Halton offsets (= QueryState.seed_offset; read before init completes)
-};
-
-struct SetupArgs {
-    QueryState* qs;
-    const double* starts;   // (nq, CP_N)
-    const double* goals;
-    const i64* seeds;
-    float* trees;
-    int* parents;
-    int cap;
-    Con<double> con;
-    double tau_task;
-    const double* box_min;  // (nb,3) FP64 scene for the exact endpoint test
-    const double* box_max;
-    const double* sph_c;
-    const double* sph_r;
-    int nb, ne;
-    int* counters;          // planner queue counters, zeroed by block 0 (may be null)
-    struct QueryOut* out;   // endpoint-check codes go straight to the results
+    // single query in pair mode: the FP64 endpoint checks run on the first
+    // two teams' certifier warps (no cp_check_kernel launch in the graph)
+    int chk_in_kernel;
+    SetupArgs chk;
 };
 
 struct QueryOut {
@@ -132,6 +138,7 @@ struct QueryOut {
     int n_nodes[2];
     int pad;
     double device_ms;
+    double total_ms;       // init -> the last team out (globaltimer)
     u64 stats[ST_NSTAT];
     // completion words (the call's sequence number, from the input block):
     // written last, behind a system-scope fence, by the query's finalizer and
