@@ -9,10 +9,13 @@ waypoints per motion; start/goal pairs from the reference's own generate_pair
 
 A step = plan Q queries one after another, each with the whole GPU (one
 persistent-kernel launch per query).  value = median planning time of the
-solved queries on the device (inputs resident: CUDA events from the H2D copy
-to the results); e2e = the same median through the public plan() call (host
-buffers in, H2D + D2H inside the timed region); success rate beside it.  The
-L2 is flushed (256 MiB write) before every query.
+solved queries on the device (inputs resident): the planner's own clock
+(globaltimer) from the init kernel's start to the last team leaving the
+query, when the results are complete -- the single-query graph records no
+CUDA events ("Teardown after the solve"; r2s and earlier: events
+from the H2D copy to the results); e2e = the same median through the public
+plan() call (host buffers in, H2D + D2H inside the timed region); success
+rate beside it.  The L2 is flushed (256 MiB write) before every query.
 
 Every N also reports ``throughput``: BASELINE configs[4], 1024 independent
 constrained queries per GPU per step in one persistent launch (weak scaling:
@@ -340,6 +343,7 @@ def run_b200(args, world, rank, local):
         "config": headline_config(args, world),
         "device_options": {"teams": args.teams or "auto", "cc_broadphase": args.cc_broadphase},
         "l2": "flushed (256 MiB write) before every query",
+        "value_clock": "planner globaltimer, init kernel start -> last team out of the query (results complete)",
         "success_rate": len(solved) / max(1, len(all_recs)),
         "success_rate_feasible": sum(r["solved"] for r in rf) / max(1, len(rf)),
         "feasible_note": "14 of the 100 pairs are unsolved by the reference planner too (3 seeds x 20 s, "
