@@ -1829,6 +1829,18 @@ __device__ __noinline__ int cp_extend_once(const Team& tm, TeamWS& ws, const Pla
 
 __device__ __noinline__ void cp_extract_path(const Team tm, const PlanArgs& A, int qi, int meet0, int meet1,
                                              float (*stage)[CP_NP]);   // below
+__device__ __noinline__ void cp_extract_query(const Team tm, const PlanArgs& A, int qi);   // below
+
+// add a team's counters to the query's (lane 0, the non-zero ones) and clear them
+__device__ __forceinline__ void cp_flush_stats(const Team& tm, QueryState& Q, Stats& st) {
+    if (tm.lane == 0) {
+#pragma unroll
+        for (int i = 0; i < ST_NSTAT; i++)
+            if (st.v[i]) atomicAdd(&Q.stats[i], st.v[i]);
+    }
+#pragma unroll
+    for (int i = 0; i < ST_NSTAT; i++) st.v[i] = 0ull;
+}
 
 // ===========================================================================
 // Pair mode (single queries): a team is two warps.  Warp P draws samples and
@@ -2065,6 +2077,10 @@ __device__ void cp_plan_query_pair(const Team& tm, TeamWS& ws, TeamWS& wsc, Pair
 #define CP_TL(id) ((void)0)
 #endif
     for (int round = 0;; round++) {
+        // counters go to the query every round: a solved query's result
+        // carries the work finished by the time it was solved (the solving
+        // team finalises it at once, without waiting for the others to leave)
+        if (round > 0) cp_flush_stats(tm, Q, st);
         CP_PF_T0(t_stop); CP_TL(1);
         if (!(round == 0 && first_it > 0 && A.budget_ns >= 0) && cp_should_stop(tm, Q, A)) { CP_WHY(0); break; }
         CP_PF_ADD(PF_STOP, t_stop);
@@ -2247,6 +2263,9 @@ __device__ void cp_plan_query_pair(const Team& tm, TeamWS& ws, TeamWS& wsc, Pair
             if (tm.bcast(won, 0)) {   // while the other teams leave
                 CP_WHY(6);
                 cp_extract_path(tm, A, qi, a == 0 ? node : meet, a == 0 ? meet : node, ws.seg);
+                cp_flush_stats(tm, Q, st);
+                __threadfence();
+                cp_extract_query(tm, A, qi);   // the result is complete: counters, node counts, completion word
             }
             else CP_WHY(4);
             break;
@@ -2713,7 +2732,8 @@ cp_plan_kernel(const __grid_constant__ PlanArgs A) {
             __threadfence();
             last = atomicSub(&Q.active, 1) == 1;
         }
-        if (tm.bcast(last, 0)) {
+        // (pair mode: a solved query was finalised by the team that solved it)
+        if (tm.bcast(last, 0) && !(bx && cp_ldvol(&Q.solved))) {
             __threadfence();
             cp_extract_query(tm, A, qi);
         }
