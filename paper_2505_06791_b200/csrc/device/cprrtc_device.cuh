@@ -2569,7 +2569,9 @@ __device__ __noinline__ void cp_extract_path(const Team tm, const PlanArgs& A, i
         Q.pad1_[1] = (int)(cp_clock_ns() - Q.t0_ns);
 #endif
     }
-    if (A.nq == 1) __threadfence_system();   // the path reaches the host before the finalizer's completion word
+    // the path reaches the host before the finalizer's completion word (pair
+    // mode: the same lanes finalise next, behind their own system fence)
+    if (A.nq == 1 && !A.pair) __threadfence_system();
     tm.sync();
 }
 
