@@ -159,7 +159,12 @@ CPRRTC_API int cprrtc_set_constraint(void *ctx, const cprrtc_constraint *con);
 CPRRTC_API int cprrtc_prepare(void *ctx, int width);
 /* launches of this library's kernels since context creation */
 CPRRTC_API int64_t cprrtc_launch_count(void *ctx);
-/* device time (CUDA events) of the last cprrtc_plan: whole call / plan kernel */
+/* device time of the last cprrtc_plan: whole call / plan kernel.  Batches:
+ * CUDA events (H2D copy -> results; the planner kernel).  A single query (its
+ * lean graph records no events): the planner's own clock, init -> the result
+ * complete / init -> solved.  cprrtc_plan returns for a single query as soon
+ * as its result is complete (completion words in mapped memory), before the
+ * planner grid retires; later calls on the context are stream-ordered. */
 CPRRTC_API int cprrtc_last_timing(void *ctx, double *total_ms, double *plan_kernel_ms);
 /* overwrite `bytes` of device scratch (L2 flush between timed iterations) */
 CPRRTC_API int cprrtc_flush_l2(void *ctx, size_t bytes);
@@ -238,7 +243,8 @@ CPRRTC_API int cprrtc_plan_wait(void *ctx, int B, cprrtc_result *results, int64_
                                 int32_t *sources, int64_t flat_capacity);
 /* device time (CUDA events) from the start of ctx_from's last submitted batch
  * to the end of ctx_to's (same device): a pipelined stream of batches */
-CPRRTC_API int cprrtc_elapsed_ms(void *ctx_from, void *ctx_to, double *ms);
+CPRRTC_API int cprrtc_elapsed_ms(void *ctx_from, void *ctx_to, double *ms);   /* (batches and races:
+                                      a single-query launch records no events -> CPRRTC_EARG) */
 /* cprrtc_plan's batch sharded over n_ctx contexts (typically one per GPU):
  * context k plans the contiguous slice [k*B/n_ctx, (k+1)*B/n_ctx); every shard
  * is launched before any is awaited, and the results land in the caller's
