@@ -37,6 +37,9 @@
 #define CP_NP ((CP_N % 2) ? CP_N : (CP_N + 1))   // odd row pitch: no bank conflicts
 #define CP_CHUNK 8
 #define CP_VOTE 4                    // lockstep CC: early-exit vote every CP_VOTE chunks
+#ifndef CP_NN_PAIRS
+#define CP_NN_PAIRS 1                // planner NN: two chunks per L2 round trip
+#endif
 #define CP_BCH (2 + 2 * CP_CHUNK)   // float4s per box chunk of the clustered scene
 #define CP_SCH (2 + CP_CHUNK)       // float4s per sphere chunk
 #define CP_INTMAX 0x7fffffff
@@ -1490,7 +1493,22 @@ __device__ __noinline__ int cp_nearest_ld(const Team tm, const float* nodes, int
     for (int k = 0; k < CP_N; k++) bc[k] = 0.f;
     take(v, 4 * lane);
     const int n4 = (count + 3) >> 2;
-    for (int i4 = lane + CP_G; i4 < n4; i4 += CP_G) {
+    int i4 = lane + CP_G;
+#if CP_NN_PAIRS
+    // two chunks per round trip: their loads are issued together (a tree of
+    // ~500 nodes is ~8 chunks per lane: 4 L2 round trips instead of 8)
+    for (; i4 + CP_G < n4; i4 += 2 * CP_G) {
+        float4 u[CP_N];
+#pragma unroll
+        for (int k = 0; k < CP_N; k++) {
+            v[k] = cp_ldcg4(nodes + (size_t)k * cap + 4 * i4);
+            u[k] = cp_ldcg4(nodes + (size_t)k * cap + 4 * (i4 + CP_G));
+        }
+        take(v, 4 * i4);
+        take(u, 4 * (i4 + CP_G));
+    }
+#endif
+    for (; i4 < n4; i4 += CP_G) {
 #pragma unroll
         for (int k = 0; k < CP_N; k++) v[k] = cp_ldcg4(nodes + (size_t)k * cap + 4 * i4);
         take(v, 4 * i4);
