@@ -1845,8 +1845,9 @@ __device__ __noinline__ int cp_extend_once(const Team& tm, TeamWS& ws, const Pla
     return node < 0 ? -4 : node;
 }
 
+struct PairBox;
 __device__ __noinline__ void cp_extract_path(const Team tm, const PlanArgs& A, int qi, int meet0, int meet1,
-                                             float (*stage)[CP_NP]);   // below
+                                             float (*stage)[CP_NP], const PairBox* bx);   // below
 __device__ __noinline__ void cp_extract_query(const Team tm, const PlanArgs& A, int qi);   // below
 
 // add a team's counters to the query's (lane 0, the non-zero ones) and clear them
@@ -1873,6 +1874,12 @@ __device__ __forceinline__ void cp_flush_stats(const Team& tm, QueryState& Q, St
 // warp): two mbarriers -- `full` (P's 16 lanes arrive after writing a job, C
 // waits), `done` (C's 16 lanes arrive after finishing it, P waits) -- give the
 // hand-offs release / acquire ordering without a CTA barrier.
+// C's ancestor-chain cache (per tree): entries pw_anc[t][h .. h + len) are the
+// node C appended last in tree t and its ancestors, root last when pw_root;
+// sized to what the TeamWS slot holds beside the mailbox (48 for arm7)
+#define CP_PW_FIT (((64 + (CP_G + 7) * CP_NP * 4) - (124 + 8 * CP_NP)) / 8)
+#define CP_PW (CP_PW_FIT < 2 ? 2 : (CP_PW_FIT < 48 ? CP_PW_FIT : 48))
+#define CP_PW_SLACK (CP_PW / 4)    // room to prepend connect nodes
 struct PairBox {
     unsigned long long full, done;   // mbarriers
     int result;                      // new node index, or -2 projection, -3 collision, -4 full
@@ -1880,10 +1887,14 @@ struct PairBox {
     int qi, tree, parent, derive, exit;
     int p_ndone, p_pend;             // P's bookkeeping: done phases consumed, a result outstanding
     float from[CP_NP], to[CP_NP];
+    int pw_h[2], pw_len[2], pw_root[2];
+    int pw_anc[2][CP_PW];
 #ifdef CP_PROFILE
     unsigned long long cprof[6];     // warp C clock64 phases: P2, CC, append, jobs, idle, P2 iterations
 #endif
 };
+static_assert(sizeof(PairBox) <= sizeof(TeamWS), "the pair mailbox must fit a team workspace slot");
+static_assert(CP_PW <= 4 * CP_G, "a cached chain fits the extraction's register slots");
 __device__ __forceinline__ PairBox* cp_pair_box(TeamWS* slot) {
     return reinterpret_cast<PairBox*>((reinterpret_cast<unsigned long long>(slot) + 7ull) & ~7ull);
 }
@@ -1999,6 +2010,7 @@ __device__ void cp_pair_certifier(const Team& tm, TeamWS& ws, PairBox& bx, const
         int res;
         bool ok;
         int polled = 0;
+        int walk_tree = -1;
         if (bx.derive) {
             if ((int)tm.lane < CP_N) { ws.qr[tm.lane] = bx.from[tm.lane]; ws.qn[tm.lane] = bx.to[tm.lane]; }
             tm.sync();
@@ -2040,6 +2052,22 @@ __device__ void cp_pair_certifier(const Team& tm, TeamWS& ws, PairBox& bx, const
                 if (st.v[i]) atomicAdd(&Q.stats[i], st.v[i]);
             bx.result = res;
             bx.over = over;
+            if (res >= 0) {   // the ancestor cache of tree `tree` now starts at the new node
+                const int t = tree, par = bx.parent;
+                if (bx.pw_len[t] > 0 && bx.pw_anc[t][bx.pw_h[t]] == par && bx.pw_h[t] > 0) {
+                    const int h = bx.pw_h[t] - 1;   // a connect chain: prepend
+                    bx.pw_anc[t][h] = res;
+                    bx.pw_h[t] = h;
+                    bx.pw_len[t] = bx.pw_len[t] + 1;
+                } else {                           // a new chain: the node and its parent, ancestors below
+                    bx.pw_h[t] = CP_PW_SLACK;
+                    bx.pw_anc[t][CP_PW_SLACK] = res;
+                    bx.pw_anc[t][CP_PW_SLACK + 1] = par;
+                    bx.pw_root[t] = 0;
+                    bx.pw_len[t] = 2;
+                    walk_tree = t;
+                }
+            }
 #ifdef CP_TIMELINE
             // the longest job running across the solve: (ns after the solve) & ~15 | kind
             // (1 derive ok, 2 derive failed, 3 check ok, 4 check failed)
@@ -2048,8 +2076,37 @@ __device__ void cp_pair_certifier(const Team& tm, TeamWS& ws, PairBox& bx, const
                 atomicMax(&Q.pad1_[0], (int)((((now - ts) >> 4) << 4) | (u64)((bx.derive ? 1 : 3) + (ok ? 0 : 1))));
 #endif
         }
+        walk_tree = tm.bcast(walk_tree, 0);
         tm.sync();
         cp_mb_arrive(&bx.done);   // every lane: release
+        // Idle until the next job: walk the new chain's ancestors (dependent L2
+        // loads) into the cache, so the team that solves the query finds its
+        // path's parent chains in shared memory instead of walking them.  A
+        // posted job ends the walk (non-blocking mbarrier test between steps).
+        if (walk_tree >= 0 && tm.lane == 0) {
+            const int t = walk_tree;
+            const int* pp = cp_par(A, qi, t);
+            int h = bx.pw_h[t], len = bx.pw_len[t], cur = bx.pw_anc[t][h + len - 1];
+            while (h + len < CP_PW) {
+                unsigned posted;
+                asm volatile("{ .reg .pred p; mbarrier.test_wait.parity.shared::cta.b64 p, [%1], %2; "
+                             "selp.u32 %0, 1, 0, p; }"
+                             : "=r"(posted) : "r"(cp_smem_addr(&bx.full)), "r"((nfull + 1) & 1) : "memory");
+                if (posted) break;
+                int q = cp_ldvol(pp + cur);
+                if (q < 0) break;   // not landed yet: leave it to the extraction's walk
+                if (q == cur) {
+                    *(volatile int*)&bx.pw_root[t] = 1;
+                    break;
+                }
+                bx.pw_anc[t][h + len] = q;
+                __threadfence_block();
+                *(volatile int*)&bx.pw_len[t] = ++len;
+                cur = q;
+            }
+        }
+        walk_tree = -1;
+        tm.sync();
     }
 }
 
@@ -2280,7 +2337,7 @@ __device__ void cp_plan_query_pair(const Team& tm, TeamWS& ws, TeamWS& wsc, Pair
             }
             if (tm.bcast(won, 0)) {   // while the other teams leave
                 CP_WHY(6);
-                cp_extract_path(tm, A, qi, a == 0 ? node : meet, a == 0 ? meet : node, ws.seg);
+                cp_extract_path(tm, A, qi, a == 0 ? node : meet, a == 0 ? meet : node, ws.seg, &bx);
                 cp_flush_stats(tm, Q, st);
                 __threadfence();
                 cp_extract_query(tm, A, qi);   // the result is complete: counters, node counts, completion word
@@ -2374,7 +2431,7 @@ __device__ void cp_plan_query(const Team& tm, TeamWS& ws, const PlanArgs& A, con
                 won = 1;
             }
             if (tm.bcast(won, 0))   // while the other teams leave
-                cp_extract_path(tm, A, qi, a == 0 ? node : meet, a == 0 ? meet : node, ws.seg);
+                cp_extract_path(tm, A, qi, a == 0 ? node : meet, a == 0 ? meet : node, ws.seg, nullptr);
             break;
         }
     }
@@ -2477,7 +2534,7 @@ __device__ __forceinline__ SceneSm cp_stage_scene(const SceneSm& g, float4* sm) 
 // by cp_check_kernel.
 #define CP_XK 4
 __device__ __noinline__ void cp_extract_path(const Team tm, const PlanArgs& A, int qi, int meet0, int meet1,
-                                             float (*stage)[CP_NP]) {
+                                             float (*stage)[CP_NP], const PairBox* bx) {
     QueryOut& O = A.out[qi];
     const int lane = (int)tm.lane, cap = A.cap, path_cap = A.path_cap;
     const float* ts = cp_tree(A, qi, 0);
@@ -2500,6 +2557,37 @@ __device__ __noinline__ void cp_extract_path(const Team tm, const PlanArgs& A, i
     for (int j = 0; j < CP_XK; j++) { rs[j] = 0; rg[j] = 0; }
     int cur = lane == 0 ? meet0 : meet1, cnt = 0;
     bool walking = lane < 2;
+    // pair mode: the certifier's ancestor cache of tree `lane` (lanes 0 / 1),
+    // when it starts at this chain's meet node (root flag, then length, then entries)
+    const int* cc = nullptr;
+    int clen = 0, ch0 = 0;
+    bool croot = false;
+    if (bx && walking) {
+        croot = *(const volatile int*)&bx->pw_root[lane] != 0;
+        __threadfence_block();
+        clen = *(const volatile int*)&bx->pw_len[lane];
+        ch0 = *(const volatile int*)&bx->pw_h[lane];
+        __threadfence_block();
+        if (clen > 0 && bx->pw_anc[lane][ch0] == cur) cc = &bx->pw_anc[lane][ch0];
+        else clen = 0;
+    }
+#ifdef CP_TIMELINE
+    const int dbg_clen = clen, dbg_croot = croot ? 1 : 0;
+#endif
+    if (bx) {   // both chains cached down to their roots: every lane takes its entries from shared memory
+        const int l0 = tm.bcast(croot ? clen : 0, 0), l1 = tm.bcast(croot ? clen : 0, 1);
+        const int h0 = tm.bcast(ch0, 0), h1 = tm.bcast(ch0, 1);
+        if (l0 > 0 && l1 > 0) {   // (a cache holds at most CP_PW <= CP_XK CP_G entries)
+#pragma unroll
+            for (int j = 0; j < CP_XK; j++) {
+                const int e = CP_G * j + lane;
+                rs[j] = e < l0 ? bx->pw_anc[0][h0 + e] : 0;
+                rg[j] = e < l1 ? bx->pw_anc[1][h1 + e] : 0;
+            }
+            cnt = lane == 0 ? l0 : l1;
+            walking = false;
+        }
+    }
     for (int c = 0;; c++) {
         const unsigned wm = tm.ballot(walking);
         if (!(wm & 3u) || c > cap) break;   // (a chain is never longer than its tree)
@@ -2518,12 +2606,20 @@ __device__ __noinline__ void cp_extract_path(const Team tm, const PlanArgs& A, i
                 else ch[path_cap - 1 - c] = (1 << 30) | cur;             // goal chain, from the end
             }
             cnt++;
-            const int p = parent_of(lane == 0 ? ps : pg, cur);
+            const int p = c + 1 < clen ? cc[c + 1]
+                                       : (croot && c + 1 == clen ? cur : parent_of(lane == 0 ? ps : pg, cur));
             if (p == cur) walking = false;
             else cur = p;
         }
     }
     const int ca = tm.bcast(cnt, 0), cb = tm.bcast(cnt, 1);
+#ifdef CP_TIMELINE
+    {   // diagnostic: cached chain lengths / root flags / chain lengths of both trees
+        const int l0 = tm.bcast(dbg_clen, 0), l1 = tm.bcast(dbg_clen, 1);
+        const int r0 = tm.bcast(dbg_croot, 0), r1 = tm.bcast(dbg_croot, 1);
+        if (lane == 0) A.qs[qi].pad1_[5] = (l0 << 24) | (l1 << 16) | (r0 << 15) | (r1 << 14) | (min(ca, 127) << 7) | min(cb, 127);
+    }
+#endif
     const int skip = tm.ballot(lane < CP_N && cm0 != cm1) == 0u ? 1 : 0;
     const int len = ca + cb - skip;
     int status = 0;
@@ -2676,6 +2772,8 @@ cp_plan_kernel(const __grid_constant__ PlanArgs A) {
             PairBox* b = cp_pair_box(&wsa[w * (32 / CP_G) + 1]);
             cp_mb_init(&b->full, CP_G);
             cp_mb_init(&b->done, CP_G);
+            b->pw_len[0] = 0;
+            b->pw_len[1] = 0;
             b->p_ndone = 0;
             b->p_pend = 0;
         }

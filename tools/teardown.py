@@ -79,3 +79,10 @@ if TIMELINE:
     for k, c in collections.Counter(kind.tolist()).most_common():
         sel = kind == k
         print(f"    {KN.get(k, k)}: {c} ({np.median((raw6[sel] & ~15) * 1e-3):.1f})")
+    raw7 = np.array([r[7] for r in RAW], np.int64)
+    l0, l1 = (raw7 >> 24) & 255, (raw7 >> 16) & 255
+    r0, r1 = (raw7 >> 15) & 1, (raw7 >> 14) & 1
+    ca, cb = (raw7 >> 7) & 127, raw7 & 127
+    print(f"  path chains (start / goal) median {np.median(ca):.0f} / {np.median(cb):.0f} nodes; certifier cache hit "
+          f"{np.mean(l0 > 0)*100:.0f} % / {np.mean(l1 > 0)*100:.0f} %, complete to the root {np.mean(r0)*100:.0f} % / "
+          f"{np.mean(r1)*100:.0f} %, cached entries median {np.median(l0):.0f} / {np.median(l1):.0f}")
