@@ -374,3 +374,29 @@ def test_fast_and_ctypes_single_query_paths(oracle):
         assert set(r.edge_sources) <= {"start", "junction", "goal"}
         assert r.stats.wall_ms > 0 and r.stats.device_ms > 0 and r.stats.nodes_start >= 1
         _check_path(oracle, prob, r)
+
+
+def test_endpoint_collision_codes_and_one_team_launch():
+    """The single-query endpoint checks run on the certifier warps of the
+    first two teams (the lean graph, no check kernel): a colliding start /
+    goal raises the reference's PlanSetupError (planner.py:426-427, codes 3 /
+    6), the start's verdict wins when both are bad, and a launch small enough
+    to hold one team (max_iterations 1) checks both endpoints on it."""
+    from paper_2505_06791_b200.errors import PlanSetupError
+    from paper_2505_06791_b200.geometry import Aabb, Scene
+    from paper_2505_06791_b200.planner import PlanParams, PlanProblem, plan
+    m = fx.robot("planar2")
+    # link sphere 0 sits on the r = 0.25 circle at angle q0: a box at angle 0
+    box = Scene(boxes=[Aabb([0.2, -0.05, -0.1], [0.3, 0.05, 0.1])])
+    hit, free = np.array([0.0, 0.0]), np.array([np.pi / 2, 0.0])
+    for iters in (1, 2000):
+        prm = PlanParams(width=8, max_iterations=iters)
+        with pytest.raises(PlanSetupError, match="start is in collision"):
+            plan(PlanProblem(m, box, None, hit, free, prm))
+        with pytest.raises(PlanSetupError, match="goal is in collision"):
+            plan(PlanProblem(m, box, None, free, hit, prm))
+        with pytest.raises(PlanSetupError, match="start is in collision"):
+            plan(PlanProblem(m, box, None, hit, hit + np.array([0.0, 0.3]), prm))
+    # one team, valid endpoints: the query ends (IterLimit or solved), no hang
+    r = plan(PlanProblem(m, box, None, free, np.array([2.5, 0.3]), PlanParams(width=8, max_iterations=1)))
+    assert r.status in ("IterLimit", "Solved")
