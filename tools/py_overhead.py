@@ -1,7 +1,8 @@
-"""Host-side split of one plan() call on the bench workload (back to back):
-the Python phases of planner._plan_one timed separately, and -- with
-CPRRTC_HOST_PROFILE=1 -- the C call's own phases (printed by the library at
-exit)."""
+"""Host-side split of one single-query call on the bench workload (back to
+back), through the ctypes path of planner._plan_one (the one plan() takes
+without the _cprrtc_fast module): its Python phases timed separately, and --
+with CPRRTC_HOST_PROFILE=1 -- the C call's own phases (printed by the library
+at exit).  tools/teardown.py times plan() itself (fast path)."""
 import os, sys, time
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path[:0] = [ROOT, os.path.join(ROOT, "tests")]
