@@ -37,6 +37,9 @@
 #define CP_NP ((CP_N % 2) ? CP_N : (CP_N + 1))   // odd row pitch: no bank conflicts
 #define CP_CHUNK 8
 #define CP_VOTE 4                    // lockstep CC: early-exit vote every CP_VOTE chunks
+#ifndef CP_ROOT_FIRST
+#define CP_ROOT_FIRST 1              // single query: the first extension's nearest node is the root
+#endif
 #ifndef CP_NN_PAIRS
 #define CP_NN_PAIRS 1                // planner NN: two chunks per L2 round trip
 #endif
@@ -2181,7 +2184,21 @@ __device__ void cp_plan_query_pair(const Team& tm, TeamWS& ws, TeamWS& wsc, Pair
         CP_PF_T0(t_nn); CP_TL(3);
         // extension P1 (planner.py:265-281)
         int cnt_a;
-        const int inear = cp_nearest_ld(tm, cp_tree(A, qi, a), A.cap, &Q.count[a], ws.qr, ws.qn, &cnt_a);
+        int inear;
+#if CP_ROOT_FIRST
+        if (round == 0 && first_it > 0) {
+            // a single query's first extension: every team starts at once and
+            // no motion has been appended yet, so tree a is its root (node 0)
+            // -- the root's stored coordinates without the L2 round trip
+            // (nodes another team appends meanwhile are as if drawn later)
+            if ((int)tm.lane < CP_N)
+                ws.qn[tm.lane] = (float)(a == 0 ? A.chk.starts : A.chk.goals)[tm.lane];
+            tm.sync();
+            inear = 0;
+            cnt_a = 1;
+        } else
+#endif
+            inear = cp_nearest_ld(tm, cp_tree(A, qi, a), A.cap, &Q.count[a], ws.qr, ws.qn, &cnt_a);
         st.v[ST_NNODES] += cnt_a;
         cp_steer(tm, ws.qn, ws.qr, A.step, ws.qs);
         if (cp_vec_equal(tm, ws.qs, ws.qn)) continue;

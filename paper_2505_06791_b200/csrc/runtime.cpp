@@ -1459,7 +1459,7 @@ static int plan_launch(Ctx* c, const cprrtc_params* prm, int B, const double* st
     static const bool pdl_on = !(getenv("CPRRTC_PDL") && atoi(getenv("CPRRTC_PDL")) == 0);
     const bool lean = pair && !race && pdl_on;
     A.chk_in_kernel = lean ? 1 : 0;
-    if (lean) A.chk = S;
+    if (pair) A.chk = S;   // (the pair planner also reads the roots' FP64 inputs through it)
     if (int rc = upload_conf(c, m)) return rc;
     // the per-call sequence as one CUDA graph, replayed while shapes and
     // arguments repeat (inputs change only inside the pinned staging block)
