@@ -31,6 +31,7 @@ from __future__ import annotations
 import ctypes as C
 import math
 import os
+import sys
 import threading
 import time
 import weakref
@@ -873,9 +874,12 @@ class _Arena:
     B * path_capacity (virtual memory: only the rows a batch writes are ever
     touched).  The BatchResult built on it keeps views and owns it; a later
     call reuses it only after that result is gone (no copy-out, no fresh
-    page faults per call)."""
+    page faults per call).  "Gone" includes every view of the buffers a
+    caller kept (``r.rows``, ``r.codes``, ... outliving ``r``): each view holds
+    a reference to its buffer, so the buffers' reference counts must be back
+    at their resting values before the arena is handed out again."""
 
-    __slots__ = ("res", "offsets", "paths", "srcs", "owner")
+    __slots__ = ("res", "offsets", "paths", "srcs", "owner", "_rest")
 
     def __init__(self, B, pc, n):
         self.res = (_lib.Result * B)()
@@ -883,6 +887,15 @@ class _Arena:
         self.paths = np.empty((B * pc, n))
         self.srcs = np.empty(B * pc, np.int32)
         self.owner = None
+        self._rest = self._refs()
+
+    def _refs(self):
+        return (sys.getrefcount(self.res), sys.getrefcount(self.offsets), sys.getrefcount(self.paths),
+                sys.getrefcount(self.srcs))
+
+    def free(self) -> bool:
+        """No owner alive and no outstanding view of any buffer."""
+        return (self.owner is None or self.owner() is None) and self._refs() == self._rest
 
 
 def _arena(B, pc, n) -> _Arena:
@@ -891,7 +904,7 @@ def _arena(B, pc, n) -> _Arena:
         pools = _TLS.arenas = {}
     pool = pools.setdefault((B, pc, n), [])
     for a in pool:
-        if a.owner is None or a.owner() is None:
+        if a.free():
             a.owner = None
             return a
     a = _Arena(B, pc, n)

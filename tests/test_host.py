@@ -95,3 +95,33 @@ def test_plan_race_argument_checks():
         plan_race(prob, devices=())
     with pytest.raises(ValueError):
         plan_race(prob, devices=tuple(range(9)))
+
+
+def test_batch_arena_reused_only_without_live_views():
+    """A result arena goes back to plan_many only when its BatchResult and
+    every view a caller kept of its buffers (rows, codes, ...) are gone."""
+    import gc
+    from paper_2505_06791_b200 import planner as P
+    B, pc, n = 3, 4, 2
+    key = (B, pc, n)
+
+    def result():
+        a = P._arena(B, pc, n)
+        a.offsets[:] = 0
+        st = np.zeros((B, n))
+        return a, P._batch_result(a, a.res, a.offsets, a.paths[:0], a.srcs[:0], st, st, 0.0, B, pc)
+
+    P._TLS.arenas = {}
+    a1, r1 = result()
+    assert P._arena(B, pc, n) is not a1          # owned by a live result
+    P._TLS.arenas = {key: [a1]}
+    codes, rows = r1.codes, r1.rows
+    del r1
+    gc.collect()
+    assert not a1.free()                         # views still alive
+    assert P._arena(B, pc, n) is not a1
+    P._TLS.arenas = {key: [a1]}
+    del codes, rows
+    gc.collect()
+    assert a1.free()
+    assert P._arena(B, pc, n) is a1
