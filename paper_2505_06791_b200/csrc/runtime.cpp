@@ -1583,7 +1583,15 @@ static int wait_results(Ctx* c, int B) {
         if (all) break;
         if ((spin & 4095) == 0) {
             const cudaError_t e = c->plan_lean ? cudaStreamQuery(c->stream) : cudaEventQuery(c->ev[3]);
-            if (e == cudaSuccess) break;
+            if (e == cudaSuccess) {
+                // the launch is complete, so its mapped-memory stores are
+                // visible: words still from an earlier call mean a result
+                // that was never written -- never hand that back as this call's
+                for (int i = 0; i < B; i++)
+                    if (out[i].done_seq != seq || out[i].chk_seq != seq)
+                        return fail(CPRRTC_ECUDA, "launch completed without writing its results");
+                break;
+            }
             if (e != cudaErrorNotReady)
                 return fail(CPRRTC_ECUDA, std::string("kernel failed: ") + cudaGetErrorString(e));
         }
