@@ -40,6 +40,9 @@
 #ifndef CP_ROOT_FIRST
 #define CP_ROOT_FIRST 1              // single query: the first extension's nearest node is the root
 #endif
+#ifndef CP_SPEC_JUNC
+#define CP_SPEC_JUNC 1               // pair mode: the junction runs while C certifies the meeting motion
+#endif
 #ifndef CP_NN_PAIRS
 #define CP_NN_PAIRS 1                // planner NN: two chunks per L2 round trip
 #endif
@@ -2134,6 +2137,18 @@ enum { PF_LAUNCH_NS = 0, PF_TOTAL, PF_PROJ, PF_PITER, PF_WAIT, PF_NN, PF_SAMPLE,
 // out statically (team k draws k + 1; the shared counter then continues
 // above n_teams), and no stop poll before it -- a team's first extension
 // starts without an L2 round trip.
+// junction (planner.py:466-481): the edge between q_new (tree a) and the meet
+// node of tree b, derived start side -> goal side
+__device__ __forceinline__ bool cp_junction(const Team& tm, TeamWS& ws, const PlanArgs& A, const SceneSm& sc, int a,
+                                            const float* q_new, const float* q_meet, Stats& st, const int* stop) {
+    const float* js = a == 0 ? q_new : q_meet;
+    const float* jg = a == 0 ? q_meet : q_new;
+    if (cp_vec_equal(tm, js, jg)) return true;
+    cp_copy(tm, ws.qr, js);
+    cp_copy(tm, ws.qn, jg);
+    return cp_derive_edge(tm, ws, A, sc, ws.qr, ws.qn, st, stop);
+}
+
 __device__ void cp_plan_query_pair(const Team& tm, TeamWS& ws, TeamWS& wsc, PairBox& bx, const PlanArgs& A,
                                    const SceneSm& sc, int qi, int first_it, int n_teams) {
     QueryState& Q = A.qs[qi];
@@ -2231,7 +2246,17 @@ __device__ void cp_plan_query_pair(const Team& tm, TeamWS& ws, TeamWS& wsc, Pair
         int prev = -1;          // node of the last accepted connect motion
         bool pending_con = false;
         bool over = false;      // C saw the stop word set (after its last check)
+        // Speculative junction: the meet node's coordinates are known before C
+        // accepts the motion that creates it (C appends exactly the posted
+        // endpoint; an existing node's come from the NN), so P derives the
+        // junction edge while C certifies, instead of after C's verdict.  Its
+        // verdict counts only if C accepts (the reference's order of effects
+        // on the trees is unchanged).  -1: not run.
+        int spec = -1;
         if (dist <= A.tol) {
+#if CP_SPEC_JUNC
+            spec = cp_junction(tm, ws, A, sc, a, ws.qt, ws.qc, st, &Q.stop) ? 1 : 0;
+#endif
             node = cp_pair_result(tm, bx, over);
             pending_ext = false;
             if (node == -4) full = true;
@@ -2283,6 +2308,9 @@ __device__ void cp_plan_query_pair(const Team& tm, TeamWS& ws, TeamWS& wsc, Pair
                 dist = nd;
                 CP_PF_ADD(PF_WAIT, t_w2);
                 if (dist <= A.tol) {
+#if CP_SPEC_JUNC
+                    spec = cp_junction(tm, ws, A, sc, a, ws.qt, ws.qc, st, &Q.stop) ? 1 : 0;
+#endif
                     CP_PF_T0(t_w3); CP_TL(11);
                     const int r = cp_pair_result(tm, bx, over);
                     CP_PF_ADD(PF_WAIT, t_w3);
@@ -2313,14 +2341,12 @@ __device__ void cp_plan_query_pair(const Team& tm, TeamWS& ws, TeamWS& wsc, Pair
         if (node < 0 || meet < 0) continue;
         CP_PF_T0(t_j); CP_TL(12);
         // junction (planner.py:466-481): q_new (tree a) against the meet node (tree b)
-        cp_load_node(tm, A, qi, b, meet, ws.qm);
-        const float* js = a == 0 ? ws.qt : ws.qm;
-        const float* jg = a == 0 ? ws.qm : ws.qt;
-        bool ok = cp_vec_equal(tm, js, jg);
-        if (!ok) {
-            cp_copy(tm, ws.qr, js);
-            cp_copy(tm, ws.qn, jg);
-            ok = cp_derive_edge(tm, ws, A, sc, ws.qr, ws.qn, st, &Q.stop);
+        bool ok;
+        if (spec >= 0) {
+            ok = spec != 0;
+        } else {
+            cp_load_node(tm, A, qi, b, meet, ws.qm);
+            ok = cp_junction(tm, ws, A, sc, a, ws.qt, ws.qm, st, &Q.stop);
         }
         CP_PF_ADD(PF_JUNC, t_j);
         if (ok) {
