@@ -40,6 +40,9 @@
 #ifndef CP_ROOT_FIRST
 #define CP_ROOT_FIRST 1              // single query: the first extension's nearest node is the root
 #endif
+#ifndef CP_ROOT_FIRST_CONNECT
+#define CP_ROOT_FIRST_CONNECT 0      // single query: round 0's connect starts at tree b's root too (A/B knob)
+#endif
 #ifndef CP_SPEC_JUNC
 #define CP_SPEC_JUNC 1               // pair mode: the junction runs while C certifies the meeting motion
 #endif
@@ -2237,7 +2240,17 @@ __device__ void cp_plan_query_pair(const Team& tm, TeamWS& ws, TeamWS& wsc, Pair
         // greedy connect of tree b toward q_new while C certifies the extension
         cp_copy(tm, ws.qt, ws.qe);
         int cnt_b;
-        int icur = cp_nearest_ld(tm, cp_tree(A, qi, b), A.cap, &Q.count[b], ws.qt, ws.qc, &cnt_b);
+        int icur;
+#if CP_ROOT_FIRST_CONNECT
+        if (round == 0 && first_it > 0) {   // as for the extension: tree b's root, no L2 round trip
+            if ((int)tm.lane < CP_N)
+                ws.qc[tm.lane] = (float)(b == 0 ? A.chk.starts : A.chk.goals)[tm.lane];
+            tm.sync();
+            icur = 0;
+            cnt_b = 1;
+        } else
+#endif
+            icur = cp_nearest_ld(tm, cp_tree(A, qi, b), A.cap, &Q.count[b], ws.qt, ws.qc, &cnt_b);
         st.v[ST_NNODES] += cnt_b;
         float dist = cp_vec_dist(tm, ws.qc, ws.qt);
         CP_PF_ADD(PF_NN, t_nn2);
