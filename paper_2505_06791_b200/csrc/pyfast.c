@@ -112,6 +112,11 @@ static PyObject* fast_plan_one(PyObject* self, PyObject* const* args, Py_ssize_t
     PyTuple_SET_ITEM(stats, 9, PyLong_FromLong(r->nodes_goal));
     PyTuple_SET_ITEM(stats, 10, PyFloat_FromDouble(r->device_ms));
     for (int k = 8; k < 12; k++) PyTuple_SET_ITEM(stats, 3 + k, PyLong_FromUnsignedLongLong(st[k]));
+    for (int k = 0; k < 15; k++)
+        if (!PyTuple_GET_ITEM(stats, k)) {   /* an allocation failed: no tuple with holes */
+            Py_DECREF(stats);
+            return NULL;
+        }
 
     PyObject* path = Py_None;
     PyObject* sources = Py_None;
@@ -161,6 +166,10 @@ static PyObject* fast_plan_one(PyObject* self, PyObject* const* args, Py_ssize_t
     PyTuple_SET_ITEM(out, 3, stats);
     PyTuple_SET_ITEM(out, 4, path);
     PyTuple_SET_ITEM(out, 5, sources);
+    if (!PyTuple_GET_ITEM(out, 0) || !PyTuple_GET_ITEM(out, 1) || !PyTuple_GET_ITEM(out, 2)) {
+        Py_DECREF(out);
+        return NULL;
+    }
     return out;
 }
 
