@@ -164,7 +164,9 @@ CPRRTC_API int64_t cprrtc_launch_count(void *ctx);
  * lean graph records no events): the planner's own clock, init -> the result
  * complete / init -> solved.  cprrtc_plan returns for a single query as soon
  * as its result is complete (completion words in mapped memory), before the
- * planner grid retires; later calls on the context are stream-ordered. */
+ * planner grid retires; later calls on the context are stream-ordered.  A
+ * launch that completes without writing its completion words is an error
+ * (CPRRTC_ECUDA), never a stale result. */
 CPRRTC_API int cprrtc_last_timing(void *ctx, double *total_ms, double *plan_kernel_ms);
 /* overwrite `bytes` of device scratch (L2 flush between timed iterations) */
 CPRRTC_API int cprrtc_flush_l2(void *ctx, size_t bytes);
