@@ -43,9 +43,6 @@
 #ifndef CP_ROOT_FIRST_CONNECT
 #define CP_ROOT_FIRST_CONNECT 0      // single query: round 0's connect starts at tree b's root too (A/B knob)
 #endif
-#ifndef CP_DEFER_WAIT
-#define CP_DEFER_WAIT 0              // single query: P warps wait for the init grid only after their first projection (A/B knob)
-#endif
 #ifndef CP_SPEC_JUNC
 #define CP_SPEC_JUNC 1               // pair mode: the junction runs while C certifies the meeting motion
 #endif
@@ -2156,22 +2153,9 @@ __device__ __forceinline__ bool cp_junction(const Team& tm, TeamWS& ws, const Pl
 }
 
 __device__ void cp_plan_query_pair(const Team& tm, TeamWS& ws, TeamWS& wsc, PairBox& bx, const PlanArgs& A,
-                                   const SceneSm& sc, int qi, int first_it, int n_teams, bool joined = true) {
+                                   const SceneSm& sc, int qi, int first_it, int n_teams) {
     QueryState& Q = A.qs[qi];
     Stats st;
-    // joined == false (CP_DEFER_WAIT): this warp has not yet waited for the
-    // init grid (griddepcontrol.wait) nor counted itself into Q.active; round
-    // 0's sample, root NN, steer and P1 projection touch no query state (the
-    // stop word they poll was cleared by the previous run's reset kernel), so
-    // the wait moves behind that projection, before any query-state access
-    auto join = [&]() {
-        if (!joined) {
-            asm volatile("griddepcontrol.wait;" ::: "memory");
-            if (tm.lane == 0) atomicAdd(&Q.active, 1);
-            tm.sync();
-            joined = true;
-        }
-    };
     const int W = A.W;
 #ifdef CP_PROFILE
     u64 pf[ST_NSTAT] = {};
@@ -2192,7 +2176,6 @@ __device__ void cp_plan_query_pair(const Team& tm, TeamWS& ws, TeamWS& wsc, Pair
         // counters go to the query every round: a solved query's result
         // carries the work finished by the time it was solved (the solving
         // team finalises it at once, without waiting for the others to leave)
-        if (round > 0 || !(first_it > 0 && A.budget_ns >= 0)) join();
         if (round > 0) cp_flush_stats(tm, Q, st);
         CP_PF_T0(t_stop); CP_TL(1);
         if (!(round == 0 && first_it > 0 && A.budget_ns >= 0) && cp_should_stop(tm, Q, A)) { CP_WHY(0); break; }
@@ -2204,7 +2187,6 @@ __device__ void cp_plan_query_pair(const Team& tm, TeamWS& ws, TeamWS& wsc, Pair
             it = tm.bcast(it, 0);
         }
         if (it > A.max_iterations) {
-            join();
             if (tm.lane == 0) atomicExch(&Q.exhausted, 1);
             break;
         }
@@ -2234,10 +2216,7 @@ __device__ void cp_plan_query_pair(const Team& tm, TeamWS& ws, TeamWS& wsc, Pair
             cnt_a = 1;
         } else
 #endif
-        {
-            join();
             inear = cp_nearest_ld(tm, cp_tree(A, qi, a), A.cap, &Q.count[a], ws.qr, ws.qn, &cnt_a);
-        }
         st.v[ST_NNODES] += cnt_a;
         cp_steer(tm, ws.qn, ws.qr, A.step, ws.qs);
         if (cp_vec_equal(tm, ws.qs, ws.qn)) continue;
@@ -2246,7 +2225,6 @@ __device__ void cp_plan_query_pair(const Team& tm, TeamWS& ws, TeamWS& wsc, Pair
         int pit, ppr;
         CP_PF_T0(t_p1); CP_TL(4);
         bool okp = cp_project(tm, ws.seg, W, A.pa, &pit, &ppr, nullptr, nullptr, &st.v[ST_STAGE1], &Q.stop, ws.poll);
-        join();
         CP_PF_ADD(PF_PROJ, t_p1);
         CP_PF_INC(PF_NPROJ, 1);
         CP_PF_INC(PF_PITER, pit > 0 ? pit : 0);
@@ -2424,7 +2402,6 @@ __device__ void cp_plan_query_pair(const Team& tm, TeamWS& ws, TeamWS& wsc, Pair
             break;
         }
     }
-    join();
     if (tm.lane == 0) {
 #pragma unroll
         for (int i = 0; i < ST_NSTAT; i++)
@@ -2844,15 +2821,8 @@ cp_plan_kernel(const __grid_constant__ PlanArgs A) {
     }
     // launched as a programmatic dependent of cp_init_kernel: the scene staging
     // and first samples above overlapped it; query state, trees and queue
-    // counters are read only after its writes (a no-op in a plain launch).
-    // CP_DEFER_WAIT: a single query's P warps wait inside round 0 instead
-    // (cp_plan_query_pair's join), after their first projection
-#if CP_DEFER_WAIT && !defined(CP_PROFILE) && !defined(CP_TIMELINE)
-    const bool defer = single && A.pair && !((threadIdx.x >> 5) & 1) && A.budget_ns >= 0;
-#else
-    const bool defer = false;
-#endif
-    if (!defer) asm volatile("griddepcontrol.wait;" ::: "memory");
+    // counters are read only after its writes (a no-op in a plain launch)
+    asm volatile("griddepcontrol.wait;" ::: "memory");
     if (A.pair) {   // pair mailboxes live in shared memory: set them up before any warp uses one
         for (int w = 2 * threadIdx.x; w < (int)(blockDim.x >> 5); w += 2 * blockDim.x) {
             PairBox* b = cp_pair_box(&wsa[w * (32 / CP_G) + 1]);
@@ -2918,10 +2888,9 @@ cp_plan_kernel(const __grid_constant__ PlanArgs A) {
         }
         if (qi < 0 || ++visits > 4 * A.nq + 4) break;
         QueryState& Q = A.qs[qi];
-        if (!defer && tm.lane == 0) atomicAdd(&Q.active, 1);
+        if (tm.lane == 0) atomicAdd(&Q.active, 1);
         const int first = single ? gteam + 1 : 0;
-        if (bx) cp_plan_query_pair(tm, ws, wsa[((threadIdx.x >> 5) + 1) * (32 / CP_G)], *bx, A, sc, qi, first, n_teams,
-                                   !defer);
+        if (bx) cp_plan_query_pair(tm, ws, wsa[((threadIdx.x >> 5) + 1) * (32 / CP_G)], *bx, A, sc, qi, first, n_teams);
         else cp_plan_query(tm, ws, A, sc, qi, first, n_teams);
         // the last team to leave the query extracts its result (a late
         // joiner may extract again: identical values)
