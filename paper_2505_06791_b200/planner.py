@@ -514,9 +514,15 @@ class PlanStream:
     ``depth`` batches are in flight and a batch's slowest queries overlap the
     next batch's start (a persistent launch ends with its last query; its
     finished teams free their SMs for the next launch).  Results come back in
-    submission order; each is exactly the batch plan_many would return."""
+    submission order; each is exactly the batch plan_many would return.
+    ``close()`` (or leaving a ``with`` block, or garbage collection) drains
+    the batches still in flight and hands the stream's context slots to the
+    next stream, so streams created one after another reuse their device
+    contexts instead of accumulating them."""
 
     _instances = 0
+    _free_bases: list = []
+    _slot_lock = threading.Lock()
 
     def __init__(self, model, scene, spec, params: PlanParams = PlanParams(),
                  options: DeviceOptions = DeviceOptions(), depth: int = 2):
@@ -526,8 +532,12 @@ class PlanStream:
         self._prm = _make_params(params, options)
         self._auto_teams = options.teams == 0
         self._pc = int(self._prm.path_capacity)
-        PlanStream._instances += 1      # private contexts for every stream
-        base = 1000 + 8 * PlanStream._instances
+        with PlanStream._slot_lock:     # private contexts for every live stream
+            if PlanStream._free_bases:
+                base = PlanStream._free_bases.pop()
+            else:
+                PlanStream._instances += 1
+                base = 1000 + 8 * PlanStream._instances
         self._ctxs = [kernels.context(model, options.device, slot=base + k) for k in range(depth)]
         for c in self._ctxs:
             with c.lock:
@@ -538,6 +548,33 @@ class PlanStream:
         self._next = 0
         self._inflight: dict = {}   # ticket -> (ctx, B, starts, goals, arena, t0): submitted, not collected
         self._ready: dict = {}      # ticket -> BatchResult: collected, not yet handed out
+        self._finalizer = weakref.finalize(self, PlanStream._release, base, self._inflight)
+        self._finalizer.atexit = False   # no device calls during interpreter shutdown
+
+    @staticmethod
+    def _release(base, inflight):
+        # drain: a context holds one batch in flight and refuses the next
+        # submit until it is collected (cprrtc_plan_submit)
+        for ctx, B, _s, _g, arena, _t0 in list(inflight.values()):
+            with ctx.lock:
+                ctx.L.cprrtc_plan_wait(ctx.h, B, arena.res, _lib.ptr(arena.offsets, _lib._lp), _lib.ptr(arena.paths),
+                                       _lib.ptr(arena.srcs, _lib._ip), C.c_int64(arena.srcs.shape[0]))
+            arena.owner = None
+        inflight.clear()
+        with PlanStream._slot_lock:
+            PlanStream._free_bases.append(base)
+
+    def close(self) -> None:
+        """Drain the batches still in flight and release the context slots
+        (results not collected yet are dropped)."""
+        self._ready.clear()
+        self._finalizer()
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *exc):
+        self.close()
 
     def submit(self, starts, goals, seed_offsets) -> int:
         """Launch one batch; returns its ticket.  Blocks only when the context
@@ -551,6 +588,8 @@ class PlanStream:
             raise ValueError(f"starts / goals must be (B, {self._n}) and seed_offsets (B,), B >= 1")
         if (seeds < 0).any():
             raise ValueError("seed_offset must be >= 0")
+        if not self._finalizer.alive:
+            raise RuntimeError("PlanStream is closed")
         t = self._next
         prev = t - len(self._ctxs)
         if prev in self._inflight:

@@ -352,6 +352,35 @@ def test_plan_stream_batches(oracle):
                                   _lib.ptr(srcs, _lib._ip), C.c_int64(1024 * 1024)) == 0
 
 
+def test_plan_stream_close_drains_and_reuses_contexts():
+    """A stream closed (or dropped) with batches in flight drains them, and
+    the next stream takes over its context slots: the same contexts, ready
+    for a fresh submit (no context per stream left behind)."""
+    import gc
+
+    import bench
+    from paper_2505_06791_b200.planner import PlanParams, PlanStream
+    m, sc, sp = fx.robot("arm7"), fx.scene("table"), fx.spec("table_plane")
+    prm = PlanParams(width=16, max_iterations=300)
+    with PlanStream(m, sc, sp, prm, depth=2) as a:
+        a.submit(*bench.batch_arrays(0))
+        a.submit(*bench.batch_arrays(1))     # both contexts busy at close
+        ctxs = list(a._ctxs)
+    with pytest.raises(RuntimeError):
+        a.submit(*bench.batch_arrays(2))
+    b = PlanStream(m, sc, sp, prm, depth=2)
+    assert b._ctxs == ctxs
+    r = b.result(b.submit(*bench.batch_arrays(3)))
+    assert r.solved.mean() > 0.97
+    b.submit(*bench.batch_arrays(4))         # in flight when dropped
+    del b
+    gc.collect()
+    c = PlanStream(m, sc, sp, prm, depth=2)
+    assert c._ctxs == ctxs
+    assert c.result(c.submit(*bench.batch_arrays(5))).solved.mean() > 0.97
+    c.close()
+
+
 def test_fast_and_ctypes_single_query_paths(oracle):
     """plan() goes through the CPython fast path (csrc/pyfast.c) when the
     inputs are float64 C-contiguous and through ctypes otherwise; both give
