@@ -586,7 +586,7 @@ def other_configs(args, local):
     for name in OTHER:
         label, probs = _cfg_problems(name)
         # configs[2] ablations: early-exit flag on/off x broad phase (auto: on
-        # from 32 primitives) / the reference's lockstep check order
+        # whenever the scene has obstacles) / the reference's lockstep check order
         variants = ((("on", -1, ""), ("off", -1, " (cc flag off)"), ("on", 0, " (lockstep order)"),
                      ("off", 0, " (lockstep order, cc flag off)"))
                     if name.startswith("configs[2]") else (("on", -1, ""),))
